@@ -1,0 +1,181 @@
+/*
+ * parsweep_b200 — C ABI of the B200-native batched dichotomy tridiagonal
+ * solver (Terekhov, arXiv:0901.2859). Drop-in for the hot path of the
+ * reference `parsweep` library: one-time setup on the matrix, then the
+ * batched solve of A X_k = F_k for many right-hand sides.
+ *
+ * Plain pointers and sizes only; no CUDA, torch or C++ types cross this
+ * boundary (streams are passed as `void*` = cudaStream_t). Reference paths
+ * below are relative to parsweep/ in the reference tree
+ * (proj/include/parsweep/). Every call is thread-safe; a plan is immutable
+ * after creation and may be used concurrently from several streams.
+ *
+ * Storage layouts of the right-hand-side / solution series (N systems of
+ * order n, element (row i, rhs k), 0-based):
+ *   PSW_LAYOUT_R  "RHS-contiguous":    F[i * ld + k], ld >= N
+ *   PSW_LAYOUT_S  "system-contiguous": F[k * ld + i], ld >= n   (the reference's
+ *                 own layout: each std::vector<double> is one system,
+ *                 dichotomy/batch.hpp:57-60)
+ */
+#ifndef PARSWEEP_B200_H
+#define PARSWEEP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSW_ABI_VERSION 1
+
+/* Status codes. The C++ wrapper (parsweep_b200.hpp) maps them back onto the
+ * reference exception types of core/errors.hpp:9-62. */
+typedef enum psw_status {
+    PSW_OK = 0,
+    PSW_INVALID_ARGUMENT = 1, /* std::invalid_argument: tridiag.hpp:57-66, partition.hpp:31-42 */
+    PSW_PIVOT_BREAKDOWN = 2,  /* PivotBreakdown(row): thomas.hpp:14,32,38; row in last_error_index */
+    PSW_TOO_MANY_PES = 3,     /* TooManyPEs: decompose.hpp:34-35 */
+    PSW_NOT_SUPPORTED = 4,    /* e.g. non-symmetric A (Symmetrize route, preliminary.hpp:111-132) */
+    PSW_CUDA_ERROR = 5,
+    PSW_NCCL_ERROR = 6,
+    PSW_OUT_OF_MEMORY = 7
+} psw_status;
+
+typedef enum psw_dtype { PSW_F64 = 0, PSW_F32 = 1 } psw_dtype;
+typedef enum psw_layout { PSW_LAYOUT_R = 0, PSW_LAYOUT_S = 1 } psw_layout;
+
+/* Solve-path selection (psw_solve_ex). AUTO picks the fastest path that
+ * supports the plan/shape: FUSED keeps every RHS tile resident on chip and
+ * reads F once; STAGED is the general three-kernel path. */
+typedef enum psw_path { PSW_PATH_AUTO = 0, PSW_PATH_STAGED = 1, PSW_PATH_FUSED = 2 } psw_path;
+
+typedef struct psw_plan psw_plan;
+
+/* Description of a created plan (psw_plan_info). */
+typedef struct psw_plan_info_t {
+    int64_t n;              /* order */
+    int64_t p;              /* interior boundaries (partition.hpp:20), P = p + 1 blocks */
+    int32_t dtype;          /* psw_dtype */
+    int32_t device;         /* CUDA ordinal */
+    int32_t uniform;        /* 1 if the partition is decompose(n, p+1).induced_partition() */
+    int32_t fused_ok;       /* 1 if the fused on-chip path supports this plan (layout R) */
+    int64_t device_bytes;   /* resident preliminary bytes in HBM */
+    int64_t combine_terms;  /* WorkCounters::combine_terms of one RHS (boundary_solve.hpp:18-34) */
+    int64_t comm_rounds;    /* RunStats::comm_rounds (run.hpp:93-94) */
+    double setup_seconds;   /* host time of the preliminary phase */
+    double max_z_norm;      /* PreliminaryData::max_z_norm (preliminary.hpp:75-83) */
+} psw_plan_info_t;
+
+/* ---- errors ------------------------------------------------------------ */
+/* Message and index (row for PIVOT_BREAKDOWN) of the last failing call on
+ * the calling thread. */
+const char* psw_last_error_message(void);
+int64_t psw_last_error_index(void);
+int psw_abi_version(void);
+
+/* ---- partition helpers ------------------------------------------------ */
+/* Replaces runtime/decompose.hpp:33-47 + Decomposition::induced_partition
+ * (:23-29): writes the P-1 one-based interior boundaries of the near-equal
+ * split of n rows into P ranges. PSW_TOO_MANY_PES if n < 2P. */
+int psw_decompose(int64_t n, int64_t P, int64_t* boundaries_out);
+
+/* Replaces Partition::validate (dichotomy/partition.hpp:31-42). */
+int psw_partition_validate(int64_t n, int64_t p, const int64_t* boundaries);
+
+/* ---- setup ------------------------------------------------------------ */
+/* Replaces compute_preliminary(A, part, GRowStrategy::Auto, exec)
+ * (dichotomy/preliminary.hpp:171-199) for symmetric A (sub == super,
+ * tridiag.hpp:43 -> DirectSymmetric route :110-112). `sub`/`sup` hold n-1
+ * entries (a_2..a_n / c_1..c_{n-1}), `diag` n entries, all host fp64 (the
+ * reference's TridiagMatrix, tridiag.hpp:31-34). `boundaries` are the p
+ * one-based interior rows of the reference `Partition` (partition.hpp:16-18).
+ * The preliminary is computed in fp64 on the host, reduced to what the
+ * per-RHS kernels read, and uploaded to `device` (dtype = PSW_F64 or
+ * PSW_F32 for the solve arithmetic). Fails with PSW_PIVOT_BREAKDOWN exactly
+ * where the reference's preliminary would throw. */
+int psw_plan_create(psw_plan** out, int64_t n, const double* sub, const double* diag,
+                    const double* sup, int64_t p, const int64_t* boundaries, int dtype,
+                    int device);
+int psw_plan_destroy(psw_plan* plan);
+int psw_plan_info(const psw_plan* plan, psw_plan_info_t* info);
+
+/* ---- batched solve ---------------------------------------------------- */
+/* Replaces the per-RHS loop of solve_batch (dichotomy/batch.hpp:67-73) over
+ * solve_with_preliminary_into (batch.hpp:20-51): solves all `nrhs` systems
+ * whose right-hand sides are in F (device memory, plan dtype) and writes the
+ * solutions to X (device). Asynchronous on `stream` (cudaStream_t, NULL =
+ * legacy default stream). F == X with ldf == ldx is allowed (in place). */
+int psw_solve(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
+              int64_t nrhs, int layout, void* stream);
+
+/* Extended solve: explicit path, and optional device outputs of the
+ * per-RHS intermediates for parity checks — betas_left/right ((p+1) x nrhs,
+ * fp64, [t * nrhs + k], as BetaSet betas.hpp:20-23) and boundary values
+ * (p x nrhs, fp64, [j * nrhs + k], as solve_boundaries boundary_solve.hpp:96).
+ * Intermediates are only produced by the STAGED path. */
+typedef struct psw_solve_opts {
+    int32_t path;            /* psw_path */
+    int32_t nevents;         /* entries in `events` (0 = none) */
+    double* betas_left;      /* device, optional */
+    double* betas_right;     /* device, optional */
+    double* boundary_values; /* device, optional */
+    void** events;           /* optional cudaEvent_t[nevents]: events[i] is recorded on the
+                                stream before kernel i of the path and events[L] after the
+                                last of its L kernels (per-kernel timing, bench.py) */
+} psw_solve_opts;
+int psw_solve_ex(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
+                 int64_t nrhs, int layout, void* stream, const psw_solve_opts* opts);
+
+/* End-to-end variant of solve_batch (batch.hpp:57-75) on HOST buffers: the
+ * series is copied to the device in RHS chunks, solved and copied back, with
+ * copies of chunk c+1 / c-1 overlapping the solve of chunk c. Blocking.
+ * Pinned host memory gives full PCIe/C2C bandwidth. */
+int psw_solve_host(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
+                   int64_t nrhs, int layout);
+
+/* Device kernels launched by the last successful psw_solve* on this thread
+ * (launch accounting for the benchmark). */
+int64_t psw_last_launch_count(void);
+
+/* ---- multi-GPU row sharding (dichotomy across devices) ---------------- */
+/* The reference simulates message passing (runtime/run.hpp:30-35,93-94);
+ * here each rank owns a contiguous slab of blocks of one global partition
+ * and the only exchange is a sum of per-RHS coarse partial sums. Protocol:
+ *   psw_shard_plan_create  (every rank, same global A and partition)
+ *   psw_shard_forward      -> local forward sweep, writes d0 into X and the
+ *                             coarse partial sums into `partials` (device,
+ *                             psw_shard_partials_count(plan) * nrhs fp64)
+ *   <all-reduce(sum) of `partials` across ranks: NCCL / torch.distributed>
+ *   psw_shard_backward     -> coarse + local dichotomy and back substitution.
+ * Rank r owns blocks [r*P/G, (r+1)*P/G) (P = p+1 must be divisible by G, both
+ * powers of two), i.e. rows of those blocks; F/X hold only the owned rows
+ * (row offset psw_shard_row_offset). */
+int psw_shard_plan_create(psw_plan** out, int64_t n, const double* sub, const double* diag,
+                          const double* sup, int64_t p, const int64_t* boundaries, int dtype,
+                          int device, int rank, int world);
+int64_t psw_shard_partials_count(const psw_plan* plan);
+int64_t psw_shard_row_offset(const psw_plan* plan);
+int64_t psw_shard_rows(const psw_plan* plan);
+int psw_shard_forward(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
+                      int64_t nrhs, double* partials, void* stream);
+int psw_shard_backward(const psw_plan* plan, void* X, int64_t ldx, int64_t nrhs,
+                       const double* partials, void* stream);
+
+/* ---- utilities (benchmark / test data) -------------------------------- */
+/* Fill a device buffer with the seeded counter-based uniform generator
+ * u_i = (splitmix64(seed ^ (offset + i)) >> 11) * 2^-53, v = lo + (hi-lo) u
+ * (SURVEY.md §8(d)); bitwise identical to the host generator for fp64. */
+int psw_fill_uniform(void* dst, int dtype, int64_t count, uint64_t seed, uint64_t offset,
+                     double lo, double hi, void* stream);
+/* Standard normal via Box-Muller on pairs of the same uniform stream. */
+int psw_fill_normal(void* dst, int dtype, int64_t count, uint64_t seed, uint64_t offset,
+                    void* stream);
+/* Write `bytes` of zeros+index pattern over a scratch buffer (L2 flush). */
+int psw_l2_flush(void* scratch, int64_t bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PARSWEEP_B200_H */

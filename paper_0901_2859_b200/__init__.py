@@ -1,0 +1,437 @@
+"""parsweep_b200 — B200-native batched dichotomy tridiagonal solver.
+
+Python mirror of the reference `parsweep` hot-path API (C++20 header-only,
+/root/reference/proj/include/parsweep) over the C ABI in
+include/parsweep_b200.h. Names, argument meaning and error behaviour follow
+the reference so parity tests read like its own tests:
+
+    reference (C++)                              this package
+    -------------------------------------------  ---------------------------------
+    TridiagMatrix (core/tridiag.hpp:31-67)       TridiagMatrix
+    Partition (dichotomy/partition.hpp:16-73)    Partition
+    decompose(n,p).induced_partition()           decompose(n, P).induced_partition()
+      (runtime/decompose.hpp:23-47)
+    compute_preliminary(A, part)                 compute_preliminary(A, part, dtype=, device=)
+      (dichotomy/preliminary.hpp:171-199)          -> Plan (resident in HBM)
+    solve_with_preliminary_into / solve_batch    Plan.solve(F, X) on CUDA tensors,
+      (dichotomy/batch.hpp:20-75)                  solve_batch(A, part, series) on host data
+    SolverError, PivotBreakdown, TooManyPEs      same names (core/errors.hpp:9-62)
+
+The product path is the CUDA library only: there is no CPU fallback, and
+every call fails loudly when the extension or a GPU is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+__all__ = [
+    "TridiagMatrix", "Partition", "Decomposition", "decompose", "compute_preliminary", "Plan",
+    "solve_batch", "SolverError", "PivotBreakdown", "TooManyPEs", "NotSupported", "CudaError",
+    "F64", "F32", "LAYOUT_R", "LAYOUT_S", "PATH_AUTO", "PATH_STAGED", "PATH_FUSED", "lib",
+    "library_path",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libparsweep_b200.so")
+
+F64, F32 = 0, 1
+LAYOUT_R, LAYOUT_S = 0, 1
+PATH_AUTO, PATH_STAGED, PATH_FUSED = 0, 1, 2
+OK, INVALID_ARGUMENT, PIVOT_BREAKDOWN, TOO_MANY_PES, NOT_SUPPORTED, CUDA_ERROR, NCCL_ERROR, OOM = range(8)
+
+
+# ---------------------------------------------------------------- errors
+class SolverError(RuntimeError):
+    """core/errors.hpp:9-12"""
+
+
+class PivotBreakdown(SolverError):
+    """core/errors.hpp:16-22 — carries the failing row."""
+
+    def __init__(self, row: int, msg: str | None = None):
+        super().__init__(msg or f"pivot breakdown during forward elimination at row {row}")
+        self.row = row
+
+
+class TooManyPEs(SolverError):
+    """core/errors.hpp:42-47"""
+
+
+class NotSupported(SolverError):
+    pass
+
+
+class CudaError(SolverError):
+    pass
+
+
+# ---------------------------------------------------------------- library
+_lib = None
+
+
+def library_path() -> str:
+    return LIB_PATH
+
+
+def lib() -> C.CDLL:
+    """Load the in-tree CUDA library; raises if it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `make -C paper_0901_2859_b200/csrc` "
+                "(or __graft_entry__.build()); there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        d, i64, vp = C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_void_p
+        L.psw_last_error_message.restype = C.c_char_p
+        L.psw_last_error_index.restype = C.c_int64
+        L.psw_last_launch_count.restype = C.c_int64
+        L.psw_decompose.argtypes = [C.c_int64, C.c_int64, i64]
+        L.psw_partition_validate.argtypes = [C.c_int64, C.c_int64, i64]
+        L.psw_plan_create.argtypes = [C.POINTER(vp), C.c_int64, d, d, d, C.c_int64, i64, C.c_int, C.c_int]
+        L.psw_shard_plan_create.argtypes = [C.POINTER(vp), C.c_int64, d, d, d, C.c_int64, i64,
+                                            C.c_int, C.c_int, C.c_int, C.c_int]
+        L.psw_plan_destroy.argtypes = [vp]
+        L.psw_plan_info.argtypes = [vp, vp]
+        L.psw_solve.argtypes = [vp, vp, C.c_int64, vp, C.c_int64, C.c_int64, C.c_int, vp]
+        L.psw_solve_ex.argtypes = [vp, vp, C.c_int64, vp, C.c_int64, C.c_int64, C.c_int, vp, vp]
+        L.psw_solve_host.argtypes = [vp, vp, C.c_int64, vp, C.c_int64, C.c_int64, C.c_int]
+        L.psw_shard_partials_count.argtypes = [vp]
+        L.psw_shard_partials_count.restype = C.c_int64
+        L.psw_shard_row_offset.argtypes = [vp]
+        L.psw_shard_row_offset.restype = C.c_int64
+        L.psw_shard_rows.argtypes = [vp]
+        L.psw_shard_rows.restype = C.c_int64
+        L.psw_shard_forward.argtypes = [vp, vp, C.c_int64, vp, C.c_int64, C.c_int64, vp, vp]
+        L.psw_shard_backward.argtypes = [vp, vp, C.c_int64, C.c_int64, vp, vp]
+        L.psw_fill_uniform.argtypes = [vp, C.c_int, C.c_int64, C.c_uint64, C.c_uint64, C.c_double,
+                                       C.c_double, vp]
+        L.psw_fill_normal.argtypes = [vp, C.c_int, C.c_int64, C.c_uint64, C.c_uint64, vp]
+        L.psw_l2_flush.argtypes = [vp, C.c_int64, vp]
+        _lib = L
+    return _lib
+
+
+def _raise(rc: int):
+    L = lib()
+    msg = (L.psw_last_error_message() or b"").decode()
+    idx = int(L.psw_last_error_index())
+    if rc == INVALID_ARGUMENT:
+        raise ValueError(msg)  # std::invalid_argument
+    if rc == PIVOT_BREAKDOWN:
+        raise PivotBreakdown(idx, msg)
+    if rc == TOO_MANY_PES:
+        raise TooManyPEs(msg)
+    if rc == NOT_SUPPORTED:
+        raise NotSupported(msg)
+    if rc == OOM:
+        raise MemoryError(msg)
+    raise CudaError(f"status {rc}: {msg}")
+
+
+def _check(rc: int):
+    if rc != OK:
+        _raise(rc)
+
+
+def last_launch_count() -> int:
+    return int(lib().psw_last_launch_count())
+
+
+# ---------------------------------------------------------------- types
+@dataclass
+class TridiagMatrix:
+    """core/tridiag.hpp:31-67: sub = a_2..a_n, diag = b_1..b_n, super = c_1..c_{n-1}."""
+
+    sub: np.ndarray
+    diag: np.ndarray
+    super: np.ndarray
+
+    def __post_init__(self):
+        self.sub = np.ascontiguousarray(self.sub, dtype=np.float64)
+        self.diag = np.ascontiguousarray(self.diag, dtype=np.float64)
+        self.super = np.ascontiguousarray(self.super, dtype=np.float64)
+
+    def n(self) -> int:
+        return int(self.diag.size)
+
+    def is_symmetric(self) -> bool:  # tridiag.hpp:43 (exact compare)
+        return bool(np.array_equal(self.sub, self.super))
+
+    @staticmethod
+    def constant(n: int, a: float, b: float, c: float) -> "TridiagMatrix":
+        return TridiagMatrix(np.full(n - 1, a), np.full(n, b), np.full(n - 1, c))
+
+    @staticmethod
+    def symmetric(a: np.ndarray, b: np.ndarray) -> "TridiagMatrix":
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        return TridiagMatrix(a, b, a.copy())
+
+    def validate(self):  # tridiag.hpp:57-66
+        n = self.n()
+        if n < 2:
+            raise ValueError("TridiagMatrix: order must be >= 2")
+        if self.sub.size != n - 1 or self.super.size != n - 1:
+            raise ValueError("TridiagMatrix: off-diagonal lengths must be n-1")
+        if not (np.isfinite(self.sub).all() and np.isfinite(self.diag).all() and np.isfinite(self.super).all()):
+            raise ValueError("TridiagMatrix: entries must be finite")
+
+    def mat_vec(self, x: np.ndarray) -> np.ndarray:  # tridiag.hpp:70-80
+        y = self.diag * x
+        y[1:] += self.sub * x[:-1]
+        y[:-1] += self.super * x[1:]
+        return y
+
+
+@dataclass
+class Partition:
+    """dichotomy/partition.hpp:16-73 — 1-based interior boundaries."""
+
+    n: int
+    boundaries: list[int] = field(default_factory=list)
+
+    def p(self) -> int:
+        return len(self.boundaries)
+
+    def blocks(self) -> int:
+        return len(self.boundaries) + 1
+
+    def block_begin(self, t: int) -> int:
+        return 1 if t == 0 else self.boundaries[t - 1]
+
+    def block_end(self, t: int) -> int:
+        return self.n + 1 if t == self.p() else self.boundaries[t]
+
+    def validate(self):
+        b = np.ascontiguousarray(self.boundaries, dtype=np.int64)
+        _check(lib().psw_partition_validate(self.n, b.size, b.ctypes.data_as(C.POINTER(C.c_int64))))
+
+    def to_string(self) -> str:
+        return ",".join(str(b) for b in self.boundaries)
+
+    @staticmethod
+    def parse(n: int, text: str) -> "Partition":
+        items = []
+        for item in text.split(","):
+            if not item.strip():
+                continue
+            try:
+                v = int(item)
+            except ValueError:
+                raise ValueError(f"Partition: bad boundary '{item}'") from None
+            if v < 0:
+                raise ValueError(f"Partition: bad boundary '{item}'")
+            items.append(v)
+        part = Partition(n, items)
+        part.validate()
+        return part
+
+
+@dataclass
+class Decomposition:
+    """runtime/decompose.hpp:16-30"""
+
+    n: int
+    ranges: list[tuple[int, int]]
+
+    def p(self) -> int:
+        return len(self.ranges)
+
+    def induced_partition(self) -> Partition:
+        return Partition(self.n, [hi for (_, hi) in self.ranges[:-1]])
+
+
+def decompose(n: int, P: int) -> Decomposition:
+    """runtime/decompose.hpp:33-47 via psw_decompose (raises TooManyPEs)."""
+    b = np.zeros(max(P - 1, 1), np.int64)
+    _check(lib().psw_decompose(n, P, b.ctypes.data_as(C.POINTER(C.c_int64))))
+    ends = list(b[: P - 1]) + [n]
+    ranges, lo = [], 1
+    for hi in ends:
+        ranges.append((lo, int(hi)))
+        lo = int(hi) + 1
+    return Decomposition(n, ranges)
+
+
+class _Info(C.Structure):
+    _fields_ = [("n", C.c_int64), ("p", C.c_int64), ("dtype", C.c_int32), ("device", C.c_int32),
+                ("uniform", C.c_int32), ("fused_ok", C.c_int32), ("device_bytes", C.c_int64),
+                ("combine_terms", C.c_int64), ("comm_rounds", C.c_int64),
+                ("setup_seconds", C.c_double), ("max_z_norm", C.c_double)]
+
+
+class _Opts(C.Structure):
+    _fields_ = [("path", C.c_int32), ("nevents", C.c_int32), ("betas_left", C.c_void_p),
+                ("betas_right", C.c_void_p), ("boundary_values", C.c_void_p),
+                ("events", C.c_void_p)]
+
+
+def _ptr(t) -> int:
+    """Device (or host) address of a torch tensor / numpy array / int."""
+    if t is None:
+        return 0
+    if isinstance(t, int):
+        return t
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return int(t.data_ptr())
+
+
+class Plan:
+    """Device-resident preliminary data (the PreliminaryData of
+    dichotomy/preliminary.hpp:53-101, restricted to what the kernels read)."""
+
+    def __init__(self, A: TridiagMatrix, part: Partition, dtype: int = F64, device: int = 0,
+                 rank: int = 0, world: int = 1):
+        L = lib()
+        A.validate() if A.n() >= 2 else None
+        self.n = A.n()
+        self.part = Partition(part.n, list(part.boundaries))
+        self.dtype = dtype
+        self.device = device
+        self.rank, self.world = rank, world
+        b = np.ascontiguousarray(part.boundaries, dtype=np.int64)
+        if b.size == 0:
+            b = np.zeros(1, np.int64)
+        dp = C.POINTER(C.c_double)
+        h = C.c_void_p()
+        args = (C.byref(h), self.n, A.sub.ctypes.data_as(dp), A.diag.ctypes.data_as(dp),
+                A.super.ctypes.data_as(dp), len(part.boundaries),
+                b.ctypes.data_as(C.POINTER(C.c_int64)), dtype, device)
+        if world == 1:
+            _check(L.psw_plan_create(*args))
+        else:
+            _check(L.psw_shard_plan_create(*args, rank, world))
+        self._h = h
+        info = _Info()
+        _check(L.psw_plan_info(self._h, C.byref(info)))
+        self.info = {k: getattr(info, k) for k, _ in _Info._fields_}
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                lib().psw_plan_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def p(self) -> int:
+        return self.part.p()
+
+    # -- device-resident batched solve (psw_solve / psw_solve_ex) ----------
+    def solve(self, F, X=None, *, nrhs: int | None = None, layout: int = LAYOUT_R,
+              ldf: int | None = None, ldx: int | None = None, stream=None, path: int = PATH_AUTO,
+              betas_left=None, betas_right=None, boundary_values=None, events=None):
+        """Solve A X_k = F_k for every RHS in F (a CUDA tensor of the plan's
+        dtype). layout R: F is (n, N) row-major [i*ld + k]; layout S: F is
+        (N, n) [k*ld + i]. X defaults to F (in place)."""
+        if X is None:
+            X = F
+        if nrhs is None:
+            nrhs = F.shape[1] if layout == LAYOUT_R else F.shape[0]
+        if ldf is None:
+            ldf = F.stride(0)
+        if ldx is None:
+            ldx = X.stride(0)
+        s = _stream_ptr(stream)
+        opts = None
+        if (path != PATH_AUTO or betas_left is not None or betas_right is not None
+                or boundary_values is not None or events is not None):
+            ev_arr = None
+            if events is not None:
+                ev_arr = (C.c_void_p * len(events))(*[e.cuda_event if hasattr(e, "cuda_event") else int(e)
+                                                      for e in events])
+            opts = _Opts(path, len(events) if events is not None else 0, _ptr(betas_left) or None,
+                         _ptr(betas_right) or None, _ptr(boundary_values) or None,
+                         C.cast(ev_arr, C.c_void_p) if ev_arr is not None else None)
+            self._ev_keepalive = ev_arr
+        rc = lib().psw_solve_ex(self._h, _ptr(F), ldf, _ptr(X), ldx, nrhs, layout, s,
+                                C.byref(opts) if opts is not None else None)
+        _check(rc)
+        return X
+
+    def solve_host(self, F: np.ndarray, X: np.ndarray | None = None, layout: int = LAYOUT_S):
+        """End-to-end solve on host arrays (psw_solve_host)."""
+        dt = np.float64 if self.dtype == F64 else np.float32
+        if F.dtype != dt or not F.flags.c_contiguous:
+            raise ValueError("F must be a C-contiguous array of the plan dtype")
+        if X is None:
+            X = np.empty_like(F)
+        nrhs = F.shape[1] if layout == LAYOUT_R else F.shape[0]
+        _check(lib().psw_solve_host(self._h, F.ctypes.data, F.shape[1], X.ctypes.data, X.shape[1],
+                                    nrhs, layout))
+        return X
+
+    # -- row sharding (psw_shard_*) -----------------------------------------
+    def partials_count(self) -> int:
+        return int(lib().psw_shard_partials_count(self._h))
+
+    def row_offset(self) -> int:
+        return int(lib().psw_shard_row_offset(self._h))
+
+    def rows(self) -> int:
+        return int(lib().psw_shard_rows(self._h))
+
+    def shard_forward(self, F, X, partials, nrhs: int, stream=None):
+        _check(lib().psw_shard_forward(self._h, _ptr(F), F.stride(0), _ptr(X), X.stride(0), nrhs,
+                                       _ptr(partials), _stream_ptr(stream)))
+
+    def shard_backward(self, X, partials, nrhs: int, stream=None):
+        _check(lib().psw_shard_backward(self._h, _ptr(X), X.stride(0), nrhs, _ptr(partials),
+                                        _stream_ptr(stream)))
+
+
+def _stream_ptr(stream) -> int | None:
+    if stream is None:
+        try:
+            import torch
+            return torch.cuda.current_stream().cuda_stream
+        except Exception:
+            return None
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def compute_preliminary(A: TridiagMatrix, part: Partition, dtype: int = F64, device: int = 0) -> Plan:
+    """dichotomy/preliminary.hpp:171-199 -> device-resident Plan."""
+    return Plan(A, part, dtype=dtype, device=device)
+
+
+def solve_batch(A: TridiagMatrix, part: Partition, rhs_series: Sequence[Sequence[float]],
+                dtype: int = F64, device: int = 0) -> list[np.ndarray]:
+    """dichotomy/batch.hpp:57-75 on host data: validate, preliminary once,
+    then the whole series on the GPU (psw_solve_host, layout S)."""
+    part.validate()
+    plan = Plan(A, part, dtype=dtype, device=device)
+    dt = np.float64 if dtype == F64 else np.float32
+    F = np.ascontiguousarray(np.asarray(rhs_series, dtype=dt).reshape(len(rhs_series), A.n()))
+    X = plan.solve_host(F, layout=LAYOUT_S)
+    return [X[k] for k in range(X.shape[0])]
+
+
+def fill_uniform(t, seed: int, lo: float, hi: float, offset: int = 0, stream=None):
+    """Seeded uniform fill of a CUDA tensor (SURVEY.md §8(d) generator)."""
+    dt = F64 if str(t.dtype) == "torch.float64" else F32
+    _check(lib().psw_fill_uniform(_ptr(t), dt, t.numel(), seed, offset, lo, hi, _stream_ptr(stream)))
+    return t
+
+
+def fill_normal(t, seed: int, offset: int = 0, stream=None):
+    dt = F64 if str(t.dtype) == "torch.float64" else F32
+    _check(lib().psw_fill_normal(_ptr(t), dt, t.numel(), seed, offset, _stream_ptr(stream)))
+    return t
+
+
+def l2_flush(t, stream=None):
+    _check(lib().psw_l2_flush(_ptr(t), t.numel() * t.element_size(), _stream_ptr(stream)))

@@ -1,0 +1,115 @@
+// Internal declarations shared by the host setup (psw_plan.cpp) and the CUDA
+// solve paths (psw_staged.cu, psw_fused.cu). Not part of the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "parsweep_b200.h"
+
+namespace psw {
+
+// ---- error plumbing (thread-local last error, psw_last_error_*) ----------
+void set_error(int code, const std::string& msg, int64_t index = -1);
+int clear_error();
+int cuda_fail(cudaError_t e, const char* what);
+void note_launches(int64_t k);   // accumulate per-call kernel launch count
+void reset_launches();
+
+#define PSW_CUDA_TRY(expr)                                   \
+    do {                                                     \
+        cudaError_t _e = (expr);                             \
+        if (_e != cudaSuccess) return ::psw::cuda_fail(_e, #expr); \
+    } while (0)
+
+// ---- per-row local sweep coefficients ------------------------------------
+// Block t (0-based) owns rows [s_t, e_t) (0-based) = the reference half-open
+// block [n_t, n_{t+1}) (partition.hpp:26-29). Its closed sweep block ends at
+// h_t = e_t (t < p, the next boundary row) or n-1 (t = p)
+// (local_solve.hpp:29-31). With the unit first row (t > 0) carrying the
+// unknown boundary value x_l, the sweep of local_solve.hpp:39-48 /
+// thomas.hpp:31-44 is affine in x_l:
+//   forward   d_q = f_q * rp_q + ma_q * d_{q-1}          (d at the unit row = 0)
+//   betas     bR += f_q * gR_q,  bL += f_q * gL_q         (betas.hpp:42-57)
+//   backward  x_q = d_q + x_l * w_q + al_q * x_{q+1}       (x_{h_t} = x_r given)
+// rp = 1/pivot, ma = -a_q/pivot, al = -c_q/pivot, w_q = ma_q w_{q-1}, w = 1 at
+// the unit row; gR = row r_t of inv(A), gL = row r_{t-1} of inv(A) on block t.
+template <typename T>
+struct alignas(4 * sizeof(T)) FwdCoef {
+    T rp, ma, gr, gl;
+};
+template <typename T>
+struct alignas(2 * sizeof(T)) BwdCoef {
+    T w, al;
+};
+
+// One dichotomy item in level order (boundary_solve.hpp:104-119): the
+// boundary index i and its nearest already-known neighbours kl < i < kr
+// (sentinels -1 and p).
+struct CombineItem {
+    int32_t i, kl, kr, pad;
+};
+
+}  // namespace psw
+
+// The plan: immutable after psw_plan_create.
+struct psw_plan {
+    int64_t n = 0, p = 0, P = 1;
+    int dtype = PSW_F64;
+    int device = 0;
+    bool uniform = false;
+    int64_t m = 0;  // rows per range when uniform (n / P)
+    std::vector<int64_t> bnd;          // 1-based boundaries (reference Partition)
+    std::vector<int32_t> blk;          // [2t] = s_t, [2t+1] = e_t (0-based, owned rows)
+    std::vector<psw::CombineItem> items;
+    psw_plan_info_t info{};
+
+    // device-resident preliminary
+    void* d_fwd = nullptr;   // FwdCoef<T>[n]
+    void* d_bwd = nullptr;   // BwdCoef<T>[n]
+    int32_t* d_blk = nullptr;
+    double* d_zr = nullptr;  // p x p samples ZR[j][i] (preliminary.hpp:69)
+    double* d_zl = nullptr;  // p x p samples ZL[j][i] (preliminary.hpp:71)
+    psw::CombineItem* d_items = nullptr;
+
+    // multi-GPU row shard (psw_shard_*); world == 1 for a full plan
+    int rank = 0, world = 1;
+    int64_t blk0 = 0, blk1 = 0;   // owned blocks [blk0, blk1)
+    int64_t row0 = 0, row1 = 0;   // owned rows [row0, row1) (0-based, global)
+    int64_t ncoarse = 0;          // coarse boundaries (world - 1)
+    int64_t npartials = 0;        // partial sums per RHS exchanged
+    // per coarse partial-sum slot: (segment kl, kr, target e); device copy
+    std::vector<int32_t> partial_spec;  // 3 * npartials
+    int32_t* d_partial_spec = nullptr;
+    // coarse items and local items of this rank (level order)
+    std::vector<psw::CombineItem> coarse_items, local_items;
+    psw::CombineItem* d_coarse_items = nullptr;
+    psw::CombineItem* d_local_items = nullptr;
+    int32_t* d_partial_index = nullptr;  // per coarse item: slots of its 3 sums
+};
+
+namespace psw {
+// Solve paths (psw_staged.cu / psw_fused.cu). All asynchronous on `s`.
+int solve_staged(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
+                 int64_t N, int layout, cudaStream_t s, double* ext_bl, double* ext_br,
+                 double* ext_v, void** events, int nevents);
+bool fused_supported(const psw_plan* plan, int layout, int64_t N);
+int solve_fused(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
+                int64_t N, int layout, cudaStream_t s, void** events, int nevents);
+// records events[i] (if present) on s
+inline void mark(void** events, int nevents, int i, cudaStream_t s) {
+    if (events && i < nevents && events[i]) cudaEventRecord(static_cast<cudaEvent_t>(events[i]), s);
+}
+int shard_forward(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
+                  int64_t N, double* partials, cudaStream_t s);
+int shard_backward(const psw_plan* plan, void* X, int64_t ldx, int64_t N, const double* partials,
+                   cudaStream_t s);
+int fill_uniform(void* dst, int dtype, int64_t count, uint64_t seed, uint64_t offset, double lo,
+                 double hi, cudaStream_t s);
+int fill_normal(void* dst, int dtype, int64_t count, uint64_t seed, uint64_t offset,
+                cudaStream_t s);
+int l2_flush(void* scratch, int64_t bytes, cudaStream_t s);
+}  // namespace psw

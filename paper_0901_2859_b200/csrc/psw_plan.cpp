@@ -1,0 +1,598 @@
+// Host side of the C ABI: validation, the fp64 preliminary phase, upload of
+// the block-restricted data to HBM, and the public entry points.
+//
+// The preliminary mirrors compute_preliminary (dichotomy/preliminary.hpp:
+// 171-199, DirectSymmetric route :139-143) operation for operation — this
+// file is compiled with -ffp-contract=off so the inverse rows and Z samples
+// are bitwise what the reference computes — but keeps only what the per-RHS
+// kernels read: each inverse row restricted to its two adjacent blocks, the
+// p x p Z-sample tables, and per-row sweep coefficients (psw_internal.h).
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <thread>
+
+#include "psw_internal.h"
+
+namespace psw {
+
+namespace {
+thread_local std::string t_msg;
+thread_local int64_t t_index = -1;
+thread_local int64_t t_launches = 0;
+constexpr double kPivotFloor = 1e-300;  // core/thomas.hpp:14
+}  // namespace
+
+void set_error(int code, const std::string& msg, int64_t index) {
+    (void)code;
+    t_msg = msg;
+    t_index = index;
+}
+int clear_error() {
+    t_msg.clear();
+    t_index = -1;
+    return PSW_OK;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+    set_error(PSW_CUDA_ERROR, std::string("CUDA error ") + cudaGetErrorName(e) + " (" +
+                                  cudaGetErrorString(e) + ") in " + what);
+    return e == cudaErrorMemoryAllocation ? PSW_OUT_OF_MEMORY : PSW_CUDA_ERROR;
+}
+void note_launches(int64_t k) { t_launches += k; }
+void reset_launches() { t_launches = 0; }
+
+namespace {
+
+// core/thomas.hpp:22-45, same operation order (no contraction in this TU).
+// Returns -1 on success or the failing (local) row.
+int64_t thomas(int64_t n, const double* sub, const double* diag, const double* sup,
+               const double* f, double* x, double* al, double* be) {
+    double piv = diag[0];
+    if (std::fabs(piv) < kPivotFloor) return 0;
+    al[0] = (n > 1) ? -sup[0] / piv : 0.0;
+    be[0] = f[0] / piv;
+    for (int64_t i = 1; i < n; ++i) {
+        piv = diag[i] + sub[i - 1] * al[i - 1];
+        if (std::fabs(piv) < kPivotFloor) return i;
+        al[i] = (i + 1 < n) ? -sup[i] / piv : 0.0;
+        be[i] = (f[i] - sub[i - 1] * be[i - 1]) / piv;
+    }
+    x[n - 1] = be[n - 1];
+    for (int64_t i = n - 1; i-- > 0;) x[i] = be[i] + al[i] * x[i + 1];
+    return -1;
+}
+
+// Forward pivots only (for p == 0 the reference fails in the first solve's
+// sweep of A itself, local_solve.hpp:49 -> thomas.hpp:32,38).
+int64_t forward_breakdown(int64_t n, const double* sub, const double* diag, const double* sup) {
+    double piv = diag[0];
+    if (std::fabs(piv) < kPivotFloor) return 0;
+    double al = (n > 1) ? -sup[0] / piv : 0.0;
+    for (int64_t i = 1; i < n; ++i) {
+        piv = diag[i] + sub[i - 1] * al;
+        if (std::fabs(piv) < kPivotFloor) return i;
+        al = (i + 1 < n) ? -sup[i] / piv : 0.0;
+    }
+    return -1;
+}
+
+// dichotomy/level_sets.hpp:18-37 -> level-ordered items with the nearest known
+// neighbours that solve_boundaries finds by scanning (boundary_solve.hpp:106-113).
+std::vector<psw::CombineItem> build_items(int64_t p, int64_t* terms_out) {
+    std::vector<psw::CombineItem> items;
+    if (p == 0) {
+        if (terms_out) *terms_out = 0;
+        return items;
+    }
+    int64_t depth = 1;
+    while ((int64_t{1} << depth) <= p) ++depth;
+    std::vector<char> taken(p + 1, 0), known(p, 0);
+    int64_t terms = 0;
+    for (int64_t l = 1; l <= depth; ++l) {
+        const int64_t stride = int64_t{1} << (depth - l);
+        std::vector<int64_t> level;
+        for (int64_t k = 1; k < (int64_t{1} << l); ++k) {
+            const int64_t j = stride * k;
+            if (j > p) break;
+            if (taken[j]) continue;
+            taken[j] = 1;
+            level.push_back(j);
+        }
+        for (int64_t pos : level) {
+            const int64_t i = pos - 1;
+            int64_t kl = i - 1;
+            while (kl >= 0 && !known[kl]) --kl;
+            int64_t kr = i + 1;
+            while (kr < p && !known[kr]) ++kr;
+            items.push_back({int32_t(i), int32_t(kl), int32_t(kr), 0});
+            // segment_particular counts (e - kl) + (kr - e) terms per call
+            const int64_t per = kr - kl;
+            terms += per * (1 + (kl >= 0) + (kr < p));
+        }
+        for (int64_t pos : level) known[pos - 1] = 1;
+    }
+    if (terms_out) *terms_out = terms;
+    return items;
+}
+
+template <typename T>
+int upload(psw_plan* pl, const std::vector<double>& rp, const std::vector<double>& ma,
+           const std::vector<double>& gr, const std::vector<double>& gl,
+           const std::vector<double>& w, const std::vector<double>& al,
+           const std::vector<double>& zr, const std::vector<double>& zl) {
+    const int64_t n = pl->n, p = pl->p;
+    std::vector<FwdCoef<T>> fwd(n);
+    std::vector<BwdCoef<T>> bwd(n);
+    for (int64_t q = 0; q < n; ++q) {
+        fwd[q] = {T(rp[q]), T(ma[q]), T(gr[q]), T(gl[q])};
+        bwd[q] = {T(w[q]), T(al[q])};
+    }
+    PSW_CUDA_TRY(cudaMalloc(&pl->d_fwd, sizeof(FwdCoef<T>) * n));
+    PSW_CUDA_TRY(cudaMalloc(&pl->d_bwd, sizeof(BwdCoef<T>) * n));
+    PSW_CUDA_TRY(cudaMemcpy(pl->d_fwd, fwd.data(), sizeof(FwdCoef<T>) * n, cudaMemcpyHostToDevice));
+    PSW_CUDA_TRY(cudaMemcpy(pl->d_bwd, bwd.data(), sizeof(BwdCoef<T>) * n, cudaMemcpyHostToDevice));
+    PSW_CUDA_TRY(cudaMalloc(&pl->d_blk, sizeof(int32_t) * pl->blk.size()));
+    PSW_CUDA_TRY(cudaMemcpy(pl->d_blk, pl->blk.data(), sizeof(int32_t) * pl->blk.size(),
+                            cudaMemcpyHostToDevice));
+    int64_t bytes = int64_t(sizeof(FwdCoef<T>) + sizeof(BwdCoef<T>)) * n +
+                    int64_t(sizeof(int32_t) * pl->blk.size());
+    if (p > 0) {
+        PSW_CUDA_TRY(cudaMalloc(&pl->d_zr, sizeof(double) * p * p));
+        PSW_CUDA_TRY(cudaMalloc(&pl->d_zl, sizeof(double) * p * p));
+        PSW_CUDA_TRY(cudaMemcpy(pl->d_zr, zr.data(), sizeof(double) * p * p, cudaMemcpyHostToDevice));
+        PSW_CUDA_TRY(cudaMemcpy(pl->d_zl, zl.data(), sizeof(double) * p * p, cudaMemcpyHostToDevice));
+        PSW_CUDA_TRY(cudaMalloc(&pl->d_items, sizeof(psw::CombineItem) * p));
+        PSW_CUDA_TRY(cudaMemcpy(pl->d_items, pl->items.data(), sizeof(psw::CombineItem) * p,
+                                cudaMemcpyHostToDevice));
+        bytes += int64_t(2 * sizeof(double) * p * p + sizeof(psw::CombineItem) * p);
+    }
+    pl->info.device_bytes = bytes;
+    return PSW_OK;
+}
+
+void free_plan(psw_plan* pl) {
+    if (!pl) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(pl->device);
+    void* ptrs[] = {pl->d_fwd, pl->d_bwd, pl->d_blk, pl->d_zr, pl->d_zl, pl->d_items,
+                    pl->d_partial_spec, pl->d_coarse_items, pl->d_local_items, pl->d_partial_index};
+    for (void* q : ptrs)
+        if (q) cudaFree(q);
+    cudaSetDevice(prev);
+    delete pl;
+}
+
+int validate_inputs(int64_t n, const double* sub, const double* diag, const double* sup,
+                    int64_t p, const int64_t* bnd) {
+    if (n < 2) {
+        set_error(PSW_INVALID_ARGUMENT, "TridiagMatrix: order must be >= 2");
+        return PSW_INVALID_ARGUMENT;
+    }
+    if (n > (int64_t{1} << 30)) {
+        set_error(PSW_INVALID_ARGUMENT, "order exceeds 2^30 rows");
+        return PSW_INVALID_ARGUMENT;
+    }
+    if (!sub || !diag || !sup || (p > 0 && !bnd) || p < 0) {
+        set_error(PSW_INVALID_ARGUMENT, "null matrix or partition pointer");
+        return PSW_INVALID_ARGUMENT;
+    }
+    for (int64_t i = 0; i < n; ++i)
+        if (!std::isfinite(diag[i])) {
+            set_error(PSW_INVALID_ARGUMENT, "TridiagMatrix: entries must be finite");
+            return PSW_INVALID_ARGUMENT;
+        }
+    for (int64_t i = 0; i + 1 < n; ++i)
+        if (!std::isfinite(sub[i]) || !std::isfinite(sup[i])) {
+            set_error(PSW_INVALID_ARGUMENT, "TridiagMatrix: entries must be finite");
+            return PSW_INVALID_ARGUMENT;
+        }
+    return psw_partition_validate(n, p, bnd);
+}
+
+}  // namespace
+
+// Builds the plan for a (possibly sharded) solve. Rank/world select the
+// owned block range for psw_shard_*; world == 1 is the full plan.
+int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
+               const double* sup, int64_t p, const int64_t* bnd, int dtype, int device,
+               int rank, int world);
+
+int build_shard_tables(psw_plan* pl);  // psw_shard.cpp
+
+int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
+               const double* sup, int64_t p, const int64_t* bnd, int dtype, int device,
+               int rank, int world) {
+    clear_error();
+    if (!out) {
+        set_error(PSW_INVALID_ARGUMENT, "null plan output");
+        return PSW_INVALID_ARGUMENT;
+    }
+    *out = nullptr;
+    if (dtype != PSW_F64 && dtype != PSW_F32) {
+        set_error(PSW_INVALID_ARGUMENT, "dtype must be PSW_F64 or PSW_F32");
+        return PSW_INVALID_ARGUMENT;
+    }
+    if (int rc = validate_inputs(n, sub, diag, sup, p, bnd)) return rc;
+    for (int64_t i = 0; i + 1 < n; ++i)
+        if (sub[i] != sup[i]) {
+            set_error(PSW_NOT_SUPPORTED,
+                      "non-symmetric matrix: GRowStrategy Symmetrize/ExplicitInverse/"
+                      "TransposeSolve are not part of the GPU hot path (SURVEY §8 f4)");
+            return PSW_NOT_SUPPORTED;
+        }
+    const auto t0 = std::chrono::steady_clock::now();
+
+    auto* pl = new (std::nothrow) psw_plan();
+    if (!pl) {
+        set_error(PSW_OUT_OF_MEMORY, "host allocation failed");
+        return PSW_OUT_OF_MEMORY;
+    }
+    pl->n = n;
+    pl->p = p;
+    pl->P = p + 1;
+    pl->dtype = dtype;
+    pl->device = device;
+    pl->rank = rank;
+    pl->world = world;
+    pl->bnd.assign(bnd, bnd + p);
+
+    // block ranges (partition.hpp:26-29, 0-based owned rows)
+    pl->blk.resize(2 * pl->P);
+    for (int64_t t = 0; t <= p; ++t) {
+        pl->blk[2 * t] = int32_t(t == 0 ? 0 : bnd[t - 1] - 1);
+        pl->blk[2 * t + 1] = int32_t(t == p ? n : bnd[t] - 1);
+    }
+    pl->uniform = (n % pl->P == 0);
+    if (pl->uniform) {
+        std::vector<int64_t> ref(p);
+        if (p > 0 && psw_decompose(n, pl->P, ref.data()) != PSW_OK) pl->uniform = false;
+        for (int64_t j = 0; pl->uniform && j < p; ++j) pl->uniform = ref[j] == bnd[j];
+        clear_error();
+    }
+    pl->m = pl->uniform ? n / pl->P : 0;
+
+    // ---- preliminary (preliminary.hpp:171-199) --------------------------
+    std::vector<double> gr(n, 0.0), gl(n, 0.0), zr(p * p, 0.0), zl(p * p, 0.0);
+    double max_z = 0.0;
+    if (p == 0) {
+        int64_t bad = forward_breakdown(n, sub, diag, sup);
+        if (bad >= 0) {
+            set_error(PSW_PIVOT_BREAKDOWN,
+                      "pivot breakdown during forward elimination at row " + std::to_string(bad),
+                      bad);
+            delete pl;
+            return PSW_PIVOT_BREAKDOWN;
+        }
+    } else {
+        // boundaries are independent items (preliminary.hpp:182-195); errors
+        // are reported in the serial executor's order (boundary, then g,
+        // z_left, z_right).
+        struct Fail {
+            int64_t j = -1, stage = 0, row = 0;
+        };
+        std::vector<Fail> fails(p);
+        std::vector<std::vector<double>> zl_rows(p), zr_rows(p);  // sampled only
+        std::atomic<int64_t> next{0};
+        std::mutex mz_mu;
+        auto worker = [&]() {
+            std::vector<double> e(n), x(n), al(n), be(n), bd(n), bs(n), bu(n);
+            double mz_local = 0.0;
+            for (;;) {
+                const int64_t j = next.fetch_add(1);
+                if (j >= p) break;
+                const int64_t r = bnd[j];
+                Fail& f = fails[j];
+                // g_j = A^-1 e_r (DirectSymmetric, :139-143), restricted to
+                // blocks j and j+1 (the only rows betas.hpp:46-55 reads)
+                std::fill(e.begin(), e.end(), 0.0);
+                e[r - 1] = 1.0;
+                int64_t bad = thomas(n, sub, diag, sup, e.data(), x.data(), al.data(), be.data());
+                if (bad >= 0) { f = {j, 0, bad}; continue; }
+                for (int32_t q = pl->blk[2 * j]; q < pl->blk[2 * j + 1]; ++q) gr[q] = x[q];
+                for (int32_t q = pl->blk[2 * (j + 1)]; q < pl->blk[2 * (j + 1) + 1]; ++q) gl[q] = x[q];
+                // z_left: b_left_matrix (:29-37), rhs e_last
+                std::copy(diag, diag + r, bd.begin());
+                bd[r - 1] = 1.0;
+                std::copy(sub, sub + (r - 1), bs.begin());
+                bs[r - 2] = 0.0;
+                std::copy(sup, sup + (r - 1), bu.begin());
+                std::fill(e.begin(), e.begin() + r, 0.0);
+                e[r - 1] = 1.0;
+                bad = thomas(r, bs.data(), bd.data(), bu.data(), e.data(), x.data(), al.data(), be.data());
+                if (bad >= 0) { f = {j, 1, bad}; continue; }
+                auto& zlr = zl_rows[j];
+                zlr.resize(j + 1);
+                for (int64_t i = 0; i <= j; ++i) zlr[i] = x[bnd[i] - 1];
+                for (int64_t q = 0; q < r; ++q) mz_local = std::max(mz_local, std::fabs(x[q]));
+                // z_right: b_right_matrix (:41-49), rhs e_first
+                const int64_t m = n - r + 1;
+                std::copy(diag + (r - 1), diag + n, bd.begin());
+                bd[0] = 1.0;
+                std::copy(sub + (r - 1), sub + (n - 1), bs.begin());
+                std::copy(sup + (r - 1), sup + (n - 1), bu.begin());
+                bu[0] = 0.0;
+                std::fill(e.begin(), e.begin() + m, 0.0);
+                e[0] = 1.0;
+                bad = thomas(m, bs.data(), bd.data(), bu.data(), e.data(), x.data(), al.data(), be.data());
+                if (bad >= 0) { f = {j, 2, bad}; continue; }
+                auto& zrr = zr_rows[j];
+                zrr.resize(p - j);
+                for (int64_t i = j; i < p; ++i) zrr[i - j] = x[bnd[i] - r];
+                for (int64_t q = 0; q < m; ++q) mz_local = std::max(mz_local, std::fabs(x[q]));
+            }
+            std::lock_guard<std::mutex> lk(mz_mu);
+            max_z = std::max(max_z, mz_local);
+        };
+        int nth = int(std::min<int64_t>(p, std::max(1u, std::thread::hardware_concurrency())));
+        nth = std::min(nth, 32);
+        std::vector<std::thread> th;
+        for (int w = 1; w < nth; ++w) th.emplace_back(worker);
+        worker();
+        for (auto& t : th) t.join();
+        for (int64_t j = 0; j < p; ++j)
+            if (fails[j].j >= 0) {
+                const int64_t bad = fails[j].row;
+                set_error(PSW_PIVOT_BREAKDOWN,
+                          "pivot breakdown during forward elimination at row " + std::to_string(bad),
+                          bad);
+                delete pl;
+                return PSW_PIVOT_BREAKDOWN;
+            }
+        // build_samples (preliminary.hpp:85-96)
+        for (int64_t j = 0; j < p; ++j) {
+            for (int64_t i = j; i < p; ++i) zr[j * p + i] = zr_rows[j][i - j];
+            for (int64_t i = 0; i <= j; ++i) zl[j * p + i] = zl_rows[j][i];
+        }
+    }
+
+    // ---- per-row sweep coefficients of every block (local_solve.hpp:25-50)
+    std::vector<double> rp(n, 0.0), ma(n, 0.0), w(n, 0.0), alv(n, 0.0);
+    for (int64_t t = 0; t <= p; ++t) {
+        const int64_t s = pl->blk[2 * t], e = pl->blk[2 * t + 1];
+        const int64_t h = (t == p) ? n - 1 : e;  // closed block end
+        double alpha_prev;
+        if (t > 0) {  // unit first row carrying x_{t-1}
+            rp[s] = 0.0;
+            ma[s] = 0.0;
+            w[s] = 1.0;
+            alv[s] = 0.0;
+            alpha_prev = 0.0;
+        } else {
+            const double piv = diag[0];
+            alpha_prev = (h > s) ? -sup[0] / piv : 0.0;
+            rp[s] = 1.0 / piv;
+            ma[s] = 0.0;
+            w[s] = 0.0;
+            alv[s] = alpha_prev;
+        }
+        const int64_t last = (t == p) ? n : e;  // owned rows beyond the first
+        for (int64_t q = s + 1; q < last; ++q) {
+            const double piv = diag[q] + sub[q - 1] * alpha_prev;
+            const double a = (q < h) ? -sup[q] / piv : 0.0;
+            rp[q] = 1.0 / piv;
+            ma[q] = -sub[q - 1] / piv;
+            w[q] = (t > 0) ? ma[q] * w[q - 1] : 0.0;
+            alv[q] = a;
+            alpha_prev = a;
+        }
+    }
+    int64_t terms = 0;
+    pl->items = build_items(p, &terms);
+
+    // the device is only needed for the upload: host validation and the
+    // preliminary (and its PivotBreakdown) come first, like the reference
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        set_error(PSW_CUDA_ERROR, "no CUDA device available (the product has no CPU fallback)");
+        delete pl;
+        return PSW_CUDA_ERROR;
+    }
+    if (device < 0 || device >= ndev) {
+        set_error(PSW_INVALID_ARGUMENT, "device ordinal out of range");
+        delete pl;
+        return PSW_INVALID_ARGUMENT;
+    }
+    int prev_dev = 0;
+    cudaGetDevice(&prev_dev);
+    if (cudaSetDevice(device) != cudaSuccess) {
+        set_error(PSW_CUDA_ERROR, "cudaSetDevice failed");
+        delete pl;
+        return PSW_CUDA_ERROR;
+    }
+    int rc = (dtype == PSW_F64) ? upload<double>(pl, rp, ma, gr, gl, w, alv, zr, zl)
+                                : upload<float>(pl, rp, ma, gr, gl, w, alv, zr, zl);
+    if (rc == PSW_OK && world > 1) rc = build_shard_tables(pl);
+    cudaSetDevice(prev_dev);
+    if (rc != PSW_OK) {
+        free_plan(pl);
+        return rc;
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+    auto& in = pl->info;
+    in.n = n;
+    in.p = p;
+    in.dtype = dtype;
+    in.device = device;
+    in.uniform = pl->uniform ? 1 : 0;
+    in.fused_ok = psw::fused_supported(pl, PSW_LAYOUT_R, 1 << 20) ? 1 : 0;
+    in.combine_terms = terms;
+    int64_t depth = 0;
+    if (p > 0) {
+        depth = 1;
+        while ((int64_t{1} << depth) <= p) ++depth;
+    }
+    in.comm_rounds = p > 0 ? depth + 2 : 0;
+    in.setup_seconds = std::chrono::duration<double>(t1 - t0).count();
+    in.max_z_norm = max_z;
+    *out = pl;
+    return PSW_OK;
+}
+
+void destroy_plan(psw_plan* pl) { free_plan(pl); }
+
+}  // namespace psw
+
+// ============================ C ABI ========================================
+extern "C" {
+
+const char* psw_last_error_message(void) { return psw::t_msg.c_str(); }
+int64_t psw_last_error_index(void) { return psw::t_index; }
+int psw_abi_version(void) { return PSW_ABI_VERSION; }
+int64_t psw_last_launch_count(void) { return psw::t_launches; }
+
+int psw_decompose(int64_t n, int64_t P, int64_t* out) {
+    psw::clear_error();
+    // runtime/decompose.hpp:33-47
+    if (P <= 0 || n < 2 * P) {
+        psw::set_error(PSW_TOO_MANY_PES, "cannot place " + std::to_string(n) + " rows on " +
+                                             std::to_string(P) + " PEs with every range >= 2 rows");
+        return PSW_TOO_MANY_PES;
+    }
+    if (!out && P > 1) {
+        psw::set_error(PSW_INVALID_ARGUMENT, "null output");
+        return PSW_INVALID_ARGUMENT;
+    }
+    const int64_t base = n / P, rem = n % P;
+    int64_t last = 0;
+    for (int64_t i = 0; i + 1 < P; ++i) {
+        last += base + (i < rem ? 1 : 0);
+        out[i] = last;  // induced_partition: right ends but the last (:23-29)
+    }
+    return PSW_OK;
+}
+
+int psw_partition_validate(int64_t n, int64_t p, const int64_t* b) {
+    psw::clear_error();
+    // dichotomy/partition.hpp:31-42
+    if (n < 2) {
+        psw::set_error(PSW_INVALID_ARGUMENT, "Partition: order must be >= 2");
+        return PSW_INVALID_ARGUMENT;
+    }
+    int64_t prev = 0;
+    for (int64_t j = 0; j < p; ++j) {
+        if (b[j] < 2 || b[j] > n - 1) {
+            psw::set_error(PSW_INVALID_ARGUMENT, "Partition: boundary " + std::to_string(b[j]) +
+                                                     " is not interior to 1.." + std::to_string(n),
+                           j);
+            return PSW_INVALID_ARGUMENT;
+        }
+        if (b[j] <= prev) {
+            psw::set_error(PSW_INVALID_ARGUMENT, "Partition: boundaries must be strictly increasing", j);
+            return PSW_INVALID_ARGUMENT;
+        }
+        prev = b[j];
+    }
+    return PSW_OK;
+}
+
+int psw_plan_create(psw_plan** out, int64_t n, const double* sub, const double* diag,
+                    const double* sup, int64_t p, const int64_t* boundaries, int dtype,
+                    int device) {
+    return psw::build_plan(out, n, sub, diag, sup, p, boundaries, dtype, device, 0, 1);
+}
+
+int psw_plan_destroy(psw_plan* plan) {
+    psw::clear_error();
+    psw::destroy_plan(plan);
+    return PSW_OK;
+}
+
+int psw_plan_info(const psw_plan* plan, psw_plan_info_t* info) {
+    psw::clear_error();
+    if (!plan || !info) {
+        psw::set_error(PSW_INVALID_ARGUMENT, "null plan or info");
+        return PSW_INVALID_ARGUMENT;
+    }
+    *info = plan->info;
+    return PSW_OK;
+}
+
+static int check_solve_args(const psw_plan* plan, const void* F, int64_t ldf, const void* X,
+                            int64_t ldx, int64_t nrhs, int layout) {
+    if (!plan) {
+        psw::set_error(PSW_INVALID_ARGUMENT, "null plan");
+        return PSW_INVALID_ARGUMENT;
+    }
+    if (nrhs < 0 || (nrhs > 0 && (!F || !X))) {
+        psw::set_error(PSW_INVALID_ARGUMENT, "invalid right-hand-side buffers");
+        return PSW_INVALID_ARGUMENT;
+    }
+    if (layout != PSW_LAYOUT_R && layout != PSW_LAYOUT_S) {
+        psw::set_error(PSW_INVALID_ARGUMENT, "layout must be PSW_LAYOUT_R or PSW_LAYOUT_S");
+        return PSW_INVALID_ARGUMENT;
+    }
+    const int64_t need = layout == PSW_LAYOUT_R ? nrhs : plan->n;
+    if (ldf < need || ldx < need) {
+        psw::set_error(PSW_INVALID_ARGUMENT, "leading dimension too small for the layout");
+        return PSW_INVALID_ARGUMENT;
+    }
+    if (plan->world != 1) {
+        psw::set_error(PSW_INVALID_ARGUMENT, "sharded plan: use psw_shard_forward/backward");
+        return PSW_INVALID_ARGUMENT;
+    }
+    return PSW_OK;
+}
+
+int psw_solve_ex(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
+                 int64_t nrhs, int layout, void* stream, const psw_solve_opts* opts) {
+    psw::clear_error();
+    psw::reset_launches();
+    if (int rc = check_solve_args(plan, F, ldf, X, ldx, nrhs, layout)) return rc;
+    if (nrhs == 0) return PSW_OK;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != plan->device) PSW_CUDA_TRY(cudaSetDevice(plan->device));
+    auto s = static_cast<cudaStream_t>(stream);
+    int path = opts ? opts->path : PSW_PATH_AUTO;
+    const bool want_intermediates =
+        opts && (opts->betas_left || opts->betas_right || opts->boundary_values);
+    int rc;
+    if (path == PSW_PATH_FUSED && !psw::fused_supported(plan, layout, nrhs)) {
+        psw::set_error(PSW_NOT_SUPPORTED, "fused path does not support this plan/shape");
+        rc = PSW_NOT_SUPPORTED;
+    } else if ((path == PSW_PATH_FUSED || path == PSW_PATH_AUTO) && !want_intermediates &&
+               psw::fused_supported(plan, layout, nrhs)) {
+        rc = psw::solve_fused(plan, F, ldf, X, ldx, nrhs, layout, s, opts ? opts->events : nullptr,
+                              opts ? opts->nevents : 0);
+    } else {
+        rc = psw::solve_staged(plan, F, ldf, X, ldx, nrhs, layout, s,
+                               opts ? opts->betas_left : nullptr,
+                               opts ? opts->betas_right : nullptr,
+                               opts ? opts->boundary_values : nullptr,
+                               opts ? opts->events : nullptr, opts ? opts->nevents : 0);
+    }
+    if (prev != plan->device) cudaSetDevice(prev);
+    return rc;
+}
+
+int psw_solve(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
+              int64_t nrhs, int layout, void* stream) {
+    return psw_solve_ex(plan, F, ldf, X, ldx, nrhs, layout, stream, nullptr);
+}
+
+int psw_fill_uniform(void* dst, int dtype, int64_t count, uint64_t seed, uint64_t offset,
+                     double lo, double hi, void* stream) {
+    psw::clear_error();
+    psw::reset_launches();
+    return psw::fill_uniform(dst, dtype, count, seed, offset, lo, hi,
+                             static_cast<cudaStream_t>(stream));
+}
+
+int psw_fill_normal(void* dst, int dtype, int64_t count, uint64_t seed, uint64_t offset,
+                    void* stream) {
+    psw::clear_error();
+    psw::reset_launches();
+    return psw::fill_normal(dst, dtype, count, seed, offset, static_cast<cudaStream_t>(stream));
+}
+
+int psw_l2_flush(void* scratch, int64_t bytes, void* stream) {
+    psw::clear_error();
+    return psw::l2_flush(scratch, bytes, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,402 @@
+// STAGED solve path: three kernels, any partition, any shape, both layouts.
+//
+//   K1 fwd      one thread per (rhs k, block t): forward sweep of the block's
+//               unit-row system (local_solve.hpp:39-48 + thomas.hpp:31-41 in
+//               the affine form of psw_internal.h) fused with both beta dot
+//               products (betas.hpp:42-57) on the same read of F; the forward
+//               intermediate d0 is parked in X.
+//   K2 combine  one thread per rhs: the dichotomy combination in level order
+//               (boundary_solve.hpp:96-121) -> boundary values V.
+//   K3 bwd      one thread per (rhs k, block t): back substitution with the
+//               boundary values, x = d0 + x_l w + al x_next, in place in X.
+//
+// HBM traffic: F read once, X written twice and read once (d0 round trip):
+// 4 s bytes / unknown; the FUSED path (psw_fused.cu) removes the round trip.
+// Betas and the combination use separately rounded products and sums in the
+// reference's summation order, so betas and boundary values are bitwise the
+// reference's (compiled without FP contraction) for the same inputs.
+#include "psw_internal.h"
+
+namespace psw {
+namespace {
+
+constexpr int kThreads = 128;
+constexpr int kUnroll = 8;
+
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T* p) {
+    return __ldcs(p);  // F is read exactly once: evict-first
+}
+
+// Reference-rounded multiply-add (no contraction): s + a*b.
+__device__ __forceinline__ double madd_rn(double s, double a, double b) {
+    return __dadd_rn(s, __dmul_rn(a, b));
+}
+
+// ---------------------------------------------------------------- layout R
+template <typename T>
+__global__ void __launch_bounds__(kThreads) fwd_r_kernel(
+    const T* F, int64_t ldf, T* X, int64_t ldx, int64_t N, const int32_t* __restrict__ blk,
+    const FwdCoef<T>* __restrict__ cf, double* __restrict__ bl_out, double* __restrict__ br_out,
+    int p) {
+    const int t = blockIdx.y;
+    const int64_t k = int64_t(blockIdx.x) * kThreads + threadIdx.x;
+    if (k >= N) return;
+    const int s = blk[2 * t], e = blk[2 * t + 1];
+    const T* f = F + k;
+    T* x = X + k;
+    T d = T(0);
+    double br = 0.0, bl = 0.0;
+    int q = s;
+    for (; q + kUnroll <= e; q += kUnroll) {
+        T fv[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) fv[u] = ld_stream(f + int64_t(q + u) * ldf);
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const FwdCoef<T> c = cf[q + u];
+            d = fma(c.ma, d, fv[u] * c.rp);
+            br = madd_rn(br, double(fv[u]), double(c.gr));
+            bl = madd_rn(bl, double(fv[u]), double(c.gl));
+            x[int64_t(q + u) * ldx] = d;
+        }
+    }
+    for (; q < e; ++q) {
+        const T fv = ld_stream(f + int64_t(q) * ldf);
+        const FwdCoef<T> c = cf[q];
+        d = fma(c.ma, d, fv * c.rp);
+        br = madd_rn(br, double(fv), double(c.gr));
+        bl = madd_rn(bl, double(fv), double(c.gl));
+        x[int64_t(q) * ldx] = d;
+    }
+    if (t < p) br_out[int64_t(t) * N + k] = br;
+    if (t > 0) bl_out[int64_t(t) * N + k] = bl;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) bwd_r_kernel(
+    T* X, int64_t ldx, int64_t N, const int32_t* __restrict__ blk,
+    const BwdCoef<T>* __restrict__ cb, const double* __restrict__ V, int p) {
+    const int t = blockIdx.y;
+    const int64_t k = int64_t(blockIdx.x) * kThreads + threadIdx.x;
+    if (k >= N) return;
+    const int s = blk[2 * t], e = blk[2 * t + 1];
+    const T xl = t > 0 ? T(V[int64_t(t - 1) * N + k]) : T(0);
+    T xn = t < p ? T(V[int64_t(t) * N + k]) : T(0);
+    T* x = X + k;
+    int q = e - 1;
+    for (; q - kUnroll + 1 >= s; q -= kUnroll) {
+        T dv[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) dv[u] = x[int64_t(q - u) * ldx];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const BwdCoef<T> c = cb[q - u];
+            xn = fma(c.al, xn, fma(xl, c.w, dv[u]));
+            __stcs(x + int64_t(q - u) * ldx, xn);
+        }
+    }
+    for (; q >= s; --q) {
+        const BwdCoef<T> c = cb[q];
+        xn = fma(c.al, xn, fma(xl, c.w, x[int64_t(q) * ldx]));
+        __stcs(x + int64_t(q) * ldx, xn);
+    }
+}
+
+// ---------------------------------------------------------------- layout S
+// One warp per (32 RHS, block): chunks of 32 rows are read coalesced along
+// the system (each RHS contiguous), transposed through shared memory so each
+// lane sweeps its own RHS, and written back the same way.
+constexpr int kWarps = kThreads / 32;
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) fwd_s_kernel(
+    const T* F, int64_t ldf, T* X, int64_t ldx, int64_t N, const int32_t* __restrict__ blk,
+    const FwdCoef<T>* __restrict__ cf, double* __restrict__ bl_out, double* __restrict__ br_out,
+    int p) {
+    __shared__ T tiles[kWarps][32][33];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    T(*tile)[33] = tiles[warp];
+    const int t = blockIdx.y;
+    const int64_t k0 = (int64_t(blockIdx.x) * kWarps + warp) * 32;
+    if (k0 >= N) return;
+    const int nk = int(N - k0 < 32 ? N - k0 : 32);
+    const int s = blk[2 * t], e = blk[2 * t + 1];
+    T d = T(0);
+    double br = 0.0, bl = 0.0;
+    for (int q0 = s; q0 < e; q0 += 32) {
+        const int cnt = e - q0 < 32 ? e - q0 : 32;
+        if (lane < cnt) {
+            const T* src = F + k0 * ldf + q0 + lane;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (j < nk) tile[j][lane] = ld_stream(src + int64_t(j) * ldf);
+        }
+        __syncwarp();
+        if (lane < nk) {
+            for (int r = 0; r < cnt; ++r) {
+                const FwdCoef<T> c = cf[q0 + r];
+                const T fv = tile[lane][r];
+                d = fma(c.ma, d, fv * c.rp);
+                br = madd_rn(br, double(fv), double(c.gr));
+                bl = madd_rn(bl, double(fv), double(c.gl));
+                tile[lane][r] = d;
+            }
+        }
+        __syncwarp();
+        if (lane < cnt) {
+            T* dst = X + k0 * ldx + q0 + lane;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (j < nk) dst[int64_t(j) * ldx] = tile[j][lane];
+        }
+        __syncwarp();
+    }
+    if (lane < nk) {
+        if (t < p) br_out[int64_t(t) * N + k0 + lane] = br;
+        if (t > 0) bl_out[int64_t(t) * N + k0 + lane] = bl;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) bwd_s_kernel(
+    T* X, int64_t ldx, int64_t N, const int32_t* __restrict__ blk,
+    const BwdCoef<T>* __restrict__ cb, const double* __restrict__ V, int p) {
+    __shared__ T tiles[kWarps][32][33];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    T(*tile)[33] = tiles[warp];
+    const int t = blockIdx.y;
+    const int64_t k0 = (int64_t(blockIdx.x) * kWarps + warp) * 32;
+    if (k0 >= N) return;
+    const int nk = int(N - k0 < 32 ? N - k0 : 32);
+    const int s = blk[2 * t], e = blk[2 * t + 1];
+    T xl = T(0), xn = T(0);
+    if (lane < nk) {
+        if (t > 0) xl = T(V[int64_t(t - 1) * N + k0 + lane]);
+        if (t < p) xn = T(V[int64_t(t) * N + k0 + lane]);
+    }
+    for (int q1 = e; q1 > s; q1 -= 32) {
+        const int q0 = q1 - 32 > s ? q1 - 32 : s;
+        const int cnt = q1 - q0;
+        if (lane < cnt) {
+            const T* src = X + k0 * ldx + q0 + lane;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (j < nk) tile[j][lane] = src[int64_t(j) * ldx];
+        }
+        __syncwarp();
+        if (lane < nk) {
+            for (int r = cnt - 1; r >= 0; --r) {
+                const BwdCoef<T> c = cb[q0 + r];
+                xn = fma(c.al, xn, fma(xl, c.w, tile[lane][r]));
+                tile[lane][r] = xn;
+            }
+        }
+        __syncwarp();
+        if (lane < cnt) {
+            T* dst = X + k0 * ldx + q0 + lane;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (j < nk) __stcs(dst + int64_t(j) * ldx, tile[j][lane]);
+        }
+        __syncwarp();
+    }
+}
+
+// --------------------------------------------------------------- combine
+// boundary_solve.hpp:42-55 (segment_particular) with betas [t * N + k].
+__device__ __forceinline__ double seg_sum(const double* __restrict__ bl,
+                                          const double* __restrict__ br, int64_t N, int64_t k,
+                                          const double* __restrict__ zr,
+                                          const double* __restrict__ zl, int p, int kl, int kr,
+                                          int e) {
+    double s = 0.0;
+    for (int t = kl + 1; t <= e; ++t) s = madd_rn(s, br[int64_t(t) * N + k], zr[t * p + e]);
+    for (int t = e + 1; t <= kr; ++t) s = madd_rn(s, bl[int64_t(t) * N + k], zl[(t - 1) * p + e]);
+    return s;
+}
+
+__global__ void __launch_bounds__(kThreads) combine_kernel(
+    const double* __restrict__ bl, const double* __restrict__ br, int64_t N, int p,
+    const CombineItem* __restrict__ items, const double* __restrict__ zr,
+    const double* __restrict__ zl, double* __restrict__ V) {
+    const int64_t k = int64_t(blockIdx.x) * kThreads + threadIdx.x;
+    if (k >= N) return;
+    for (int w = 0; w < p; ++w) {
+        const CombineItem it = items[w];
+        const int i = it.i, kl = it.kl, kr = it.kr;
+        // boundary_solve.hpp:61-88 (segment_component)
+        const double vi = seg_sum(bl, br, N, k, zr, zl, p, kl, kr, i);
+        double v;
+        if (kl >= 0 && kr < p) {
+            const double b1 = __dsub_rn(V[int64_t(kl) * N + k], seg_sum(bl, br, N, k, zr, zl, p, kl, kr, kl));
+            const double b2 = __dsub_rn(V[int64_t(kr) * N + k], seg_sum(bl, br, N, k, zr, zl, p, kl, kr, kr));
+            const double m12 = zl[kr * p + kl];
+            const double m21 = zr[kl * p + kr];
+            const double det = __dsub_rn(1.0, __dmul_rn(m12, m21));
+            const double cl = __ddiv_rn(__dsub_rn(b1, __dmul_rn(m12, b2)), det);
+            const double cr = __ddiv_rn(__dsub_rn(b2, __dmul_rn(m21, b1)), det);
+            v = madd_rn(madd_rn(vi, cl, zr[kl * p + i]), cr, zl[kr * p + i]);
+        } else if (kr < p) {
+            const double cr = __dsub_rn(V[int64_t(kr) * N + k], seg_sum(bl, br, N, k, zr, zl, p, kl, kr, kr));
+            v = madd_rn(vi, cr, zl[kr * p + i]);
+        } else if (kl >= 0) {
+            const double cl = __dsub_rn(V[int64_t(kl) * N + k], seg_sum(bl, br, N, k, zr, zl, p, kl, kr, kl));
+            v = madd_rn(vi, cl, zr[kl * p + i]);
+        } else {
+            v = vi;
+        }
+        V[int64_t(i) * N + k] = v;
+    }
+}
+
+template <typename T>
+int launch_staged(const psw_plan* pl, const void* Fv, int64_t ldf, void* Xv, int64_t ldx,
+                  int64_t N, int layout, cudaStream_t s, double* bl, double* br, double* V,
+                  void** ev, int nev) {
+    const T* F = static_cast<const T*>(Fv);
+    T* X = static_cast<T*>(Xv);
+    const int p = int(pl->p);
+    const auto* cf = static_cast<const FwdCoef<T>*>(pl->d_fwd);
+    const auto* cb = static_cast<const BwdCoef<T>*>(pl->d_bwd);
+    int64_t launches = 0;
+    if (layout == PSW_LAYOUT_R) {
+        dim3 grid(unsigned((N + kThreads - 1) / kThreads), unsigned(pl->P));
+        mark(ev, nev, 0, s);
+        fwd_r_kernel<T><<<grid, kThreads, 0, s>>>(F, ldf, X, ldx, N, pl->d_blk, cf, bl, br, p);
+        ++launches;
+        mark(ev, nev, 1, s);
+        if (p > 0) {
+            combine_kernel<<<grid.x, kThreads, 0, s>>>(bl, br, N, p, pl->d_items, pl->d_zr, pl->d_zl, V);
+            ++launches;
+        }
+        mark(ev, nev, 2, s);
+        bwd_r_kernel<T><<<grid, kThreads, 0, s>>>(X, ldx, N, pl->d_blk, cb, V, p);
+        ++launches;
+        mark(ev, nev, 3, s);
+    } else {
+        dim3 grid(unsigned((N + 32 * kWarps - 1) / (32 * kWarps)), unsigned(pl->P));
+        mark(ev, nev, 0, s);
+        fwd_s_kernel<T><<<grid, kThreads, 0, s>>>(F, ldf, X, ldx, N, pl->d_blk, cf, bl, br, p);
+        ++launches;
+        mark(ev, nev, 1, s);
+        if (p > 0) {
+            combine_kernel<<<unsigned((N + kThreads - 1) / kThreads), kThreads, 0, s>>>(
+                bl, br, N, p, pl->d_items, pl->d_zr, pl->d_zl, V);
+            ++launches;
+        }
+        mark(ev, nev, 2, s);
+        bwd_s_kernel<T><<<grid, kThreads, 0, s>>>(X, ldx, N, pl->d_blk, cb, V, p);
+        ++launches;
+        mark(ev, nev, 3, s);
+    }
+    PSW_CUDA_TRY(cudaGetLastError());
+    note_launches(launches);
+    return PSW_OK;
+}
+
+}  // namespace
+
+int solve_staged(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_t ldx, int64_t N,
+                 int layout, cudaStream_t s, double* ext_bl, double* ext_br, double* ext_v,
+                 void** events, int nevents) {
+    const int64_t P = pl->P, p = pl->p;
+    // scratch: betas (P x N each) and boundary values (p x N), stream-ordered
+    double* bl = ext_bl;
+    double* br = ext_br;
+    double* V = ext_v;
+    void* scratch = nullptr;
+    size_t need = 0;
+    if (!bl) need += sizeof(double) * P * N;
+    if (!br) need += sizeof(double) * P * N;
+    if (!V) need += sizeof(double) * (p > 0 ? p : 1) * N;
+    if (need) {
+        PSW_CUDA_TRY(cudaMallocAsync(&scratch, need, s));
+        char* c = static_cast<char*>(scratch);
+        if (!bl) { bl = reinterpret_cast<double*>(c); c += sizeof(double) * P * N; }
+        if (!br) { br = reinterpret_cast<double*>(c); c += sizeof(double) * P * N; }
+        if (!V) { V = reinterpret_cast<double*>(c); }
+    }
+    int rc = pl->dtype == PSW_F64
+                 ? launch_staged<double>(pl, F, ldf, X, ldx, N, layout, s, bl, br, V, events, nevents)
+                 : launch_staged<float>(pl, F, ldf, X, ldx, N, layout, s, bl, br, V, events, nevents);
+    if (scratch) cudaFreeAsync(scratch, s);
+    return rc;
+}
+
+// ------------------------------------------------------------ data fill
+namespace {
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+__device__ __forceinline__ double unit53(uint64_t seed, uint64_t idx) {
+    return __dmul_rn(double(splitmix64(seed ^ idx) >> 11), 1.0 / 9007199254740992.0);
+}
+
+template <typename T>
+__global__ void fill_uniform_kernel(T* out, int64_t count, uint64_t seed, uint64_t offset,
+                                    double lo, double span) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+         i += int64_t(gridDim.x) * blockDim.x)
+        out[i] = T(__dadd_rn(lo, __dmul_rn(span, unit53(seed, offset + uint64_t(i)))));
+}
+
+template <typename T>
+__global__ void fill_normal_kernel(T* out, int64_t count, uint64_t seed, uint64_t offset) {
+    const int64_t pairs = (count + 1) / 2;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < pairs;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const double u1 = 1.0 - unit53(seed, offset + 2 * uint64_t(i));  // (0, 1]
+        const double u2 = unit53(seed, offset + 2 * uint64_t(i) + 1);
+        const double r = sqrt(-2.0 * log(u1));
+        double sn, cs;
+        sincospi(2.0 * u2, &sn, &cs);
+        out[2 * i] = T(r * cs);
+        if (2 * i + 1 < count) out[2 * i + 1] = T(r * sn);
+    }
+}
+}  // namespace
+
+int fill_uniform(void* dst, int dtype, int64_t count, uint64_t seed, uint64_t offset, double lo,
+                 double hi, cudaStream_t s) {
+    if (!dst || count < 0) {
+        set_error(PSW_INVALID_ARGUMENT, "invalid fill buffer");
+        return PSW_INVALID_ARGUMENT;
+    }
+    if (count == 0) return PSW_OK;
+    const unsigned blocks = 148 * 16;
+    if (dtype == PSW_F64)
+        fill_uniform_kernel<double><<<blocks, 256, 0, s>>>(static_cast<double*>(dst), count, seed, offset, lo, hi - lo);
+    else
+        fill_uniform_kernel<float><<<blocks, 256, 0, s>>>(static_cast<float*>(dst), count, seed, offset, lo, hi - lo);
+    PSW_CUDA_TRY(cudaGetLastError());
+    note_launches(1);
+    return PSW_OK;
+}
+
+int fill_normal(void* dst, int dtype, int64_t count, uint64_t seed, uint64_t offset,
+                cudaStream_t s) {
+    if (!dst || count < 0) {
+        set_error(PSW_INVALID_ARGUMENT, "invalid fill buffer");
+        return PSW_INVALID_ARGUMENT;
+    }
+    if (count == 0) return PSW_OK;
+    const unsigned blocks = 148 * 16;
+    if (dtype == PSW_F64)
+        fill_normal_kernel<double><<<blocks, 256, 0, s>>>(static_cast<double*>(dst), count, seed, offset);
+    else
+        fill_normal_kernel<float><<<blocks, 256, 0, s>>>(static_cast<float*>(dst), count, seed, offset);
+    PSW_CUDA_TRY(cudaGetLastError());
+    note_launches(1);
+    return PSW_OK;
+}
+
+int l2_flush(void* scratch, int64_t bytes, cudaStream_t s) {
+    PSW_CUDA_TRY(cudaMemsetAsync(scratch, 0, size_t(bytes), s));
+    return PSW_OK;
+}
+
+}  // namespace psw
