@@ -147,10 +147,10 @@ def cpu_reference_rate(cfg, budget_s: float, threads: int, max_reps: int = 1000)
     """Reference per-RHS solve (oracle/_ref, the reference compiled) on all
     host threads over disjoint RHS slices; repeats the whole batch until the
     budget is spent. Returns (unknowns/s, sample description, setup s)."""
-    from oracle.pyoracle import Reference, REF_SO
+    from oracle.pyoracle import Reference, REF_SO, REF_PERF_SO
     if not os.path.exists(REF_SO):
         raise RuntimeError("oracle/_ref/libpsw_ref.so missing (built by __graft_entry__.build())")
-    ref = Reference()
+    ref = Reference(REF_PERF_SO if os.path.exists(REF_PERF_SO) else REF_SO)
     a, b, FS = _host_inputs(cfg)
     bnd = ref.decompose(cfg.n, cfg.P)
     N = FS.shape[0]
@@ -173,8 +173,8 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    from oracle.pyoracle import Reference
-    ref = Reference()
+    from oracle.pyoracle import Reference, REF_SO, REF_PERF_SO
+    ref = Reference(REF_PERF_SO if os.path.exists(REF_PERF_SO) else REF_SO)
     a, b, FS = _host_inputs(cfg)
     bnd = ref.decompose(cfg.n, cfg.P)
     N = FS.shape[0]
@@ -214,6 +214,34 @@ def _config_dict(cfg):
 
 
 # ------------------------------------------------------------------ GPU side
+class _Ev:
+    """Raw cudaEvent_t (cuda-python): psw_solve_ex records it between its
+    own kernels on the launching stream."""
+
+    def __init__(self):
+        try:
+            from cuda.bindings import runtime as cudart
+        except ImportError:  # older cuda-python
+            from cuda import cudart
+        self.rt = cudart
+        err, self.ev = cudart.cudaEventCreate()
+        assert int(err) == 0, err
+
+    def __int__(self):
+        return int(self.ev)
+
+    def elapsed_time(self, other: "_Ev") -> float:
+        err, ms = self.rt.cudaEventElapsedTime(self.ev, other.ev)
+        assert int(err) == 0, err
+        return ms
+
+    def __del__(self):
+        try:
+            self.rt.cudaEventDestroy(self.ev)
+        except Exception:  # noqa: BLE001
+            pass
+
+
 def main():
     args = _args()
     from paper_0901_2859_b200.configs import CONFIGS
@@ -274,7 +302,7 @@ def main():
         step()
     torch.cuda.synchronize()
 
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nk + 1)] for _ in range(args.steps)]
+    evs = [[_Ev() for _ in range(nk + 1)] for _ in range(args.steps)]
     if dist:
         dist.barrier()
     torch.cuda.synchronize()

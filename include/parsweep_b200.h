@@ -171,6 +171,11 @@ int psw_fill_uniform(void* dst, int dtype, int64_t count, uint64_t seed, uint64_
 /* Standard normal via Box-Muller on pairs of the same uniform stream. */
 int psw_fill_normal(void* dst, int dtype, int64_t count, uint64_t seed, uint64_t offset,
                     void* stream);
+/* Profiling aid: when `device_buffer` is non-NULL the FUSED kernel writes,
+ * per CTA, 16 uint64 slots: clock64() at its phase boundaries (0..8) and
+ * %globaltimer at start/end (14, 15). NULL disables tracing (default). */
+int psw_debug_trace(void* device_buffer);
+
 /* Write `bytes` of zeros+index pattern over a scratch buffer (L2 flush). */
 int psw_l2_flush(void* scratch, int64_t bytes, void* stream);
 

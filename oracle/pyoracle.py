@@ -18,7 +18,8 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "_build", "libpsw_oracle.so")
-REF_SO = os.path.join(HERE, "_ref", "libpsw_ref.so")
+REF_SO = os.path.join(HERE, "_ref", "libpsw_ref.so")            # parity build (no FP contraction)
+REF_PERF_SO = os.path.join(HERE, "_ref", "libpsw_ref_perf.so")  # CMake Release flags, CPU baseline
 
 OK, INVALID_ARGUMENT, PIVOT_BREAKDOWN, TOO_MANY_PES, NOT_SUPPORTED = 0, 1, 2, 3, 4
 

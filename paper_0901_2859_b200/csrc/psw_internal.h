@@ -42,7 +42,7 @@ struct alignas(4 * sizeof(T)) FwdCoef {
     T rp, ma, gr, gl;
 };
 template <typename T>
-struct alignas(2 * sizeof(T)) BwdCoef {
+struct alignas(16) BwdCoef {  // 16 B rows (TMA bulk-copy granule) for both dtypes
     T w, al;
 };
 
@@ -51,6 +51,28 @@ struct alignas(2 * sizeof(T)) BwdCoef {
 // (sentinels -1 and p).
 struct CombineItem {
     int32_t i, kl, kr, pad;
+};
+
+// FUSED path: every block is cut into S segments of kSegLen rows that are
+// swept by different threads. Within a segment [a, b) the forward recurrence
+// is run from zero (d~) and the true value is d_q = d~_q + mu_q D_{a-1},
+// mu_q = prod_{u=a..q} ma_u; the backward x_q = c_q + al_q x_{q+1},
+// c_q = d_q + x_l w_q, is started from the exact carry x_b obtained by a scan
+// over segment aggregates: x_a = sum_q lam_q c_q + nu x_b with
+// lam_q = prod_{u=a..q-1} al_u, nu = prod_{u=a..b-1} al_u, and
+// sum_q lam_q c_q = Lam + D_{a-1} K1 + x_l K2 (Lam = sum lam_q d~_q is
+// accumulated by the forward sweep, K1 = sum lam mu, K2 = sum lam w).
+constexpr int kSegLen = 32;
+template <typename T>
+struct alignas(16) FusedFwd {
+    T rp, ma, gr, gl, lam, pad;
+};
+template <typename T>
+struct alignas(16) FusedBwd {
+    T mu, w, al, pad;
+};
+struct alignas(32) SegCoef {
+    double mu_end, k1, k2, nu;
 };
 
 }  // namespace psw
@@ -74,6 +96,15 @@ struct psw_plan {
     double* d_zr = nullptr;  // p x p samples ZR[j][i] (preliminary.hpp:69)
     double* d_zl = nullptr;  // p x p samples ZL[j][i] (preliminary.hpp:71)
     psw::CombineItem* d_items = nullptr;
+    std::vector<int32_t> lvl_off;      // item offsets of every dichotomy level (+ end)
+    int32_t* d_lvl_off = nullptr;
+
+    // FUSED path tables (uniform partitions only)
+    int nseg = 0;                      // segments per block
+    double* d_cmat = nullptr;          // [p][2P] combination matrix (see build_fused_tables)
+    void* d_ffwd = nullptr;            // FusedFwd<T>[n]
+    void* d_fbwd = nullptr;            // FusedBwd<T>[n]
+    psw::SegCoef* d_seg = nullptr;     // [P][nseg]
 
     // multi-GPU row shard (psw_shard_*); world == 1 for a full plan
     int rank = 0, world = 1;
@@ -96,7 +127,18 @@ namespace psw {
 int solve_staged(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
                  int64_t N, int layout, cudaStream_t s, double* ext_bl, double* ext_br,
                  double* ext_v, void** events, int nevents);
-bool fused_supported(const psw_plan* plan, int layout, int64_t N);
+bool fused_supported(const psw_plan* plan, int layout, int64_t N, const void* F, int64_t ldf);
+// builds and uploads the FUSED tables from the per-row sweep coefficients
+int build_fused_tables(psw_plan* pl, const std::vector<double>& rp, const std::vector<double>& ma,
+                       const std::vector<double>& gr, const std::vector<double>& gl,
+                       const std::vector<double>& w, const std::vector<double>& al,
+                       const std::vector<double>& cmat);
+// The dichotomy combination (boundary_solve.hpp:96-121) is linear in the
+// betas: V = MR * right + ML * left. Returns [p][2P] rows (MR | ML), each
+// column the reference combination of a unit beta vector (host, fp64,
+// no FP contraction).
+std::vector<double> combine_matrix(const psw_plan* pl, const std::vector<double>& zr,
+                                   const std::vector<double>& zl);
 int solve_fused(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
                 int64_t N, int layout, cudaStream_t s, void** events, int nevents);
 // records events[i] (if present) on s
@@ -107,6 +149,7 @@ int shard_forward(const psw_plan* plan, const void* F, int64_t ldf, void* X, int
                   int64_t N, double* partials, cudaStream_t s);
 int shard_backward(const psw_plan* plan, void* X, int64_t ldx, int64_t N, const double* partials,
                    cudaStream_t s);
+int set_trace(void* buf);  // psw_debug_trace (FUSED kernel phase stamps)
 int fill_uniform(void* dst, int dtype, int64_t count, uint64_t seed, uint64_t offset, double lo,
                  double hi, cudaStream_t s);
 int fill_normal(void* dst, int dtype, int64_t count, uint64_t seed, uint64_t offset,

@@ -82,8 +82,10 @@ int64_t forward_breakdown(int64_t n, const double* sub, const double* diag, cons
 
 // dichotomy/level_sets.hpp:18-37 -> level-ordered items with the nearest known
 // neighbours that solve_boundaries finds by scanning (boundary_solve.hpp:106-113).
-std::vector<psw::CombineItem> build_items(int64_t p, int64_t* terms_out) {
+std::vector<psw::CombineItem> build_items(int64_t p, int64_t* terms_out,
+                                          std::vector<int32_t>* lvl_off) {
     std::vector<psw::CombineItem> items;
+    if (lvl_off) lvl_off->assign(1, 0);
     if (p == 0) {
         if (terms_out) *terms_out = 0;
         return items;
@@ -114,6 +116,7 @@ std::vector<psw::CombineItem> build_items(int64_t p, int64_t* terms_out) {
             terms += per * (1 + (kl >= 0) + (kr < p));
         }
         for (int64_t pos : level) known[pos - 1] = 1;
+        if (lvl_off) lvl_off->push_back(int32_t(items.size()));
     }
     if (terms_out) *terms_out = terms;
     return items;
@@ -141,14 +144,20 @@ int upload(psw_plan* pl, const std::vector<double>& rp, const std::vector<double
     int64_t bytes = int64_t(sizeof(FwdCoef<T>) + sizeof(BwdCoef<T>)) * n +
                     int64_t(sizeof(int32_t) * pl->blk.size());
     if (p > 0) {
-        PSW_CUDA_TRY(cudaMalloc(&pl->d_zr, sizeof(double) * p * p));
-        PSW_CUDA_TRY(cudaMalloc(&pl->d_zl, sizeof(double) * p * p));
+        // padded to a 16-byte multiple (bulk copies of the whole table)
+        PSW_CUDA_TRY(cudaMalloc(&pl->d_zr, sizeof(double) * (p * p + 2)));
+        PSW_CUDA_TRY(cudaMalloc(&pl->d_zl, sizeof(double) * (p * p + 2)));
+        PSW_CUDA_TRY(cudaMemset(pl->d_zr, 0, sizeof(double) * (p * p + 2)));
+        PSW_CUDA_TRY(cudaMemset(pl->d_zl, 0, sizeof(double) * (p * p + 2)));
         PSW_CUDA_TRY(cudaMemcpy(pl->d_zr, zr.data(), sizeof(double) * p * p, cudaMemcpyHostToDevice));
         PSW_CUDA_TRY(cudaMemcpy(pl->d_zl, zl.data(), sizeof(double) * p * p, cudaMemcpyHostToDevice));
         PSW_CUDA_TRY(cudaMalloc(&pl->d_items, sizeof(psw::CombineItem) * p));
         PSW_CUDA_TRY(cudaMemcpy(pl->d_items, pl->items.data(), sizeof(psw::CombineItem) * p,
                                 cudaMemcpyHostToDevice));
         bytes += int64_t(2 * sizeof(double) * p * p + sizeof(psw::CombineItem) * p);
+        PSW_CUDA_TRY(cudaMalloc(&pl->d_lvl_off, sizeof(int32_t) * pl->lvl_off.size()));
+        PSW_CUDA_TRY(cudaMemcpy(pl->d_lvl_off, pl->lvl_off.data(),
+                                sizeof(int32_t) * pl->lvl_off.size(), cudaMemcpyHostToDevice));
     }
     pl->info.device_bytes = bytes;
     return PSW_OK;
@@ -160,6 +169,7 @@ void free_plan(psw_plan* pl) {
     cudaGetDevice(&prev);
     cudaSetDevice(pl->device);
     void* ptrs[] = {pl->d_fwd, pl->d_bwd, pl->d_blk, pl->d_zr, pl->d_zl, pl->d_items,
+                    pl->d_lvl_off, pl->d_ffwd, pl->d_fbwd, pl->d_seg, pl->d_cmat,
                     pl->d_partial_spec, pl->d_coarse_items, pl->d_local_items, pl->d_partial_index};
     for (void* q : ptrs)
         if (q) cudaFree(q);
@@ -382,7 +392,7 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
         }
     }
     int64_t terms = 0;
-    pl->items = build_items(p, &terms);
+    pl->items = build_items(p, &terms, &pl->lvl_off);
 
     // the device is only needed for the upload: host validation and the
     // preliminary (and its PivotBreakdown) come first, like the reference
@@ -406,6 +416,8 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
     }
     int rc = (dtype == PSW_F64) ? upload<double>(pl, rp, ma, gr, gl, w, alv, zr, zl)
                                 : upload<float>(pl, rp, ma, gr, gl, w, alv, zr, zl);
+    if (rc == PSW_OK && pl->uniform && world == 1)
+        rc = build_fused_tables(pl, rp, ma, gr, gl, w, alv, combine_matrix(pl, zr, zl));
     if (rc == PSW_OK && world > 1) rc = build_shard_tables(pl);
     cudaSetDevice(prev_dev);
     if (rc != PSW_OK) {
@@ -419,7 +431,7 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
     in.dtype = dtype;
     in.device = device;
     in.uniform = pl->uniform ? 1 : 0;
-    in.fused_ok = psw::fused_supported(pl, PSW_LAYOUT_R, 1 << 20) ? 1 : 0;
+    in.fused_ok = psw::fused_supported(pl, PSW_LAYOUT_R, 1 << 20, nullptr, 1 << 20) ? 1 : 0;
     in.combine_terms = terms;
     int64_t depth = 0;
     if (p > 0) {
@@ -434,6 +446,57 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
 }
 
 void destroy_plan(psw_plan* pl) { free_plan(pl); }
+
+// boundary_solve.hpp:42-88 on the host, item by item (same arithmetic as
+// the device combine_item; this TU has no FP contraction).
+static void host_combine(const psw_plan* pl, const std::vector<double>& zr,
+                         const std::vector<double>& zl, const double* left, const double* right,
+                         double* V) {
+    const int64_t p = pl->p;
+    for (const auto& it : pl->items) {
+        const int64_t i = it.i, kl = it.kl, kr = it.kr;
+        double vi = 0.0, sl = 0.0, sr = 0.0;
+        for (int64_t t = kl + 1; t <= kr; ++t) {
+            vi += t <= i ? right[t] * zr[t * p + i] : left[t] * zl[(t - 1) * p + i];
+            if (kl >= 0) sl += left[t] * zl[(t - 1) * p + kl];
+            if (kr < p) sr += right[t] * zr[t * p + kr];
+        }
+        double v;
+        if (kl >= 0 && kr < p) {
+            const double b1 = V[kl] - sl, b2 = V[kr] - sr;
+            const double m12 = zl[kr * p + kl], m21 = zr[kl * p + kr];
+            const double det = 1.0 - m12 * m21;
+            const double cl = (b1 - m12 * b2) / det, cr = (b2 - m21 * b1) / det;
+            v = vi + cl * zr[kl * p + i] + cr * zl[kr * p + i];
+        } else if (kr < p) {
+            v = vi + (V[kr] - sr) * zl[kr * p + i];
+        } else if (kl >= 0) {
+            v = vi + (V[kl] - sl) * zr[kl * p + i];
+        } else {
+            v = vi;
+        }
+        V[i] = v;
+    }
+}
+
+std::vector<double> combine_matrix(const psw_plan* pl, const std::vector<double>& zr,
+                                   const std::vector<double>& zl) {
+    const int64_t p = pl->p, P = pl->P;
+    std::vector<double> M(size_t(p) * 2 * P, 0.0), unit(P, 0.0), zero(P, 0.0), col(p > 0 ? p : 1);
+    for (int64_t t = 0; t < P; ++t) {
+        unit[t] = 1.0;
+        if (t < p) {  // right[t] (betas.hpp:46-49)
+            host_combine(pl, zr, zl, zero.data(), unit.data(), col.data());
+            for (int64_t j = 0; j < p; ++j) M[j * 2 * P + t] = col[j];
+        }
+        if (t > 0) {  // left[t] (betas.hpp:51-55)
+            host_combine(pl, zr, zl, unit.data(), zero.data(), col.data());
+            for (int64_t j = 0; j < p; ++j) M[j * 2 * P + P + t] = col[j];
+        }
+        unit[t] = 0.0;
+    }
+    return M;
+}
 
 }  // namespace psw
 
@@ -552,11 +615,11 @@ int psw_solve_ex(const psw_plan* plan, const void* F, int64_t ldf, void* X, int6
     const bool want_intermediates =
         opts && (opts->betas_left || opts->betas_right || opts->boundary_values);
     int rc;
-    if (path == PSW_PATH_FUSED && !psw::fused_supported(plan, layout, nrhs)) {
+    if (path == PSW_PATH_FUSED && !psw::fused_supported(plan, layout, nrhs, F, ldf)) {
         psw::set_error(PSW_NOT_SUPPORTED, "fused path does not support this plan/shape");
         rc = PSW_NOT_SUPPORTED;
     } else if ((path == PSW_PATH_FUSED || path == PSW_PATH_AUTO) && !want_intermediates &&
-               psw::fused_supported(plan, layout, nrhs)) {
+               psw::fused_supported(plan, layout, nrhs, F, ldf)) {
         rc = psw::solve_fused(plan, F, ldf, X, ldx, nrhs, layout, s, opts ? opts->events : nullptr,
                               opts ? opts->nevents : 0);
     } else {
@@ -596,3 +659,8 @@ int psw_l2_flush(void* scratch, int64_t bytes, void* stream) {
 }
 
 }  // extern "C"
+
+extern "C" int psw_debug_trace(void* device_buffer) {
+    psw::clear_error();
+    return psw::set_trace(device_buffer);
+}

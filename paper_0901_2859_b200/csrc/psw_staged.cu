@@ -15,6 +15,7 @@
 // Betas and the combination use separately rounded products and sums in the
 // reference's summation order, so betas and boundary values are bitwise the
 // reference's (compiled without FP contraction) for the same inputs.
+#include "psw_device.cuh"
 #include "psw_internal.h"
 
 namespace psw {
@@ -28,10 +29,6 @@ __device__ __forceinline__ T ld_stream(const T* p) {
     return __ldcs(p);  // F is read exactly once: evict-first
 }
 
-// Reference-rounded multiply-add (no contraction): s + a*b.
-__device__ __forceinline__ double madd_rn(double s, double a, double b) {
-    return __dadd_rn(s, __dmul_rn(a, b));
-}
 
 // ---------------------------------------------------------------- layout R
 template <typename T>
@@ -204,50 +201,42 @@ __global__ void __launch_bounds__(kThreads) bwd_s_kernel(
 }
 
 // --------------------------------------------------------------- combine
-// boundary_solve.hpp:42-55 (segment_particular) with betas [t * N + k].
-__device__ __forceinline__ double seg_sum(const double* __restrict__ bl,
-                                          const double* __restrict__ br, int64_t N, int64_t k,
-                                          const double* __restrict__ zr,
-                                          const double* __restrict__ zl, int p, int kl, int kr,
-                                          int e) {
-    double s = 0.0;
-    for (int t = kl + 1; t <= e; ++t) s = madd_rn(s, br[int64_t(t) * N + k], zr[t * p + e]);
-    for (int t = e + 1; t <= kr; ++t) s = madd_rn(s, bl[int64_t(t) * N + k], zl[(t - 1) * p + e]);
-    return s;
-}
+// One thread per RHS, 32 RHS per CTA. For P <= kStageP the CTA first stages
+// its RHS' betas (coalesced, all loads in flight) and keeps the boundary
+// values in shared memory; larger P reads betas from global/L2.
+constexpr int kCombineThreads = 32;
+constexpr int kStageP = 96;
 
-__global__ void __launch_bounds__(kThreads) combine_kernel(
+__global__ void __launch_bounds__(kCombineThreads) combine_kernel(
     const double* __restrict__ bl, const double* __restrict__ br, int64_t N, int p,
     const CombineItem* __restrict__ items, const double* __restrict__ zr,
     const double* __restrict__ zl, double* __restrict__ V) {
-    const int64_t k = int64_t(blockIdx.x) * kThreads + threadIdx.x;
-    if (k >= N) return;
-    for (int w = 0; w < p; ++w) {
-        const CombineItem it = items[w];
-        const int i = it.i, kl = it.kl, kr = it.kr;
-        // boundary_solve.hpp:61-88 (segment_component)
-        const double vi = seg_sum(bl, br, N, k, zr, zl, p, kl, kr, i);
-        double v;
-        if (kl >= 0 && kr < p) {
-            const double b1 = __dsub_rn(V[int64_t(kl) * N + k], seg_sum(bl, br, N, k, zr, zl, p, kl, kr, kl));
-            const double b2 = __dsub_rn(V[int64_t(kr) * N + k], seg_sum(bl, br, N, k, zr, zl, p, kl, kr, kr));
-            const double m12 = zl[kr * p + kl];
-            const double m21 = zr[kl * p + kr];
-            const double det = __dsub_rn(1.0, __dmul_rn(m12, m21));
-            const double cl = __ddiv_rn(__dsub_rn(b1, __dmul_rn(m12, b2)), det);
-            const double cr = __ddiv_rn(__dsub_rn(b2, __dmul_rn(m21, b1)), det);
-            v = madd_rn(madd_rn(vi, cl, zr[kl * p + i]), cr, zl[kr * p + i]);
-        } else if (kr < p) {
-            const double cr = __dsub_rn(V[int64_t(kr) * N + k], seg_sum(bl, br, N, k, zr, zl, p, kl, kr, kr));
-            v = madd_rn(vi, cr, zl[kr * p + i]);
-        } else if (kl >= 0) {
-            const double cl = __dsub_rn(V[int64_t(kl) * N + k], seg_sum(bl, br, N, k, zr, zl, p, kl, kr, kl));
-            v = madd_rn(vi, cl, zr[kl * p + i]);
-        } else {
-            v = vi;
+    extern __shared__ double sh[];  // [2][P][32] betas + [p][32] values
+    const int lane = threadIdx.x;
+    const int64_t k0 = int64_t(blockIdx.x) * kCombineThreads;
+    const int64_t k = k0 + lane;
+    const int P = p + 1;
+    if (P <= kStageP) {
+        double* sl = sh;
+        double* sr = sh + P * kCombineThreads;
+        double* sv = sh + 2 * P * kCombineThreads;
+        for (int t = 0; t < P; ++t) {
+            sl[t * kCombineThreads + lane] = k < N ? bl[int64_t(t) * N + k] : 0.0;
+            sr[t * kCombineThreads + lane] = k < N ? br[int64_t(t) * N + k] : 0.0;
         }
-        V[int64_t(i) * N + k] = v;
+        __syncwarp();
+        if (k < N) combine_rhs(items, p, sl + lane, sr + lane, kCombineThreads, zr, zl, sv + lane,
+                               kCombineThreads);
+        __syncwarp();
+        if (k < N)
+            for (int j = 0; j < p; ++j) V[int64_t(j) * N + k] = sv[j * kCombineThreads + lane];
+    } else if (k < N) {
+        combine_rhs(items, p, bl + k, br + k, N, zr, zl, V + k, N);
     }
+}
+
+size_t combine_smem(int64_t P) {
+    return P <= kStageP ? size_t(sizeof(double) * kCombineThreads * (3 * P - 1)) : 0;
 }
 
 template <typename T>
@@ -267,7 +256,8 @@ int launch_staged(const psw_plan* pl, const void* Fv, int64_t ldf, void* Xv, int
         ++launches;
         mark(ev, nev, 1, s);
         if (p > 0) {
-            combine_kernel<<<grid.x, kThreads, 0, s>>>(bl, br, N, p, pl->d_items, pl->d_zr, pl->d_zl, V);
+            combine_kernel<<<unsigned((N + kCombineThreads - 1) / kCombineThreads), kCombineThreads,
+                             combine_smem(pl->P), s>>>(bl, br, N, p, pl->d_items, pl->d_zr, pl->d_zl, V);
             ++launches;
         }
         mark(ev, nev, 2, s);
@@ -281,7 +271,8 @@ int launch_staged(const psw_plan* pl, const void* Fv, int64_t ldf, void* Xv, int
         ++launches;
         mark(ev, nev, 1, s);
         if (p > 0) {
-            combine_kernel<<<unsigned((N + kThreads - 1) / kThreads), kThreads, 0, s>>>(
+            combine_kernel<<<unsigned((N + kCombineThreads - 1) / kCombineThreads), kCombineThreads,
+                             combine_smem(pl->P), s>>>(
                 bl, br, N, p, pl->d_items, pl->d_zr, pl->d_zl, V);
             ++launches;
         }

@@ -1,0 +1,68 @@
+"""Phase trace of the FUSED kernel (profiling aid, psw_debug_trace).
+
+    python tools/trace_fused.py [--config C1] [--rb 128]
+
+Runs one traced solve and prints, per phase, the median / p90 duration in
+SM cycles over all CTAs, plus how many CTAs were resident at once.
+"""
+import argparse
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+PHASES = ["tables wait", "fwd segment", "fwd scan", "scan barrier", "beta push+cluster barrier",
+          "combine", "bwd scan", "bwd segment"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C1")
+    ap.add_argument("--nrhs", type=int, default=None)
+    args = ap.parse_args()
+    import torch
+    import paper_0901_2859_b200 as psw
+    from paper_0901_2859_b200.configs import CONFIGS
+    cfg = CONFIGS[args.config]
+    if args.nrhs:
+        cfg = cfg.with_(nrhs=args.nrhs)
+    a, b = cfg.matrix_ab(0)
+    plan = psw.Plan(psw.TridiagMatrix.symmetric(a, b), psw.decompose(cfg.n, cfg.P).induced_partition(),
+                    dtype=psw.F64 if cfg.dtype == "f64" else psw.F32)
+    tdt = torch.float64 if cfg.dtype == "f64" else torch.float32
+    F = torch.empty((cfg.n, cfg.nrhs), dtype=tdt, device="cuda")
+    psw.fill_uniform(F, 3, -1, 1)
+    X = torch.empty_like(F)
+    plan.solve(F, X, path=psw.PATH_FUSED)
+    torch.cuda.synchronize()
+    buf = torch.zeros(1 << 22, dtype=torch.int64, device="cuda")
+    L = psw.lib()
+    L.psw_debug_trace.argtypes = [C.c_void_p]
+    L.psw_debug_trace(buf.data_ptr())
+    plan.solve(F, X, path=psw.PATH_FUSED)
+    torch.cuda.synchronize()
+    L.psw_debug_trace(None)
+    tr = buf.cpu().numpy().reshape(-1, 16)
+    used = tr[:, 15] > 0
+    tr = tr[used]
+    print(f"CTAs traced: {len(tr)}")
+    for k, name in enumerate(PHASES):
+        d = (tr[:, k + 1] - tr[:, k]).astype(np.float64)
+        print(f"  {name:28s} median {np.median(d):8.0f}  p90 {np.percentile(d, 90):8.0f} cycles")
+    tot = (tr[:, 8] - tr[:, 0]).astype(np.float64)
+    print(f"  {'CTA lifetime':28s} median {np.median(tot):8.0f}  p90 {np.percentile(tot, 90):8.0f} cycles")
+    t0, t1 = tr[:, 14], tr[:, 15]
+    span = (t1.max() - t0.min()) / 1e3
+    life = (t1 - t0) / 1e3
+    print(f"kernel span {span:.1f} us, CTA life median {np.median(life):.2f} us, "
+          f"mean resident CTAs {life.sum() / span:.0f}")
+    grid = np.linspace(t0.min(), t1.max(), 9)
+    res = [int(((t0 <= x) & (t1 > x)).sum()) for x in grid]
+    print("resident CTAs over time:", res)
+
+
+if __name__ == "__main__":
+    main()
