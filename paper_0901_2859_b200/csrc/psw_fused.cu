@@ -23,6 +23,8 @@
 #include <cudaTypedefs.h>
 #include <cooperative_groups.h>
 
+#include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdlib>
 #include <mutex>
@@ -38,8 +40,8 @@ namespace {
 
 constexpr int kChunk = 32;                 // rows per TMA box / mbarrier
 constexpr int kMaxCluster = 16;
-constexpr int kMaxThreads = 512;
-constexpr size_t kSmemTarget = 72 * 1024;  // ~3 CTAs per SM
+constexpr int kMaxThreads = 256;  // consumer threads per CTA (+ one producer warp)
+constexpr size_t kSmemTarget = 110 * 1024;  // >= 2 CTAs per SM
 constexpr size_t kSmemMax = 200 * 1024;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -87,46 +89,337 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
         : "memory");
 }
 
-// Optional per-CTA phase trace (psw_debug_trace): 16 slots per CTA,
-// clock64() at phase boundaries, %globaltimer at start/end.
+// Optional per-CTA phase trace (psw_debug_trace): 16 slots per CTA and
+// iteration 0, clock64() at phase boundaries, %globaltimer at start/end.
 __device__ unsigned long long* g_trace = nullptr;
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-#define PSW_TRACE(k)                                                         \
-    do {                                                                     \
-        if (trace && threadIdx.x == 0) trace[blockIdx.x * 16 + (k)] = clock64(); \
+#define PSW_TRACE(k)                                                                  \
+    do {                                                                              \
+        if (trace && it == 1 && threadIdx.x == 0) trace[blockIdx.x * 16 + (k)] = clock64(); \
     } while (0)
+
+// shared::cluster address of `addr` (own CTA) in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+
+// 16-byte remote store that completes its bytes on the remote mbarrier
+__device__ __forceinline__ void st_async_f64x2(uint32_t raddr, double a, double b, uint32_t rbar) {
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(
+            raddr),
+        "d"(a), "d"(b), "r"(rbar)
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// barrier among the consumer threads only (the producer warp never joins)
+__device__ __forceinline__ void consumer_sync(int nc) {
+    asm volatile("bar.sync 1, %0;" ::"r"(nc) : "memory");
+}
 
 struct FusedGeom {
     int n, P, p, m, G, C, S, rows_alloc, nchunks;
-    int64_t N, ldx;
+    int64_t N, ldx, ntiles;
 };
 
-// Shared-memory carve-up (bytes), identical on host and device.
+// Shared-memory carve-up (bytes), identical on host and device: the slab
+// (TMA landing zone, handed back to the producer right after the forward
+// sweep), the d~ buffer of the tile awaiting its back substitution, the plan
+// tables loaded once, per-tile-parity scan buffers and beta exchange buffers.
 struct FusedLayout {
-    size_t slab, ff, fb, seg, own, all, vals, segc, cm, bars, total;
+    size_t dbuf, ff, fb, segc, cm, seg0, seg_b, part, all0, all_b, vals, bars, total;
     __host__ __device__ FusedLayout(int rows_alloc, int nchunks, int G, int S, int P, int W,
                                     int es) {
         auto up = [](size_t x) { return (x + 127) & ~size_t(127); };
-        slab = 0;                                                   // rows x W values
-        ff = up(size_t(rows_alloc) * W * es);                       // FusedFwd rows
+        dbuf = up(size_t(rows_alloc) * W * es);                     // rows x W values
+        ff = 2 * dbuf;                                              // FusedFwd rows
         fb = up(ff + size_t(rows_alloc) * (es == 8 ? 48 : 32));     // FusedBwd rows
-        seg = up(fb + size_t(rows_alloc) * (es == 8 ? 32 : 16));    // 4 x G*S*W doubles
-        own = up(seg + size_t(4) * G * S * W * sizeof(double));     // 2 x G*W doubles
-        all = up(own + size_t(2) * G * W * sizeof(double));         // 2 x P*W doubles
-        vals = up(all + size_t(2) * P * W * sizeof(double));        // P x W doubles
-        segc = up(vals + size_t(P) * W * sizeof(double));           // G*S SegCoef
+        segc = up(fb + size_t(rows_alloc) * (es == 8 ? 32 : 16));   // G*S SegCoef
         cm = up(segc + size_t(G) * S * sizeof(SegCoef));            // (G+1) x 2P doubles
-        bars = up(cm + size_t(G + 1) * 2 * P * sizeof(double));
-        total = bars + size_t(nchunks + 1) * sizeof(uint64_t);
+        seg0 = up(cm + size_t(G + 1) * 2 * P * sizeof(double));     // 3 x G*S*W doubles / parity
+        seg_b = up(size_t(3) * G * S * W * sizeof(double));
+        part = seg0 + 2 * seg_b;                                    // 2 x G*S*W beta partials
+        all0 = up(part + size_t(2) * G * S * W * sizeof(double));   // P x W x (R,L) / parity
+        all_b = up(size_t(2) * P * W * sizeof(double));
+        vals = all0 + 2 * all_b;                                    // P x W doubles
+        bars = up(vals + size_t(P) * W * sizeof(double));           // nchunks + 4
+        total = bars + size_t(nchunks + 4) * sizeof(uint64_t);
+    }
+};
+
+constexpr int kSegMax = kSegLen + 1;  // the last block owns m + 1 rows
+
+// Forward rows of one segment, d~ kept in registers. NMAX is a compile-time
+// bound (fully unrolled); rows q >= len are skipped (only when NMAX > len).
+template <typename T, int W, int NMAX>
+__device__ __forceinline__ void fwd_rows(const FusedFwd<T>* __restrict__ cf,
+                                         const T* __restrict__ col, T (&dr)[kSegMax], T& d,
+                                         T& sr, T& sl, T& sx, int len) {
+#pragma unroll
+    for (int q = 0; q < NMAX; ++q) {
+        if (NMAX == kSegLen || q < len) {
+            const FusedFwd<T> c = cf[q];
+            const T f = col[q * W];
+            d = fma(c.ma, d, f * c.rp);
+            sr = fma(f, c.gr, sr);
+            sl = fma(f, c.gl, sl);
+            sx = fma(c.lam, d, sx);
+            dr[q] = d;
+        }
+    }
+}
+
+// Forward rows of one segment, d~ written back over f in the slab.
+template <typename T, int W, int NMAX>
+__device__ __forceinline__ void fwd_rows_smem(const FusedFwd<T>* __restrict__ cf, T* col, T& d,
+                                              T& sr, T& sl, T& sx, int len) {
+#pragma unroll
+    for (int q = 0; q < NMAX; ++q) {
+        if (NMAX == kSegLen || q < len) {
+            const FusedFwd<T> c = cf[q];
+            const T f = col[q * W];
+            d = fma(c.ma, d, f * c.rp);
+            sr = fma(f, c.gr, sr);
+            sl = fma(f, c.gl, sl);
+            sx = fma(c.lam, d, sx);
+            col[q * W] = d;
+        }
+    }
+}
+
+// Backward rows reading d~ from the slab (see bwd_rows).
+template <typename T, int W, int NMAX>
+__device__ __forceinline__ void bwd_rows_smem(const FusedBwd<T>* __restrict__ cb, const T* col,
+                                              T D, T xl, T xn, T* xp, int64_t ldx, int len) {
+#pragma unroll
+    for (int q = NMAX - 1; q >= 0; --q) {
+        if (NMAX == kSegLen || q < len) {
+            const FusedBwd<T> c = cb[q];
+            const T cq = fma(xl, c.w, fma(c.mu, D, col[q * W]));
+            xn = fma(c.al, xn, cq);
+            __stcs(xp, xn);
+            xp -= ldx;
+        }
+    }
+}
+
+// Backward rows of one segment from the exact carry xn, last row first;
+// xp points at the segment's last row of X and walks up by ldx.
+template <typename T, int NMAX>
+__device__ __forceinline__ void bwd_rows(const FusedBwd<T>* __restrict__ cb,
+                                         const T (&dr)[kSegMax], T D, T xl, T xn, T* xp,
+                                         int64_t ldx, int len) {
+#pragma unroll
+    for (int q = NMAX - 1; q >= 0; --q) {
+        if (NMAX == kSegLen || q < len) {
+            const FusedBwd<T> c = cb[q];
+            const T cq = fma(xl, c.w, fma(c.mu, D, dr[q]));
+            xn = fma(c.al, xn, cq);
+            __stcs(xp, xn);
+            xp -= ldx;
+        }
+    }
+}
+
+// Per-consumer-thread constants of the fused kernel.
+struct FusedCtx {
+    int tid, nc, lane, j, sg, t, a, b, len, c_lo, c_hi, row0, jb0, jb1;
+};
+
+// Persistent and software-pipelined. Each cluster walks the RHS tiles
+// cluster_id, cluster_id + nclusters, ...; iteration k sweeps tile k+1
+// forward (d~ in registers, the slab is handed back to the producer warp at
+// once, which streams tile k+2 into it), then combines and back-substitutes
+// tile k. A tile's DSMEM beta exchange therefore overlaps a back
+// substitution and a forward sweep, and its HBM load overlaps a combination
+// and a back substitution.
+template <typename T, int W>
+struct FusedTile {
+    const FusedGeom& g;
+    const FusedCtx& x;
+    unsigned char* smem;
+    const FusedLayout& L;
+    const FusedFwd<T>* cf;
+    const FusedBwd<T>* cb;
+    const SegCoef* segc;
+    const double* cm;
+    uint64_t* bars;
+    uint64_t* xbar;
+    uint64_t* fbar;
+    int crank, C;
+    int64_t cluster_id, nclusters;
+    T* X;
+
+    __device__ __forceinline__ double* seg(int64_t k) const {
+        return reinterpret_cast<double*>(smem + L.seg0 + (k & 1) * L.seg_b);
+    }
+    __device__ __forceinline__ double* allx(int64_t k) const {
+        return reinterpret_cast<double*>(smem + L.all0 + (k & 1) * L.all_b);
+    }
+
+    // forward sweep of tile k into dr; betas pushed after the scan
+    __device__ __forceinline__ void forward(int64_t k, T (&dr)[kSegMax]) const {
+        const int GSW = x.nc;
+        if (x.tid == 0) mbar_expect_tx(&xbar[k & 1], uint32_t(g.P * W * 2 * sizeof(double)));
+        for (int c = x.c_lo; c <= x.c_hi; ++c) mbar_wait(&bars[c], uint32_t(k) & 1u);
+        const T* col = reinterpret_cast<const T*>(smem) + x.lane + (x.a - x.row0) * W;
+        T d = T(0), sr = T(0), sl = T(0), sx = T(0);
+        if (x.len == kSegLen)
+            fwd_rows<T, W, kSegLen>(cf, col, dr, d, sr, sl, sx, kSegLen);
+        else
+            fwd_rows<T, W, kSegMax>(cf, col, dr, d, sr, sl, sx, x.len);
+        __syncwarp();
+        if ((x.tid & 31) == 0) mbar_arrive(fbar);  // this warp is done with the slab
+        double* sk = seg(k);
+        double* part = reinterpret_cast<double*>(smem + L.part);
+        sk[x.tid] = double(d);         // d~ at the segment end
+        sk[GSW + x.tid] = double(sx);  // Lam
+        part[x.tid] = double(sr);
+        part[GSW + x.tid] = double(sl);
+    }
+
+    // forward carries over the segments of a block; block betas
+    __device__ __forceinline__ void fwd_scan(int64_t k, double& R, double& Lsum) const {
+        R = 0.0;
+        Lsum = 0.0;
+        if (x.sg != 0) return;
+        double* sk = seg(k);
+        const double* part = reinterpret_cast<const double*>(smem + L.part);
+        double D = 0.0;
+        for (int q = 0; q < g.S; ++q) {
+            const int id = (x.j * g.S + q) * W + x.lane;
+            const double dend = sk[id];
+            sk[id] = D;  // carry into segment q: D_{a-1}
+            D = fma(segc[x.t * g.S + q].mu_end, D, dend);
+            R += part[id];
+            Lsum += part[x.nc + id];
+        }
+    }
+
+    // st.async of this block's betas into every CTA of the cluster
+    __device__ __forceinline__ void push(int64_t k, double R, double Lsum) const {
+        if (x.sg != 0) return;
+        const uint32_t src = smem_u32(allx(k)) + uint32_t((x.t * W + x.lane) * 16);
+        const uint32_t bar = smem_u32(&xbar[k & 1]);
+        for (int dst = 0; dst < C; ++dst) st_async_f64x2(mapa(src, dst), R, Lsum, mapa(bar, dst));
+    }
+
+    // boundary values of tile k this CTA needs: v = MR right + ML left, each
+    // dot product split over 4 lanes and reduced with shuffles
+    __device__ __forceinline__ void combine(int64_t k) const {
+        mbar_wait(&xbar[k & 1], uint32_t(k >> 1) & 1u);
+        const double* ax = allx(k);
+        double* vals = reinterpret_cast<double*>(smem + L.vals);
+        const int P = g.P, nout = (x.jb1 - x.jb0) * W;
+        const int nwork = ((nout * 4 + 31) / 32) * 32;
+        for (int idx = x.tid; idx < nwork; idx += x.nc) {
+            const int o = idx >> 2, part = idx & 3;
+            double s = 0.0;
+            if (o < nout) {
+                const int jb = o / W, ln = o % W;
+                const double* Mr = cm + jb * 2 * P;
+                for (int tt = part; tt < P; tt += 4) {
+                    s = fma(Mr[tt], ax[(tt * W + ln) * 2], s);
+                    s = fma(Mr[P + tt], ax[(tt * W + ln) * 2 + 1], s);
+                }
+            }
+            s += __shfl_xor_sync(0xffffffffu, s, 1);
+            s += __shfl_xor_sync(0xffffffffu, s, 2);
+            if (o < nout && part == 0) vals[x.jb0 * W + o] = s;
+        }
+    }
+
+    // backward carries and back substitution of tile k (d~ from the d~
+    // buffer), streamed to X
+    __device__ __forceinline__ void backward(int64_t k) const {
+        const int GSW = x.nc;
+        double* sk = seg(k);
+        const double* vals = reinterpret_cast<const double*>(smem + L.vals);
+        const double xl = x.t > 0 ? vals[(x.t - 1) * W + x.lane] : 0.0;
+        if (x.sg == 0) {
+            double xb = x.t < g.p ? vals[x.t * W + x.lane] : 0.0;  // x at row e
+            for (int q = g.S - 1; q >= 0; --q) {
+                const int id = (x.j * g.S + q) * W + x.lane;
+                const SegCoef sc = segc[x.t * g.S + q];
+                const double xa = fma(xl, sc.k2, fma(sk[id], sc.k1, sk[GSW + id]));
+                sk[2 * GSW + id] = xb;  // x at the row after the segment
+                xb = fma(sc.nu, xb, xa);
+            }
+        }
+        consumer_sync(x.nc);
+        const int64_t k0 = (cluster_id + k * nclusters) * W;
+        const T D = T(sk[x.tid]);
+        const T xlt = T(xl);
+        const T xn = T(sk[2 * GSW + x.tid]);
+        if (k0 + x.lane < g.N && x.len > 0) {
+            T* xp = X + k0 + x.lane + int64_t(x.b - 1) * g.ldx;  // last row first
+            const T* col = reinterpret_cast<const T*>(smem + L.dbuf) + x.lane + (x.a - x.row0) * W;
+            if (x.len == kSegLen)
+                bwd_rows_smem<T, W, kSegLen>(cb, col, D, xlt, xn, xp, g.ldx, kSegLen);
+            else
+                bwd_rows_smem<T, W, kSegMax>(cb, col, D, xlt, xn, xp, g.ldx, x.len);
+        }
+    }
+
+    // park d~ of the forward-swept tile in the d~ buffer
+    __device__ __forceinline__ void park(const T (&dr)[kSegMax]) const {
+        T* col = reinterpret_cast<T*>(smem + L.dbuf) + x.lane + (x.a - x.row0) * W;
+#pragma unroll
+        for (int q = 0; q < kSegMax; ++q)
+            if (q < x.len) col[q * W] = dr[q];
+    }
+
+    __device__ __forceinline__ void stamp(int64_t k, int slot) const {
+        unsigned long long* tr = g_trace;
+        if (tr && k == 2 && x.tid == 0) tr[blockIdx.x * 16 + slot] = clock64();
+    }
+
+    // iteration k: forward of tile k+1 (if any), then tile k to completion
+    __device__ __forceinline__ void step(int64_t k, int64_t ntl, T (&dr)[kSegMax]) const {
+        const bool next = k + 1 < ntl;
+        stamp(k, 0);
+        if (next) forward(k + 1, dr);
+        stamp(k, 1);
+        consumer_sync(x.nc);
+        double R, Lsum;
+        if (next) fwd_scan(k + 1, R, Lsum);
+        stamp(k, 2);
+        combine(k);
+        stamp(k, 3);
+        // pushing tile k+1 only after combining tile k keeps two exchange
+        // buffers race-free (a peer's push of tile k+2 then needs this CTA's
+        // betas of tile k+1)
+        if (next) push(k + 1, R, Lsum);
+        consumer_sync(x.nc);
+        stamp(k, 4);
+        backward(k);
+        stamp(k, 5);
+        consumer_sync(x.nc);  // d~ buffer free
+        if (next) park(dr);
+        stamp(k, 6);
+        unsigned long long* tr = g_trace;
+        if (tr && x.tid == 0) {
+            if (k == 0) tr[blockIdx.x * 16 + 10] = gtimer();
+            if (k + 1 == ntl) {
+                tr[blockIdx.x * 16 + 11] = gtimer();
+                tr[blockIdx.x * 16 + 12] = (unsigned long long)ntl;
+            }
+        }
     }
 };
 
 template <typename T, int W>
-__global__ void __launch_bounds__(kMaxThreads) fused_r_kernel(
+__global__ void __launch_bounds__(kMaxThreads + 32) fused_r_kernel(
     const __grid_constant__ CUtensorMap tmF, const __grid_constant__ CUtensorMap tmF1, T* X,
     FusedGeom g, const FusedFwd<T>* __restrict__ gff, const FusedBwd<T>* __restrict__ gfb,
     const SegCoef* __restrict__ gsegc, const double* __restrict__ gcmat) {
@@ -134,194 +427,110 @@ __global__ void __launch_bounds__(kMaxThreads) fused_r_kernel(
     cg::cluster_group cluster = cg::this_cluster();
     const int C = g.C, G = g.G, S = g.S, P = g.P, p = g.p, m = g.m;
     const int crank = int(cluster.block_rank());
-    const int64_t k0 = int64_t(blockIdx.x / C) * W;
+    const int64_t cluster_id = blockIdx.x / C, nclusters = gridDim.x / C;
+    const int64_t ntl = g.ntiles > cluster_id ? (g.ntiles - cluster_id + nclusters - 1) / nclusters : 0;
     // slab row 0 is global row c*G*m - 1 for every CTA (row -1 of CTA 0 is
     // out of bounds: TMA zero-fills it without touching memory)
     const int row0 = crank * G * m - 1;
     const int row1 = crank == C - 1 ? g.n : (crank + 1) * G * m - 1;
     const int crow0 = row0 < 0 ? 0 : row0;  // first coefficient row
-
     const FusedLayout L(g.rows_alloc, g.nchunks, G, S, P, W, int(sizeof(T)));
-    T* slab = reinterpret_cast<T*>(smem + L.slab);
-    const FusedFwd<T>* ff = reinterpret_cast<const FusedFwd<T>*>(smem + L.ff) - crow0;
-    const FusedBwd<T>* fb = reinterpret_cast<const FusedBwd<T>*>(smem + L.fb) - crow0;
-    const int GSW = G * S * W;
-    double* seg_d = reinterpret_cast<double*>(smem + L.seg);  // d~ end -> carry D_{a-1}
-    double* seg_lam = seg_d + GSW;                             // Lam
-    double* seg_br = seg_lam + GSW;                            // beta_R partial -> x carry
-    double* seg_bl = seg_br + GSW;                             // beta_L partial
-    double* own_r = reinterpret_cast<double*>(smem + L.own);
-    double* own_l = own_r + G * W;
-    double* all_r = reinterpret_cast<double*>(smem + L.all);
-    double* all_l = all_r + P * W;
-    double* vals = reinterpret_cast<double*>(smem + L.vals);
-    const SegCoef* segc = reinterpret_cast<const SegCoef*>(smem + L.segc) - crank * G * S;
-    // boundary rows [jb0, jb1) of the combination matrix this CTA needs
-    const int jb0 = crank * G - 1 < 0 ? 0 : crank * G - 1;
-    const int jb1 = crank * G + G < p ? crank * G + G : p;
-    const double* cm = reinterpret_cast<const double*>(smem + L.cm);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
-    uint64_t* cbar = &bars[g.nchunks];
-
+    uint64_t* cbar = &bars[g.nchunks];      // plan tables
+    uint64_t* xbar = &bars[g.nchunks + 1];  // [parity]: betas of a tile from every peer
+    uint64_t* fbar = &bars[g.nchunks + 3];  // slab released (one arrival per consumer warp)
+    const int nc = G * S * W;               // consumer threads; one producer warp follows
     const int tid = threadIdx.x;
-    unsigned long long* const trace = g_trace;
-    if (trace && tid == 0) trace[blockIdx.x * 16 + 14] = gtimer();
-    PSW_TRACE(0);
     const int nrows = row1 - row0;
     const int nfull = nrows / kChunk, rem = nrows % kChunk;
+    FusedCtx x;
+    x.tid = tid;
+    x.nc = nc;
+    x.row0 = row0;
+    x.jb0 = crank * G - 1 < 0 ? 0 : crank * G - 1;  // combination rows [jb0, jb1)
+    x.jb1 = crank * G + G < p ? crank * G + G : p;
+
     if (tid == 0) {
         for (int c = 0; c < nfull + (rem > 0); ++c) mbar_init(&bars[c], 1);
         mbar_init(cbar, 1);
+        mbar_init(&xbar[0], 1);
+        mbar_init(&xbar[1], 1);
+        mbar_init(fbar, nc / 32);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (tid == 0) {
-        // plan tables first (small, L2-resident), then the RHS rows
+    cluster.sync();  // peers may push into this CTA's exchange barriers from now on
+
+    if (tid >= nc) {
+        // ---- producer warp (one lane): plan tables once, then tile k into
+        // the slab as soon as the consumers swept tile k-1 out of it
+        if (tid != nc) return;
         const uint32_t crows = uint32_t(row1 - crow0);
         const uint32_t fwdb = crows * uint32_t(sizeof(FusedFwd<T>));
         const uint32_t bwdb = crows * uint32_t(sizeof(FusedBwd<T>));
         const uint32_t segb = uint32_t(G * S * sizeof(SegCoef));
-        const uint32_t cmb = uint32_t(jb1 > jb0 ? (jb1 - jb0) * 2 * P * sizeof(double) : 0);
+        const uint32_t cmb = uint32_t(x.jb1 > x.jb0 ? (x.jb1 - x.jb0) * 2 * P * sizeof(double) : 0);
         mbar_expect_tx(cbar, fwdb + bwdb + segb + cmb);
         bulk_load(smem + L.ff, gff + crow0, fwdb, cbar);
         bulk_load(smem + L.fb, gfb + crow0, bwdb, cbar);
         bulk_load(smem + L.segc, gsegc + crank * G * S, segb, cbar);
-        if (cmb) bulk_load(smem + L.cm, gcmat + size_t(jb0) * 2 * P, cmb, cbar);
-        constexpr uint32_t box_bytes = uint32_t(W * kChunk * sizeof(T));
-        for (int c = 0; c < nfull; ++c) {
-            mbar_expect_tx(&bars[c], box_bytes);
-            tma_load_2d(slab + size_t(c) * kChunk * W, &tmF, int(k0), row0 + c * kChunk, &bars[c]);
+        if (cmb) bulk_load(smem + L.cm, gcmat + size_t(x.jb0) * 2 * P, cmb, cbar);
+        T* slab = reinterpret_cast<T*>(smem);
+        for (int64_t k = 0; k < ntl; ++k) {
+            if (k > 0) {
+                mbar_wait(fbar, uint32_t(k - 1) & 1u);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            }
+            const int k0 = int((cluster_id + k * nclusters) * W);
+            constexpr uint32_t box_bytes = uint32_t(W * kChunk * sizeof(T));
+            for (int c = 0; c < nfull; ++c) {
+                mbar_expect_tx(&bars[c], box_bytes);
+                tma_load_2d(slab + size_t(c) * kChunk * W, &tmF, k0, row0 + c * kChunk, &bars[c]);
+            }
+            if (rem) {  // tail rows through the one-row box
+                mbar_expect_tx(&bars[nfull], uint32_t(rem * W * sizeof(T)));
+                for (int r = 0; r < rem; ++r)
+                    tma_load_2d(slab + size_t(nfull * kChunk + r) * W, &tmF1, k0,
+                                row0 + nfull * kChunk + r, &bars[nfull]);
+            }
         }
-        if (rem) {  // tail rows through the one-row box
-            mbar_expect_tx(&bars[nfull], uint32_t(rem * W * sizeof(T)));
-            for (int r = 0; r < rem; ++r)
-                tma_load_2d(slab + size_t(nfull * kChunk + r) * W, &tmF1, int(k0),
-                            row0 + nfull * kChunk + r, &bars[nfull]);
-        }
+        return;
     }
 
-    // ---- thread -> (block j, segment sg, rhs lane)
-    const int lane = tid % W, h = tid / W;
-    const int j = h / S, sg = h % S;
-    const int t = crank * G + j;
-    const int s = t == 0 ? 0 : t * m - 1;
-    const int e = t == P - 1 ? g.n : (t + 1) * m - 1;
-    int a = s + sg * kSegLen;
-    int b = sg == S - 1 ? e : a + kSegLen;
-    if (a > e) a = e;
-    if (b > e) b = e;
-
-    // ---- forward sweep of the segment (from zero) + betas + Lam
+    // ---- consumers: thread -> (block j, segment sg, rhs lane)
+    x.lane = tid % W;
+    const int h = tid / W;
+    x.j = h / S;
+    x.sg = h % S;
+    x.t = crank * G + x.j;
+    const int s = x.t == 0 ? 0 : x.t * m - 1;
+    const int e = x.t == P - 1 ? g.n : (x.t + 1) * m - 1;
+    x.a = s + x.sg * kSegLen;
+    x.b = x.sg == S - 1 ? e : x.a + kSegLen;
+    if (x.a > e) x.a = e;
+    if (x.b > e) x.b = e;
+    x.len = x.b - x.a;  // 0..kSegMax
+    x.c_lo = x.len ? (x.a - row0) / kChunk : 0;
+    x.c_hi = x.len ? (x.b - 1 - row0) / kChunk : -1;
+    const FusedTile<T, W> ft{g, x, smem, L,
+                             reinterpret_cast<const FusedFwd<T>*>(smem + L.ff) - crow0 + x.a,
+                             reinterpret_cast<const FusedBwd<T>*>(smem + L.fb) - crow0 + x.a,
+                             reinterpret_cast<const SegCoef*>(smem + L.segc) - crank * G * S,
+                             reinterpret_cast<const double*>(smem + L.cm),
+                             bars, xbar, fbar, crank, C, cluster_id, nclusters, X};
     mbar_wait(cbar, 0);
-    PSW_TRACE(1);
-    double dd = 0.0, br = 0.0, bl = 0.0, lam = 0.0;
-    if (a < b) {
-        for (int c = (a - row0) / kChunk; c <= (b - 1 - row0) / kChunk; ++c) mbar_wait(&bars[c], 0);
-        T d = T(0), sr = T(0), sl = T(0), sx = T(0);
-        T* col = slab + lane;
-#pragma unroll 4
-        for (int q = a; q < b; ++q) {
-            const FusedFwd<T> c = ff[q];
-            const T f = col[(q - row0) * W];
-            d = fma(c.ma, d, f * c.rp);
-            sr = fma(f, c.gr, sr);
-            sl = fma(f, c.gl, sl);
-            sx = fma(c.lam, d, sx);
-            col[(q - row0) * W] = d;
-        }
-        dd = double(d);
-        br = double(sr);
-        bl = double(sl);
-        lam = double(sx);
-    }
-    PSW_TRACE(2);
-    seg_d[tid] = dd;
-    seg_lam[tid] = lam;
-    seg_br[tid] = br;
-    seg_bl[tid] = bl;
-    __syncthreads();
+    if (ntl == 0) return;
 
-    // ---- per (block, rhs): forward carries over the segments, block betas
-    if (sg == 0) {
-        double D = 0.0, R = 0.0, Lsum = 0.0;
-        for (int k = 0; k < S; ++k) {
-            const int id = (j * S + k) * W + lane;
-            const double dend = seg_d[id];
-            seg_d[id] = D;  // carry into segment k: D_{a-1}
-            D = fma(segc[t * S + k].mu_end, D, dend);
-            R += seg_br[id];
-            Lsum += seg_bl[id];
-        }
-        own_r[j * W + lane] = R;
-        own_l[j * W + lane] = Lsum;
+    T dr[kSegMax];
+    ft.forward(0, dr);
+    ft.park(dr);
+    consumer_sync(nc);
+    {
+        double R, Lsum;
+        ft.fwd_scan(0, R, Lsum);
+        ft.push(0, R, Lsum);
     }
-    PSW_TRACE(3);
-    __syncthreads();
-    PSW_TRACE(4);
-    // ---- push this CTA's block betas into every CTA of the cluster (DSMEM)
-    for (int idx = tid; idx < C * G * W; idx += blockDim.x) {
-        const int dst = idx / (G * W), r = idx % (G * W);
-        const int slot = (crank * G) * W + r;  // [block t][lane] in the tile
-        double* rr = cluster.map_shared_rank(all_r, dst);
-        double* rl = cluster.map_shared_rank(all_l, dst);
-        rr[slot] = own_r[r];
-        rl[slot] = own_l[r];
-    }
-    // one cluster barrier: every CTA holds every beta afterwards, and no CTA
-    // touches another's shared memory again (CTAs may then exit freely)
-    asm volatile("barrier.cluster.arrive.release.aligned;\n"
-                 "barrier.cluster.wait.acquire.aligned;" ::: "memory");
-    PSW_TRACE(5);
-
-    // ---- dichotomy combination as its tabulated linear map: the CTA's
-    // boundary values v_j = sum_t MR[j][t] right_t + ML[j][t] left_t
-    for (int idx = tid; idx < (jb1 - jb0) * W; idx += blockDim.x) {
-        const int jb = idx / W, ln = idx % W;
-        const double* Mr = cm + jb * 2 * P;
-        const double* Ml = Mr + P;
-        double sr = 0.0, sl = 0.0;
-        for (int tt = 0; tt < P; ++tt) {
-            sr = fma(Mr[tt], all_r[tt * W + ln], sr);
-            sl = fma(Ml[tt], all_l[tt * W + ln], sl);
-        }
-        vals[(jb0 + jb) * W + ln] = sr + sl;
-    }
-    __syncthreads();
-
-    PSW_TRACE(6);
-    // ---- per (block, rhs): backward carries (x at each segment end)
-    const double xl = t > 0 ? vals[(t - 1) * W + lane] : 0.0;
-    if (sg == 0) {
-        double xb = t < p ? vals[t * W + lane] : 0.0;  // x at row e
-        for (int k = S - 1; k >= 0; --k) {
-            const int id = (j * S + k) * W + lane;
-            const SegCoef sc = segc[t * S + k];
-            const double xa = fma(xl, sc.k2, fma(seg_d[id], sc.k1, seg_lam[id]));
-            seg_br[id] = xb;  // x at the row after the segment
-            xb = fma(sc.nu, xb, xa);
-        }
-    }
-    __syncthreads();
-
-    PSW_TRACE(7);
-    // ---- backward sweep of the segment from its exact carry, streamed to X
-    if (a < b) {
-        const T D = T(seg_d[tid]);
-        const T xlt = T(xl);
-        T xn = T(seg_br[tid]);
-        const T* col = slab + lane;
-        const bool live = k0 + lane < g.N;
-        T* xcol = X + k0 + lane;
-#pragma unroll 4
-        for (int q = b - 1; q >= a; --q) {
-            const FusedBwd<T> c = fb[q];
-            const T cq = fma(xlt, c.w, fma(c.mu, D, col[(q - row0) * W]));
-            xn = fma(c.al, xn, cq);
-            if (live) __stcs(xcol + int64_t(q) * g.ldx, xn);
-        }
-    }
-    PSW_TRACE(8);
-    if (trace && tid == 0) trace[blockIdx.x * 16 + 15] = gtimer();
+    for (int64_t k = 0; k < ntl; ++k) ft.step(k, ntl, dr);
 }
 
 // ---------------------------------------------------------------- host side
@@ -344,11 +553,11 @@ struct Choice {
     size_t smem = 0;
 };
 
-// Row width of an RHS tile: 128 B (default) or 256 B (PSW_FUSED_ROW_BYTES).
+// Row width of an RHS tile: 256 B (default) or 128 B (PSW_FUSED_ROW_BYTES).
 int tile_row_bytes() {
     static int rb = [] {
         const char* e = std::getenv("PSW_FUSED_ROW_BYTES");
-        return (e && std::atoi(e) == 256) ? 256 : 128;
+        return (e && std::atoi(e) == 128) ? 128 : 256;
     }();
     return rb;
 }
@@ -368,6 +577,7 @@ Choice choose_w(const psw_plan* pl, int es, int row_bytes) {
         const int nchunks = (rows_alloc + kChunk - 1) / kChunk;
         const size_t smem = FusedLayout(rows_alloc, nchunks, G, S, P, W, es).total;
         if (smem > kSmemMax || G * S * W > kMaxThreads) break;
+        if ((G * S * W) % 32) continue;  // consumer warps must be full
         if (ch.G == 0 || smem <= kSmemTarget) {
             ch.W = W;
             ch.G = G;
@@ -436,9 +646,9 @@ int launch_w(const psw_plan* pl, const Choice& ch, const void* F, int64_t ldf, v
     PSW_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ch.smem)));
     if (ch.C > 8) PSW_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     const int64_t tiles = (N + W - 1) / W;
+    g.ntiles = tiles;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(unsigned(tiles * ch.C), 1, 1);
-    cfg.blockDim = dim3(unsigned(ch.G * g.S * W), 1, 1);
+    cfg.blockDim = dim3(unsigned(ch.G * g.S * W + 32), 1, 1);  // + producer warp
     cfg.dynamicSmemBytes = ch.smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -448,6 +658,26 @@ int launch_w(const psw_plan* pl, const Choice& ch, const void* F, int64_t ldf, v
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    // persistent: as many clusters as can be co-resident (cached per config)
+    static std::mutex mu;
+    static std::vector<std::pair<std::array<int64_t, 5>, int>> cache;
+    const std::array<int64_t, 5> key = {int64_t(sizeof(T)), W, ch.C, int64_t(ch.smem), pl->device};
+    int maxc = 0;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (auto& kv : cache)
+            if (kv.first == key) maxc = kv.second;
+        if (maxc == 0) {
+            cfg.gridDim = dim3(unsigned(ch.C), 1, 1);
+            PSW_CUDA_TRY(cudaOccupancyMaxActiveClusters(&maxc, kern, &cfg));
+            if (maxc < 1) maxc = 1;
+            cache.push_back({key, maxc});
+        }
+    }
+    int64_t nclusters = std::min<int64_t>(tiles, maxc);
+    if (const char* e = std::getenv("PSW_FUSED_CLUSTERS"))  // tuning override
+        nclusters = std::max<int64_t>(1, std::min<int64_t>(nclusters, std::atoll(e)));
+    cfg.gridDim = dim3(unsigned(nclusters * ch.C), 1, 1);
     mark(ev, nev, 0, s);
     PSW_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tm, tm1, static_cast<T*>(X), g,
                                     static_cast<const FusedFwd<T>*>(pl->d_ffwd),

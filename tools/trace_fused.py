@@ -14,8 +14,8 @@ import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-PHASES = ["tables wait", "fwd segment", "fwd scan", "scan barrier", "beta push+cluster barrier",
-          "combine", "bwd scan", "bwd segment"]
+PHASES = ["forward k+1 (chunk wait + sweep)", "sync + fwd scan", "exchange wait + combine k",
+          "push k+1 + sync", "backward k (scan + sweep)", "sync + park d~"]
 
 
 def main():
@@ -46,22 +46,20 @@ def main():
     torch.cuda.synchronize()
     L.psw_debug_trace(None)
     tr = buf.cpu().numpy().reshape(-1, 16)
-    used = tr[:, 15] > 0
+    used = tr[:, 6] > 0
     tr = tr[used]
     print(f"CTAs traced: {len(tr)}")
     for k, name in enumerate(PHASES):
         d = (tr[:, k + 1] - tr[:, k]).astype(np.float64)
         print(f"  {name:28s} median {np.median(d):8.0f}  p90 {np.percentile(d, 90):8.0f} cycles")
-    tot = (tr[:, 8] - tr[:, 0]).astype(np.float64)
+    tot = (tr[:, len(PHASES)] - tr[:, 0]).astype(np.float64)
     print(f"  {'CTA lifetime':28s} median {np.median(tot):8.0f}  p90 {np.percentile(tot, 90):8.0f} cycles")
-    t0, t1 = tr[:, 14], tr[:, 15]
-    span = (t1.max() - t0.min()) / 1e3
-    life = (t1 - t0) / 1e3
-    print(f"kernel span {span:.1f} us, CTA life median {np.median(life):.2f} us, "
-          f"mean resident CTAs {life.sum() / span:.0f}")
-    grid = np.linspace(t0.min(), t1.max(), 9)
-    res = [int(((t0 <= x) & (t1 > x)).sum()) for x in grid]
-    print("resident CTAs over time:", res)
+    ks, ke, nt = tr[:, 10], tr[:, 11], tr[:, 12]
+    if (ke > 0).all():
+        per = (ke - ks) / np.maximum(nt, 1)
+        print(f"whole kernel: span {(ke.max() - ks.min()) / 1e3:.1f} us, tiles/CTA {nt.min()}..{nt.max()}, "
+              f"median per-tile time {np.median(per):.0f} ns, CTA start spread "
+              f"{(ks.max() - ks.min()) / 1e3:.2f} us, end spread {(ke.max() - ke.min()) / 1e3:.2f} us")
 
 
 if __name__ == "__main__":
