@@ -1,23 +1,28 @@
-// FUSED solve path: one kernel, F read once, X written once (the minimum
-// traffic of SURVEY §8(d)); forward intermediates never leave the chip.
+// FUSED solve path: one persistent kernel, F read once, X written once (the
+// minimum traffic of SURVEY §8(d)); forward intermediates never leave the chip.
 //
 // Work decomposition (layout R, uniform partition n = P*m):
-//   * an RHS tile = W right-hand sides (128 or 256 contiguous bytes per row);
-//   * one thread-block CLUSTER of C CTAs owns the whole tile; CTA c owns G
+//   * an RHS tile = W right-hand sides (128 contiguous bytes per row by
+//     default, 256 with PSW_FUSED_ROW_BYTES=256);
+//   * one thread-block CLUSTER of C CTAs owns a tile; CTA c owns G
 //     consecutive blocks (P = C*G): rows [c*G*m - 1, (c+1)*G*m - 1), the
-//     reference's half-open blocks (partition.hpp:26-29);
+//     reference's half-open blocks (partition.hpp:26-29). Clusters are
+//     persistent and walk the tiles cluster_id, cluster_id + nclusters, ...;
 //   * TMA streams the CTA's rows (box W x 32 rows, one mbarrier per box) into
-//     a shared-memory slab; the block's sweep coefficients arrive by one bulk
-//     copy;
+//     a shared-memory slab; the plan tables (sweep coefficients, segment
+//     constants, rows of the combination matrix) arrive once by bulk copy;
 //   * every block is cut into S segments of kSegLen rows, one thread per
-//     (block, segment, rhs), so a block's forward sweep, its two beta dot
-//     products (betas.hpp:42-57) and the backward sweep run S-wide; segment
-//     carries are exact affine scans (psw_internal.h, FusedFwd/FusedBwd);
-//   * betas of all P blocks meet through distributed shared memory (DSMEM);
-//     every CTA evaluates the dichotomy combination (boundary_solve.hpp:
-//     96-121) level by level, the items of one level in parallel, with the
-//     exact per-item arithmetic of the STAGED path;
-//   * the backward sweep reads d~ from the slab and streams X with
+//     (block, segment, rhs): the forward sweep and both beta dot products
+//     (betas.hpp:42-57) run S-wide with d~ kept in registers, segment carries
+//     are exact affine scans (psw_internal.h, FusedFwd/FusedBwd). The slab is
+//     refilled with the next tile as soon as the sweep has read it;
+//   * block betas are pushed to every CTA of the cluster with st.async
+//     (DSMEM stores that complete bytes on the receiver's mbarrier: no
+//     cluster-wide barrier per tile);
+//   * the dichotomy combination (boundary_solve.hpp:96-121) is linear in the
+//     betas; the plan tabulates it (combination matrix, psw_plan.cpp
+//     combine_matrix) and each CTA evaluates only its own boundary values;
+//   * the backward sweep starts from exact segment carries and streams X with
 //     evict-first stores.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -27,6 +32,7 @@
 #include <array>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <string>
 
@@ -40,7 +46,7 @@ namespace {
 
 constexpr int kChunk = 32;                 // rows per TMA box / mbarrier
 constexpr int kMaxCluster = 16;
-constexpr int kMaxThreads = 256;  // consumer threads per CTA (+ one producer warp)
+constexpr int kMaxThreads = 256;  // threads per CTA
 constexpr size_t kSmemTarget = 110 * 1024;  // >= 2 CTAs per SM
 constexpr size_t kSmemMax = 200 * 1024;
 
@@ -118,12 +124,9 @@ __device__ __forceinline__ void st_async_f64x2(uint32_t raddr, double a, double 
         : "memory");
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
-// barrier among the consumer threads only (the producer warp never joins)
-__device__ __forceinline__ void consumer_sync(int nc) {
+// CTA-wide named barrier (id 1)
+__device__ __forceinline__ void cta_sync(int nc) {
     asm volatile("bar.sync 1, %0;" ::"r"(nc) : "memory");
 }
 
@@ -134,15 +137,15 @@ struct FusedGeom {
 
 // Shared-memory carve-up (bytes), identical on host and device: the slab
 // (TMA landing zone, handed back to the producer right after the forward
-// sweep), the d~ buffer of the tile awaiting its back substitution, the plan
-// tables loaded once, per-tile-parity scan buffers and beta exchange buffers.
+// sweep), the plan tables loaded once, per-tile-parity scan buffers and beta
+// exchange buffers. The d~ of the tile awaiting its back substitution is
+// parked in tensor memory (TMEM), not here.
 struct FusedLayout {
-    size_t dbuf, ff, fb, segc, cm, seg0, seg_b, part, all0, all_b, vals, bars, total;
+    size_t ff, fb, segc, cm, seg0, seg_b, part, all0, all_b, vals, bars, total;
     __host__ __device__ FusedLayout(int rows_alloc, int nchunks, int G, int S, int P, int W,
                                     int es) {
         auto up = [](size_t x) { return (x + 127) & ~size_t(127); };
-        dbuf = up(size_t(rows_alloc) * W * es);                     // rows x W values
-        ff = 2 * dbuf;                                              // FusedFwd rows
+        ff = up(size_t(rows_alloc) * W * es);                       // FusedFwd rows
         fb = up(ff + size_t(rows_alloc) * (es == 8 ? 48 : 32));     // FusedBwd rows
         segc = up(fb + size_t(rows_alloc) * (es == 8 ? 32 : 16));   // G*S SegCoef
         cm = up(segc + size_t(G) * S * sizeof(SegCoef));            // (G+1) x 2P doubles
@@ -152,8 +155,8 @@ struct FusedLayout {
         all0 = up(part + size_t(2) * G * S * W * sizeof(double));   // P x W x (R,L) / parity
         all_b = up(size_t(2) * P * W * sizeof(double));
         vals = all0 + 2 * all_b;                                    // P x W doubles
-        bars = up(vals + size_t(P) * W * sizeof(double));           // nchunks + 4
-        total = bars + size_t(nchunks + 4) * sizeof(uint64_t);
+        bars = up(vals + size_t(P) * W * sizeof(double));           // nchunks + 4, TMEM addr
+        total = bars + size_t(nchunks + 3) * sizeof(uint64_t);
     }
 };
 
@@ -231,7 +234,7 @@ __device__ __forceinline__ void bwd_rows(const FusedBwd<T>* __restrict__ cb,
     }
 }
 
-// Per-consumer-thread constants of the fused kernel.
+// Per-thread constants of the fused kernel.
 struct FusedCtx {
     int tid, nc, lane, j, sg, t, a, b, len, c_lo, c_hi, row0, jb0, jb1;
 };
@@ -255,10 +258,29 @@ struct FusedTile {
     const double* cm;
     uint64_t* bars;
     uint64_t* xbar;
-    uint64_t* fbar;
     int crank, C;
     int64_t cluster_id, nclusters;
     T* X;
+    const CUtensorMap* tmF;
+    const CUtensorMap* tmF1;
+    int nfull, rem;
+
+    // TMA of tile k's rows into the slab (one thread)
+    __device__ __forceinline__ void issue(int64_t k) const {
+        T* slab = reinterpret_cast<T*>(smem);
+        const int k0 = int((cluster_id + k * nclusters) * W);
+        constexpr uint32_t box_bytes = uint32_t(W * kChunk * sizeof(T));
+        for (int c = 0; c < nfull; ++c) {
+            mbar_expect_tx(&bars[c], box_bytes);
+            tma_load_2d(slab + size_t(c) * kChunk * W, tmF, k0, x.row0 + c * kChunk, &bars[c]);
+        }
+        if (rem) {  // tail rows through the one-row box
+            mbar_expect_tx(&bars[nfull], uint32_t(rem * W * sizeof(T)));
+            for (int r = 0; r < rem; ++r)
+                tma_load_2d(slab + size_t(nfull * kChunk + r) * W, tmF1, k0,
+                            x.row0 + nfull * kChunk + r, &bars[nfull]);
+        }
+    }
 
     __device__ __forceinline__ double* seg(int64_t k) const {
         return reinterpret_cast<double*>(smem + L.seg0 + (k & 1) * L.seg_b);
@@ -278,8 +300,6 @@ struct FusedTile {
             fwd_rows<T, W, kSegLen>(cf, col, dr, d, sr, sl, sx, kSegLen);
         else
             fwd_rows<T, W, kSegMax>(cf, col, dr, d, sr, sl, sx, x.len);
-        __syncwarp();
-        if ((x.tid & 31) == 0) mbar_arrive(fbar);  // this warp is done with the slab
         double* sk = seg(k);
         double* part = reinterpret_cast<double*>(smem + L.part);
         sk[x.tid] = double(d);         // d~ at the segment end
@@ -339,9 +359,9 @@ struct FusedTile {
         }
     }
 
-    // backward carries and back substitution of tile k (d~ from the d~
-    // buffer), streamed to X
-    __device__ __forceinline__ void backward(int64_t k) const {
+    // backward carries and back substitution of tile k (d~ from TMEM),
+    // streamed to X
+    __device__ __forceinline__ void backward(int64_t k, T (&dr)[kSegMax]) const {
         const int GSW = x.nc;
         double* sk = seg(k);
         const double* vals = reinterpret_cast<const double*>(smem + L.vals);
@@ -356,27 +376,18 @@ struct FusedTile {
                 xb = fma(sc.nu, xb, xa);
             }
         }
-        consumer_sync(x.nc);
+        cta_sync(x.nc);
         const int64_t k0 = (cluster_id + k * nclusters) * W;
         const T D = T(sk[x.tid]);
         const T xlt = T(xl);
         const T xn = T(sk[2 * GSW + x.tid]);
         if (k0 + x.lane < g.N && x.len > 0) {
             T* xp = X + k0 + x.lane + int64_t(x.b - 1) * g.ldx;  // last row first
-            const T* col = reinterpret_cast<const T*>(smem + L.dbuf) + x.lane + (x.a - x.row0) * W;
             if (x.len == kSegLen)
-                bwd_rows_smem<T, W, kSegLen>(cb, col, D, xlt, xn, xp, g.ldx, kSegLen);
+                bwd_rows<T, kSegLen>(cb, dr, D, xlt, xn, xp, g.ldx, kSegLen);
             else
-                bwd_rows_smem<T, W, kSegMax>(cb, col, D, xlt, xn, xp, g.ldx, x.len);
+                bwd_rows<T, kSegMax>(cb, dr, D, xlt, xn, xp, g.ldx, x.len);
         }
-    }
-
-    // park d~ of the forward-swept tile in the d~ buffer
-    __device__ __forceinline__ void park(const T (&dr)[kSegMax]) const {
-        T* col = reinterpret_cast<T*>(smem + L.dbuf) + x.lane + (x.a - x.row0) * W;
-#pragma unroll
-        for (int q = 0; q < kSegMax; ++q)
-            if (q < x.len) col[q * W] = dr[q];
     }
 
     __device__ __forceinline__ void stamp(int64_t k, int slot) const {
@@ -384,42 +395,44 @@ struct FusedTile {
         if (tr && k == 2 && x.tid == 0) tr[blockIdx.x * 16 + slot] = clock64();
     }
 
-    // iteration k: forward of tile k+1 (if any), then tile k to completion
+    // iteration k: tile k end to end. The slab is handed back to the
+    // producer right after the forward sweep (d~ stays in registers), so the
+    // HBM load of tile k+1 overlaps the exchange, the combination and the
+    // back substitution of tile k.
     __device__ __forceinline__ void step(int64_t k, int64_t ntl, T (&dr)[kSegMax]) const {
-        const bool next = k + 1 < ntl;
         stamp(k, 0);
-        if (next) forward(k + 1, dr);
+        forward(k, dr);
         stamp(k, 1);
-        consumer_sync(x.nc);
+        cta_sync(x.nc);
+        if (x.tid == 0 && k + 1 < ntl) {  // slab swept: stream the next tile into it
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(k + 1);
+        }
         double R, Lsum;
-        if (next) fwd_scan(k + 1, R, Lsum);
+        fwd_scan(k, R, Lsum);
+        // pushing tile k only after combining tile k-1 keeps two exchange
+        // buffers race-free (a peer's push of tile k+1 then needs this
+        // CTA's betas of tile k)
+        push(k, R, Lsum);
         stamp(k, 2);
         combine(k);
         stamp(k, 3);
-        // pushing tile k+1 only after combining tile k keeps two exchange
-        // buffers race-free (a peer's push of tile k+2 then needs this CTA's
-        // betas of tile k+1)
-        if (next) push(k + 1, R, Lsum);
-        consumer_sync(x.nc);
+        cta_sync(x.nc);
         stamp(k, 4);
-        backward(k);
+        backward(k, dr);
         stamp(k, 5);
-        consumer_sync(x.nc);  // d~ buffer free
-        if (next) park(dr);
         stamp(k, 6);
         unsigned long long* tr = g_trace;
         if (tr && x.tid == 0) {
             if (k == 0) tr[blockIdx.x * 16 + 10] = gtimer();
-            if (k + 1 == ntl) {
-                tr[blockIdx.x * 16 + 11] = gtimer();
-                tr[blockIdx.x * 16 + 12] = (unsigned long long)ntl;
-            }
+            tr[blockIdx.x * 16 + 11] = gtimer();
+            tr[blockIdx.x * 16 + 12] = (unsigned long long)(k + 1);
         }
     }
 };
 
 template <typename T, int W>
-__global__ void __launch_bounds__(kMaxThreads + 32) fused_r_kernel(
+__global__ void __launch_bounds__(kMaxThreads) fused_r_kernel(
     const __grid_constant__ CUtensorMap tmF, const __grid_constant__ CUtensorMap tmF1, T* X,
     FusedGeom g, const FusedFwd<T>* __restrict__ gff, const FusedBwd<T>* __restrict__ gfb,
     const SegCoef* __restrict__ gsegc, const double* __restrict__ gcmat) {
@@ -438,66 +451,16 @@ __global__ void __launch_bounds__(kMaxThreads + 32) fused_r_kernel(
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
     uint64_t* cbar = &bars[g.nchunks];      // plan tables
     uint64_t* xbar = &bars[g.nchunks + 1];  // [parity]: betas of a tile from every peer
-    uint64_t* fbar = &bars[g.nchunks + 3];  // slab released (one arrival per consumer warp)
-    const int nc = G * S * W;               // consumer threads; one producer warp follows
+    const int nc = G * S * W;               // threads
     const int tid = threadIdx.x;
     const int nrows = row1 - row0;
-    const int nfull = nrows / kChunk, rem = nrows % kChunk;
     FusedCtx x;
     x.tid = tid;
     x.nc = nc;
     x.row0 = row0;
     x.jb0 = crank * G - 1 < 0 ? 0 : crank * G - 1;  // combination rows [jb0, jb1)
     x.jb1 = crank * G + G < p ? crank * G + G : p;
-
-    if (tid == 0) {
-        for (int c = 0; c < nfull + (rem > 0); ++c) mbar_init(&bars[c], 1);
-        mbar_init(cbar, 1);
-        mbar_init(&xbar[0], 1);
-        mbar_init(&xbar[1], 1);
-        mbar_init(fbar, nc / 32);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    cluster.sync();  // peers may push into this CTA's exchange barriers from now on
-
-    if (tid >= nc) {
-        // ---- producer warp (one lane): plan tables once, then tile k into
-        // the slab as soon as the consumers swept tile k-1 out of it
-        if (tid != nc) return;
-        const uint32_t crows = uint32_t(row1 - crow0);
-        const uint32_t fwdb = crows * uint32_t(sizeof(FusedFwd<T>));
-        const uint32_t bwdb = crows * uint32_t(sizeof(FusedBwd<T>));
-        const uint32_t segb = uint32_t(G * S * sizeof(SegCoef));
-        const uint32_t cmb = uint32_t(x.jb1 > x.jb0 ? (x.jb1 - x.jb0) * 2 * P * sizeof(double) : 0);
-        mbar_expect_tx(cbar, fwdb + bwdb + segb + cmb);
-        bulk_load(smem + L.ff, gff + crow0, fwdb, cbar);
-        bulk_load(smem + L.fb, gfb + crow0, bwdb, cbar);
-        bulk_load(smem + L.segc, gsegc + crank * G * S, segb, cbar);
-        if (cmb) bulk_load(smem + L.cm, gcmat + size_t(x.jb0) * 2 * P, cmb, cbar);
-        T* slab = reinterpret_cast<T*>(smem);
-        for (int64_t k = 0; k < ntl; ++k) {
-            if (k > 0) {
-                mbar_wait(fbar, uint32_t(k - 1) & 1u);
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            }
-            const int k0 = int((cluster_id + k * nclusters) * W);
-            constexpr uint32_t box_bytes = uint32_t(W * kChunk * sizeof(T));
-            for (int c = 0; c < nfull; ++c) {
-                mbar_expect_tx(&bars[c], box_bytes);
-                tma_load_2d(slab + size_t(c) * kChunk * W, &tmF, k0, row0 + c * kChunk, &bars[c]);
-            }
-            if (rem) {  // tail rows through the one-row box
-                mbar_expect_tx(&bars[nfull], uint32_t(rem * W * sizeof(T)));
-                for (int r = 0; r < rem; ++r)
-                    tma_load_2d(slab + size_t(nfull * kChunk + r) * W, &tmF1, k0,
-                                row0 + nfull * kChunk + r, &bars[nfull]);
-            }
-        }
-        return;
-    }
-
-    // ---- consumers: thread -> (block j, segment sg, rhs lane)
+    // thread -> (block j, segment sg, rhs lane)
     x.lane = tid % W;
     const int h = tid / W;
     x.j = h / S;
@@ -517,19 +480,34 @@ __global__ void __launch_bounds__(kMaxThreads + 32) fused_r_kernel(
                              reinterpret_cast<const FusedBwd<T>*>(smem + L.fb) - crow0 + x.a,
                              reinterpret_cast<const SegCoef*>(smem + L.segc) - crank * G * S,
                              reinterpret_cast<const double*>(smem + L.cm),
-                             bars, xbar, fbar, crank, C, cluster_id, nclusters, X};
-    mbar_wait(cbar, 0);
-    if (ntl == 0) return;
+                             bars, xbar, crank, C, cluster_id, nclusters, X,
+                             &tmF, &tmF1, nrows / kChunk, nrows % kChunk};
 
-    T dr[kSegMax];
-    ft.forward(0, dr);
-    ft.park(dr);
-    consumer_sync(nc);
-    {
-        double R, Lsum;
-        ft.fwd_scan(0, R, Lsum);
-        ft.push(0, R, Lsum);
+    if (tid == 0) {
+        for (int c = 0; c < ft.nfull + (ft.rem > 0); ++c) mbar_init(&bars[c], 1);
+        mbar_init(cbar, 1);
+        mbar_init(&xbar[0], 1);
+        mbar_init(&xbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    __syncthreads();
+    cluster.sync();  // peers may push into this CTA's exchange barriers from now on
+    if (tid == 0) {
+        // plan tables once (small, L2-resident), then the first tile
+        const uint32_t crows = uint32_t(row1 - crow0);
+        const uint32_t fwdb = crows * uint32_t(sizeof(FusedFwd<T>));
+        const uint32_t bwdb = crows * uint32_t(sizeof(FusedBwd<T>));
+        const uint32_t segb = uint32_t(G * S * sizeof(SegCoef));
+        const uint32_t cmb = uint32_t(x.jb1 > x.jb0 ? (x.jb1 - x.jb0) * 2 * P * sizeof(double) : 0);
+        mbar_expect_tx(cbar, fwdb + bwdb + segb + cmb);
+        bulk_load(smem + L.ff, gff + crow0, fwdb, cbar);
+        bulk_load(smem + L.fb, gfb + crow0, bwdb, cbar);
+        bulk_load(smem + L.segc, gsegc + crank * G * S, segb, cbar);
+        if (cmb) bulk_load(smem + L.cm, gcmat + size_t(x.jb0) * 2 * P, cmb, cbar);
+        if (ntl > 0) ft.issue(0);
+    }
+    mbar_wait(cbar, 0);
+    T dr[kSegMax];
     for (int64_t k = 0; k < ntl; ++k) ft.step(k, ntl, dr);
 }
 
@@ -553,11 +531,11 @@ struct Choice {
     size_t smem = 0;
 };
 
-// Row width of an RHS tile: 256 B (default) or 128 B (PSW_FUSED_ROW_BYTES).
+// Row width of an RHS tile: 128 B (default) or 256 B (PSW_FUSED_ROW_BYTES).
 int tile_row_bytes() {
     static int rb = [] {
         const char* e = std::getenv("PSW_FUSED_ROW_BYTES");
-        return (e && std::atoi(e) == 128) ? 128 : 256;
+        return (e && std::atoi(e) == 256) ? 256 : 128;
     }();
     return rb;
 }
@@ -648,16 +626,24 @@ int launch_w(const psw_plan* pl, const Choice& ch, const void* F, int64_t ldf, v
     const int64_t tiles = (N + W - 1) / W;
     g.ntiles = tiles;
     cudaLaunchConfig_t cfg = {};
-    cfg.blockDim = dim3(unsigned(ch.G * g.S * W + 32), 1, 1);  // + producer warp
+    cfg.blockDim = dim3(unsigned(ch.G * g.S * W), 1, 1);
     cfg.dynamicSmemBytes = ch.smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    PSW_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                      cudaSharedmemCarveoutMaxShared));
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = unsigned(ch.C);
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    // pack a cluster's CTAs onto as few SMs as occupancy allows (the default
+    // spread policy needs C distinct SMs of one GPC per cluster)
+    attr[1].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
+    attr[1].val.clusterSchedulingPolicyPreference =
+        std::getenv("PSW_FUSED_SPREAD") ? cudaClusterSchedulingPolicySpread
+                                        : cudaClusterSchedulingPolicyLoadBalancing;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     // persistent: as many clusters as can be co-resident (cached per config)
     static std::mutex mu;
     static std::vector<std::pair<std::array<int64_t, 5>, int>> cache;
