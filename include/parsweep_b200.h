@@ -139,18 +139,19 @@ int psw_solve_host(const psw_plan* plan, const void* F, int64_t ldf, void* X, in
 int64_t psw_last_launch_count(void);
 
 /* ---- multi-GPU row sharding (dichotomy across devices) ---------------- */
-/* The reference simulates message passing (runtime/run.hpp:30-35,93-94);
- * here each rank owns a contiguous slab of blocks of one global partition
- * and the only exchange is a sum of per-RHS coarse partial sums. Protocol:
- *   psw_shard_plan_create  (every rank, same global A and partition)
- *   psw_shard_forward      -> local forward sweep, writes d0 into X and the
- *                             coarse partial sums into `partials` (device,
- *                             psw_shard_partials_count(plan) * nrhs fp64)
- *   <all-reduce(sum) of `partials` across ranks: NCCL / torch.distributed>
- *   psw_shard_backward     -> coarse + local dichotomy and back substitution.
- * Rank r owns blocks [r*P/G, (r+1)*P/G) (P = p+1 must be divisible by G, both
- * powers of two), i.e. rows of those blocks; F/X hold only the owned rows
- * (row offset psw_shard_row_offset). */
+/* The reference simulates message passing (runtime/run.hpp:30-35,93-94) with
+ * logical PEs; here the PEs are GPUs. Rank r of `world` owns the blocks
+ * [r*P/world, (r+1)*P/world) of ONE global partition (P = p+1 must be
+ * divisible by world) and the rows of those blocks; F/X hold only the owned
+ * rows, layout R (row offset psw_shard_row_offset, psw_shard_rows rows).
+ * The dichotomy combination is linear in the betas, so each rank forms its
+ * share of every boundary value and the only exchange is one sum:
+ *   psw_shard_forward   local forward sweep + betas; writes d0 into X and the
+ *                       rank's partial boundary values into `partials`
+ *                       (device fp64, p x nrhs, [j * nrhs + k])
+ *   <all-reduce(sum) of `partials` over the ranks: NCCL / torch.distributed>
+ *   psw_shard_backward  back substitution of the owned blocks with the
+ *                       reduced boundary values. */
 int psw_shard_plan_create(psw_plan** out, int64_t n, const double* sub, const double* diag,
                           const double* sup, int64_t p, const int64_t* boundaries, int dtype,
                           int device, int rank, int world);
@@ -161,6 +162,14 @@ int psw_shard_forward(const psw_plan* plan, const void* F, int64_t ldf, void* X,
                       int64_t nrhs, double* partials, void* stream);
 int psw_shard_backward(const psw_plan* plan, void* X, int64_t ldx, int64_t nrhs,
                        const double* partials, void* stream);
+
+/* Host-only (no GPU needed): the p x 2P combination matrix of the partition
+ * (row j = [MR[j][0..P) | ML[j][0..P)]), i.e. the action of solve_boundaries
+ * (dichotomy/boundary_solve.hpp:96-121) on unit betas: boundary value
+ * v_j = sum_t MR[j][t] right[t] + ML[j][t] left[t]. Used by the FUSED kernel
+ * and the row-sharded exchange. */
+int psw_combine_matrix(int64_t n, const double* sub, const double* diag, const double* sup,
+                       int64_t p, const int64_t* boundaries, double* out);
 
 /* ---- utilities (benchmark / test data) -------------------------------- */
 /* Fill a device buffer with the seeded counter-based uniform generator

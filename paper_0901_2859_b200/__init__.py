@@ -287,14 +287,15 @@ class Plan:
     dichotomy/preliminary.hpp:53-101, restricted to what the kernels read)."""
 
     def __init__(self, A: TridiagMatrix, part: Partition, dtype: int = F64, device: int = 0,
-                 rank: int = 0, world: int = 1):
+                 rank: int | None = None, world: int | None = None):
         L = lib()
         A.validate() if A.n() >= 2 else None
         self.n = A.n()
         self.part = Partition(part.n, list(part.boundaries))
         self.dtype = dtype
         self.device = device
-        self.rank, self.world = rank, world
+        shard = world is not None
+        self.rank, self.world = (rank or 0), (world or 1)
         b = np.ascontiguousarray(part.boundaries, dtype=np.int64)
         if b.size == 0:
             b = np.zeros(1, np.int64)
@@ -303,10 +304,10 @@ class Plan:
         args = (C.byref(h), self.n, A.sub.ctypes.data_as(dp), A.diag.ctypes.data_as(dp),
                 A.super.ctypes.data_as(dp), len(part.boundaries),
                 b.ctypes.data_as(C.POINTER(C.c_int64)), dtype, device)
-        if world == 1:
+        if not shard:
             _check(L.psw_plan_create(*args))
-        else:
-            _check(L.psw_shard_plan_create(*args, rank, world))
+        else:  # row shard of a multi-GPU solve (psw_shard_*)
+            _check(L.psw_shard_plan_create(*args, self.rank, self.world))
         self._h = h
         info = _Info()
         _check(L.psw_plan_info(self._h, C.byref(info)))

@@ -208,15 +208,17 @@ int validate_inputs(int64_t n, const double* sub, const double* diag, const doub
 
 // Builds the plan for a (possibly sharded) solve. Rank/world select the
 // owned block range for psw_shard_*; world == 1 is the full plan.
+// `cmat_host` != nullptr: host-only run (no device needed) that stops after
+// the preliminary and returns the combination matrix (psw_combine_matrix).
 int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
                const double* sup, int64_t p, const int64_t* bnd, int dtype, int device,
-               int rank, int world);
+               int rank, int world, std::vector<double>* cmat_host = nullptr, bool shard = false);
 
-int build_shard_tables(psw_plan* pl);  // psw_shard.cpp
+int build_shard_tables(psw_plan* pl, const std::vector<double>& cmat);  // psw_shard.cu
 
 int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
                const double* sup, int64_t p, const int64_t* bnd, int dtype, int device,
-               int rank, int world) {
+               int rank, int world, std::vector<double>* cmat_host, bool shard) {
     clear_error();
     if (!out) {
         set_error(PSW_INVALID_ARGUMENT, "null plan output");
@@ -228,6 +230,11 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
         return PSW_INVALID_ARGUMENT;
     }
     if (int rc = validate_inputs(n, sub, diag, sup, p, bnd)) return rc;
+    if (world < 1 || rank < 0 || rank >= world || (p + 1) % world != 0) {
+        set_error(PSW_INVALID_ARGUMENT,
+                  "row sharding needs 0 <= rank < world and P = p+1 blocks divisible by world");
+        return PSW_INVALID_ARGUMENT;
+    }
     for (int64_t i = 0; i + 1 < n; ++i)
         if (sub[i] != sup[i]) {
             set_error(PSW_NOT_SUPPORTED,
@@ -393,6 +400,11 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
     }
     int64_t terms = 0;
     pl->items = build_items(p, &terms, &pl->lvl_off);
+    if (cmat_host) {
+        *cmat_host = combine_matrix(pl, zr, zl);
+        delete pl;
+        return PSW_OK;
+    }
 
     // the device is only needed for the upload: host validation and the
     // preliminary (and its PivotBreakdown) come first, like the reference
@@ -418,7 +430,7 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
                                 : upload<float>(pl, rp, ma, gr, gl, w, alv, zr, zl);
     if (rc == PSW_OK && pl->uniform && world == 1)
         rc = build_fused_tables(pl, rp, ma, gr, gl, w, alv, combine_matrix(pl, zr, zl));
-    if (rc == PSW_OK && world > 1) rc = build_shard_tables(pl);
+    if (rc == PSW_OK && shard) rc = build_shard_tables(pl, combine_matrix(pl, zr, zl));
     cudaSetDevice(prev_dev);
     if (rc != PSW_OK) {
         free_plan(pl);
@@ -659,6 +671,16 @@ int psw_l2_flush(void* scratch, int64_t bytes, void* stream) {
 }
 
 }  // extern "C"
+
+extern "C" int psw_combine_matrix(int64_t n, const double* sub, const double* diag,
+                                  const double* sup, int64_t p, const int64_t* boundaries,
+                                  double* out) {
+    std::vector<double> M;
+    psw_plan* dummy = nullptr;
+    const int rc = psw::build_plan(&dummy, n, sub, diag, sup, p, boundaries, PSW_F64, 0, 0, 1, &M);
+    if (rc == PSW_OK && out) std::copy(M.begin(), M.end(), out);
+    return rc;
+}
 
 extern "C" int psw_debug_trace(void* device_buffer) {
     psw::clear_error();

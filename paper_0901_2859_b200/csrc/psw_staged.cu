@@ -31,17 +31,19 @@ __device__ __forceinline__ T ld_stream(const T* p) {
 
 
 // ---------------------------------------------------------------- layout R
+// Blocks t0 + blockIdx.y; F/X row 0 is global row row_off (row shards,
+// psw_shard.cu); betas land at [(t - t0) * N + k].
 template <typename T>
 __global__ void __launch_bounds__(kThreads) fwd_r_kernel(
     const T* F, int64_t ldf, T* X, int64_t ldx, int64_t N, const int32_t* __restrict__ blk,
     const FwdCoef<T>* __restrict__ cf, double* __restrict__ bl_out, double* __restrict__ br_out,
-    int p) {
-    const int t = blockIdx.y;
+    int p, int t0, int row_off) {
+    const int t = t0 + blockIdx.y;
     const int64_t k = int64_t(blockIdx.x) * kThreads + threadIdx.x;
     if (k >= N) return;
     const int s = blk[2 * t], e = blk[2 * t + 1];
-    const T* f = F + k;
-    T* x = X + k;
+    const T* f = F + k - int64_t(row_off) * ldf;  // f[q * ldf] = global row q
+    T* x = X + k - int64_t(row_off) * ldx;
     T d = T(0);
     double br = 0.0, bl = 0.0;
     int q = s;
@@ -66,21 +68,21 @@ __global__ void __launch_bounds__(kThreads) fwd_r_kernel(
         bl = madd_rn(bl, double(fv), double(c.gl));
         x[int64_t(q) * ldx] = d;
     }
-    if (t < p) br_out[int64_t(t) * N + k] = br;
-    if (t > 0) bl_out[int64_t(t) * N + k] = bl;
+    if (t < p) br_out[int64_t(t - t0) * N + k] = br;
+    if (t > 0) bl_out[int64_t(t - t0) * N + k] = bl;
 }
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads) bwd_r_kernel(
     T* X, int64_t ldx, int64_t N, const int32_t* __restrict__ blk,
-    const BwdCoef<T>* __restrict__ cb, const double* __restrict__ V, int p) {
-    const int t = blockIdx.y;
+    const BwdCoef<T>* __restrict__ cb, const double* __restrict__ V, int p, int t0, int row_off) {
+    const int t = t0 + blockIdx.y;
     const int64_t k = int64_t(blockIdx.x) * kThreads + threadIdx.x;
     if (k >= N) return;
     const int s = blk[2 * t], e = blk[2 * t + 1];
     const T xl = t > 0 ? T(V[int64_t(t - 1) * N + k]) : T(0);
     T xn = t < p ? T(V[int64_t(t) * N + k]) : T(0);
-    T* x = X + k;
+    T* x = X + k - int64_t(row_off) * ldx;
     int q = e - 1;
     for (; q - kUnroll + 1 >= s; q -= kUnroll) {
         T dv[kUnroll];
@@ -252,7 +254,7 @@ int launch_staged(const psw_plan* pl, const void* Fv, int64_t ldf, void* Xv, int
     if (layout == PSW_LAYOUT_R) {
         dim3 grid(unsigned((N + kThreads - 1) / kThreads), unsigned(pl->P));
         mark(ev, nev, 0, s);
-        fwd_r_kernel<T><<<grid, kThreads, 0, s>>>(F, ldf, X, ldx, N, pl->d_blk, cf, bl, br, p);
+        fwd_r_kernel<T><<<grid, kThreads, 0, s>>>(F, ldf, X, ldx, N, pl->d_blk, cf, bl, br, p, 0, 0);
         ++launches;
         mark(ev, nev, 1, s);
         if (p > 0) {
@@ -261,7 +263,7 @@ int launch_staged(const psw_plan* pl, const void* Fv, int64_t ldf, void* Xv, int
             ++launches;
         }
         mark(ev, nev, 2, s);
-        bwd_r_kernel<T><<<grid, kThreads, 0, s>>>(X, ldx, N, pl->d_blk, cb, V, p);
+        bwd_r_kernel<T><<<grid, kThreads, 0, s>>>(X, ldx, N, pl->d_blk, cb, V, p, 0, 0);
         ++launches;
         mark(ev, nev, 3, s);
     } else {
@@ -313,6 +315,73 @@ int solve_staged(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_
                  : launch_staged<float>(pl, F, ldf, X, ldx, N, layout, s, bl, br, V, events, nevents);
     if (scratch) cudaFreeAsync(scratch, s);
     return rc;
+}
+
+// ------------------------------------------------------------ row shards
+namespace {
+// partials[j * N + k] = sum over the rank's blocks t of
+//   MR[j][t] right_t[k] + ML[j][t] left_t[k]        (combination matrix rows)
+__global__ void __launch_bounds__(kThreads) shard_partials_kernel(
+    const double* __restrict__ bl, const double* __restrict__ br, int64_t N, int p, int P,
+    int t0, int t1, const double* __restrict__ cmat, double* __restrict__ out) {
+    const int j = blockIdx.y;
+    const int64_t k = int64_t(blockIdx.x) * kThreads + threadIdx.x;
+    if (k >= N) return;
+    const double* Mr = cmat + int64_t(j) * 2 * P;
+    double s = 0.0;
+    for (int t = t0; t < t1; ++t) {
+        const int64_t i = int64_t(t - t0) * N + k;
+        if (t < p) s = fma(Mr[t], br[i], s);
+        if (t > 0) s = fma(Mr[P + t], bl[i], s);
+    }
+    out[int64_t(j) * N + k] = s;
+}
+}  // namespace
+
+int shard_forward(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_t ldx,
+                  int64_t N, double* partials, cudaStream_t s) {
+    const int t0 = int(pl->blk0), nb = int(pl->blk1 - pl->blk0), p = int(pl->p);
+    double* scratch = nullptr;
+    PSW_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&scratch), sizeof(double) * 2 * nb * N, s));
+    double* bl = scratch;
+    double* br = scratch + int64_t(nb) * N;
+    const dim3 grid(unsigned((N + kThreads - 1) / kThreads), unsigned(nb));
+    const int row_off = int(pl->row0);
+    if (pl->dtype == PSW_F64)
+        fwd_r_kernel<double><<<grid, kThreads, 0, s>>>(
+            static_cast<const double*>(F), ldf, static_cast<double*>(X), ldx, N, pl->d_blk,
+            static_cast<const FwdCoef<double>*>(pl->d_fwd), bl, br, p, t0, row_off);
+    else
+        fwd_r_kernel<float><<<grid, kThreads, 0, s>>>(
+            static_cast<const float*>(F), ldf, static_cast<float*>(X), ldx, N, pl->d_blk,
+            static_cast<const FwdCoef<float>*>(pl->d_fwd), bl, br, p, t0, row_off);
+    int64_t launches = 1;
+    if (p > 0) {
+        shard_partials_kernel<<<dim3(grid.x, unsigned(p)), kThreads, 0, s>>>(
+            bl, br, N, p, int(pl->P), t0, t0 + nb, pl->d_cmat, partials);
+        ++launches;
+    }
+    cudaFreeAsync(scratch, s);
+    PSW_CUDA_TRY(cudaGetLastError());
+    note_launches(launches);
+    return PSW_OK;
+}
+
+int shard_backward(const psw_plan* pl, void* X, int64_t ldx, int64_t N, const double* V,
+                   cudaStream_t s) {
+    const int t0 = int(pl->blk0), nb = int(pl->blk1 - pl->blk0), p = int(pl->p);
+    const dim3 grid(unsigned((N + kThreads - 1) / kThreads), unsigned(nb));
+    if (pl->dtype == PSW_F64)
+        bwd_r_kernel<double><<<grid, kThreads, 0, s>>>(
+            static_cast<double*>(X), ldx, N, pl->d_blk,
+            static_cast<const BwdCoef<double>*>(pl->d_bwd), V, p, t0, int(pl->row0));
+    else
+        bwd_r_kernel<float><<<grid, kThreads, 0, s>>>(
+            static_cast<float*>(X), ldx, N, pl->d_blk,
+            static_cast<const BwdCoef<float>*>(pl->d_bwd), V, p, t0, int(pl->row0));
+    PSW_CUDA_TRY(cudaGetLastError());
+    note_launches(1);
+    return PSW_OK;
 }
 
 // ------------------------------------------------------------ data fill
