@@ -49,6 +49,10 @@ def _args():
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="cpu_baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="rhs", choices=["rhs", "rows"],
+                    help="multi-GPU: rhs = every rank its own RHS batch (weak scaling); rows = "
+                         "one system sharded by rows over the ranks + one NCCL all-reduce "
+                         "(strong scaling, BASELINE C3)")
     return ap.parse_args()
 
 
@@ -252,6 +256,8 @@ def main():
         cfg = cfg.with_(layout=args.layout)
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.mode == "rows":
+        return run_rows(args, cfg)
 
     import torch
     import paper_0901_2859_b200 as psw
@@ -370,6 +376,85 @@ def main():
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def run_rows(args, cfg):
+    """Row-sharded strong scaling: rank r owns the rows of
+    blocks [r P/G, (r+1) P/G) of every RHS; one NCCL all-reduce of p values per
+    RHS per solve. Timed region = forward + all-reduce + backward, max over ranks."""
+    import torch
+    import paper_0901_2859_b200 as psw
+    from paper_0901_2859_b200.configs import uniform
+    from paper_0901_2859_b200.sharded import ShardedSolver
+    rank, world, local = _dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % _port(), rank=0,
+                                world_size=1)
+    dev = torch.device("cuda", local)
+    a, b = cfg.matrix_ab(0)
+    A = psw.TridiagMatrix.symmetric(a, b)
+    part = psw.decompose(cfg.n, cfg.P).induced_partition()
+    dt = psw.F64 if cfg.dtype == "f64" else psw.F32
+    tdt = torch.float64 if dt == psw.F64 else torch.float32
+    solver = ShardedSolver(A, part, dtype=dt, device=local)
+    sh = solver.shard
+    F = torch.empty((sh.rows, cfg.nrhs), dtype=tdt, device=dev)
+    psw.fill_uniform(F, 3 + rank, -1.0, 1.0)
+    X = torch.empty_like(F)
+    flush = torch.empty(2 * torch.cuda.get_device_properties(dev).L2_cache_size // 4 + 1,
+                        dtype=torch.float32, device=dev)
+    for _ in range(args.warmup):
+        solver.solve(F, X)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            psw.l2_flush(flush)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            solver.solve(F, X)
+            e1.record()
+            ms.append((e0, e1))
+        torch.cuda.synchronize()
+    total = sum(a_.elapsed_time(b_) for a_, b_ in ms)
+    t = torch.tensor([total], dtype=torch.float64, device=dev if world > 1 else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total = float(t.item())
+    units = cfg.nrhs * cfg.n
+    value = units * args.steps / (total / 1e3)
+    peak, peak_kind = _peaks()
+    es = 8 if dt == psw.F64 else 4
+    per_gpu = (sh.rows * cfg.nrhs * 2 * es) / (total / args.steps / 1e3) / 1e9
+    line = {
+        "metric": "rhs_unknowns_per_s", "value": value, "unit": "unknowns/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype,
+        "data": "synthetic (seeded counter-based generator, BASELINE configs)",
+        "config": dict(_config_dict(cfg), parallelism=f"row-shard x{world} (NCCL all-reduce of "
+                       f"{cfg.P - 1} values/RHS)", path="staged shard kernels"),
+        "roofline": {"bound": "hbm", "achieved": per_gpu, "peak": peak, "unit": "GB/s",
+                     "frac": per_gpu / peak, "traffic": None, "kernel": "shard solve (rank 0)",
+                     "peak_kind": peak_kind},
+        "comm_bytes_per_step": solver.comm_bytes_per_rhs * cfg.nrhs,
+        "gpu_launches": 3 * args.steps, "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
+def _port():
+    import socket
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        return s_.getsockname()[1]
 
 
 def _e2e(psw, plan, cfg, F, layout, dt, args, dist, dev, world):
