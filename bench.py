@@ -45,7 +45,7 @@ def _args():
     ap.add_argument("--config", default="C1")
     ap.add_argument("--P", type=int, default=None, help="override the partition count")
     ap.add_argument("--layout", default=None, choices=[None, "R", "S"])
-    ap.add_argument("--path", default="auto", choices=["auto", "staged", "fused"])
+    ap.add_argument("--path", default="auto", choices=["auto", "staged", "fused", "pipe"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="cpu_baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -292,13 +292,15 @@ def main():
     X = torch.empty_like(F)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(2 * l2 // 4 + 1, dtype=torch.float32, device=dev)
-    path = {"auto": psw.PATH_AUTO, "staged": psw.PATH_STAGED, "fused": psw.PATH_FUSED}[args.path]
+    path = {"auto": psw.PATH_AUTO, "staged": psw.PATH_STAGED, "fused": psw.PATH_FUSED,
+            "pipe": psw.PATH_PIPE}[args.path]
 
     # discover the kernel count of the chosen path
     plan.solve(F, X, layout=layout, path=path)
     torch.cuda.synchronize()
     nk = psw.last_launch_count()
-    names = ["fused"] if nk == 1 else (["fwd", "combine", "bwd"] if nk == 3 else ["fwd", "bwd"])
+    taken = psw.last_path()
+    names = [taken] if nk == 1 else (["fwd", "combine", "bwd"] if nk == 3 else ["fwd", "bwd"])
 
     def step(events=None):
         psw.l2_flush(flush)
@@ -338,6 +340,7 @@ def main():
     kname = names[j] if j < len(names) else f"k{j}"
     coef = (2 * cfg.n - 1) * es
     alg = {"fused": units * 2 * es + coef,      # read F, write X
+           "pipe": units * 2 * es + coef,       # read F, write X (d round trip in L2)
            "fwd": units * 2 * es + coef,        # read F, write d0
            "bwd": units * 2 * es + coef,        # read d0, write X
            "combine": 2 * cfg.P * cfg.nrhs * 8 + max(cfg.P - 1, 1) * cfg.nrhs * 8}[kname]
@@ -350,7 +353,7 @@ def main():
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": cfg.dtype, "data": "synthetic (seeded counter-based generator, BASELINE configs)",
         "config": dict(_config_dict(cfg), parallelism=f"rhs-shard x{world}" if world > 1 else "1 gpu",
-                       path=args.path, kernels=names),
+                       path=taken, kernels=names),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": _traffic(cfg.name, kname),
                      "kernel": kname, "kernel_ms": kern_ms[j], "peak_kind": peak_kind,

@@ -48,7 +48,12 @@ typedef enum psw_layout { PSW_LAYOUT_R = 0, PSW_LAYOUT_S = 1 } psw_layout;
 /* Solve-path selection (psw_solve_ex). AUTO picks the fastest path that
  * supports the plan/shape: FUSED keeps every RHS tile resident on chip and
  * reads F once; STAGED is the general three-kernel path. */
-typedef enum psw_path { PSW_PATH_AUTO = 0, PSW_PATH_STAGED = 1, PSW_PATH_FUSED = 2 } psw_path;
+typedef enum psw_path {
+    PSW_PATH_AUTO = 0,
+    PSW_PATH_STAGED = 1,
+    PSW_PATH_FUSED = 2,
+    PSW_PATH_PIPE = 3
+} psw_path;
 
 typedef struct psw_plan psw_plan;
 
@@ -137,6 +142,8 @@ int psw_solve_host(const psw_plan* plan, const void* F, int64_t ldf, void* X, in
 /* Device kernels launched by the last successful psw_solve* on this thread
  * (launch accounting for the benchmark). */
 int64_t psw_last_launch_count(void);
+/* psw_path taken by the last psw_solve/psw_solve_ex on this thread (0 before any). */
+int psw_last_path(void);
 
 /* ---- multi-GPU row sharding (dichotomy across devices) ---------------- */
 /* The reference simulates message passing (runtime/run.hpp:30-35,93-94) with
@@ -182,7 +189,9 @@ int psw_fill_normal(void* dst, int dtype, int64_t count, uint64_t seed, uint64_t
                     void* stream);
 /* Profiling aid: when `device_buffer` is non-NULL the FUSED kernel writes,
  * per CTA, 16 uint64 slots: clock64() at its phase boundaries (0..8) and
- * %globaltimer at start/end (14, 15). NULL disables tracing (default). */
+ * %globaltimer at start/end (14, 15); the PIPE kernel writes 4 uint64 per
+ * work-item ticket: start, dependencies met, end (%globaltimer ns) and
+ * (item type << 32 | SM id). NULL disables tracing (default). */
 int psw_debug_trace(void* device_buffer);
 
 /* Write `bytes` of zeros+index pattern over a scratch buffer (L2 flush). */

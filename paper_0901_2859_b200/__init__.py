@@ -32,7 +32,7 @@ import numpy as np
 __all__ = [
     "TridiagMatrix", "Partition", "Decomposition", "decompose", "compute_preliminary", "Plan",
     "solve_batch", "SolverError", "PivotBreakdown", "TooManyPEs", "NotSupported", "CudaError",
-    "F64", "F32", "LAYOUT_R", "LAYOUT_S", "PATH_AUTO", "PATH_STAGED", "PATH_FUSED", "lib",
+    "F64", "F32", "LAYOUT_R", "LAYOUT_S", "PATH_AUTO", "PATH_STAGED", "PATH_FUSED", "PATH_PIPE", "last_path", "lib",
     "library_path",
 ]
 
@@ -41,7 +41,7 @@ LIB_PATH = os.path.join(HERE, "_lib", "libparsweep_b200.so")
 
 F64, F32 = 0, 1
 LAYOUT_R, LAYOUT_S = 0, 1
-PATH_AUTO, PATH_STAGED, PATH_FUSED = 0, 1, 2
+PATH_AUTO, PATH_STAGED, PATH_FUSED, PATH_PIPE = 0, 1, 2, 3
 OK, INVALID_ARGUMENT, PIVOT_BREAKDOWN, TOO_MANY_PES, NOT_SUPPORTED, CUDA_ERROR, NCCL_ERROR, OOM = range(8)
 
 
@@ -91,6 +91,8 @@ def lib() -> C.CDLL:
         L.psw_last_error_message.restype = C.c_char_p
         L.psw_last_error_index.restype = C.c_int64
         L.psw_last_launch_count.restype = C.c_int64
+        L.psw_last_path.restype = C.c_int
+        L.psw_debug_trace.argtypes = [vp]
         L.psw_decompose.argtypes = [C.c_int64, C.c_int64, i64]
         L.psw_partition_validate.argtypes = [C.c_int64, C.c_int64, i64]
         L.psw_plan_create.argtypes = [C.POINTER(vp), C.c_int64, d, d, d, C.c_int64, i64, C.c_int, C.c_int]
@@ -141,6 +143,14 @@ def _check(rc: int):
 
 def last_launch_count() -> int:
     return int(lib().psw_last_launch_count())
+
+
+PATH_NAMES = {PATH_STAGED: "staged", PATH_FUSED: "fused", PATH_PIPE: "pipe"}
+
+
+def last_path() -> str:
+    """Name of the solve path the last solve on this thread took."""
+    return PATH_NAMES.get(int(lib().psw_last_path()), "none")
 
 
 # ---------------------------------------------------------------- types

@@ -38,6 +38,7 @@
 
 #include "psw_device.cuh"
 #include "psw_internal.h"
+#include "psw_tma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -49,51 +50,6 @@ constexpr int kMaxCluster = 16;
 constexpr int kMaxThreads = 256;  // threads per CTA
 constexpr size_t kSmemTarget = 110 * 1024;  // >= 2 CTAs per SM
 constexpr size_t kSmemMax = 200 * 1024;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-    const uint32_t a = smem_u32(bar);
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-            " selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(done)
-            : "r"(a), "r"(phase)
-            : "memory");
-    }
-}
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
-                                            uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-        : "memory");
-}
-
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
-                                          uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
 
 // Optional per-CTA phase trace (psw_debug_trace): 16 slots per CTA and
 // iteration 0, clock64() at phase boundaries, %globaltimer at start/end.
@@ -512,20 +468,6 @@ __global__ void __launch_bounds__(kMaxThreads) fused_r_kernel(
 }
 
 // ---------------------------------------------------------------- host side
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-                cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    });
-    return fn;
-}
-
 struct Choice {
     int W = 0, G = 0, C = 0, rows_alloc = 0, nchunks = 0;
     size_t smem = 0;
@@ -578,7 +520,7 @@ Choice choose(const psw_plan* pl, int es) {
 
 bool encode_maps(CUtensorMap* tm, CUtensorMap* tm1, const void* F, int64_t N, int64_t n,
                  int64_t ldf, int es, int W) {
-    auto encode = encode_fn();
+    auto encode = tensor_map_encoder();
     if (!encode) {
         set_error(PSW_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
         return false;
@@ -720,13 +662,28 @@ int build_fused_tables(psw_plan* pl, const std::vector<double>& rp, const std::v
         pl->info.device_bytes += int64_t(sizeof(double) * cmat.size());
     }
     if (!pl->uniform || m < 1) return PSW_OK;
-    const int S = int((m + kSegLen - 1) / kSegLen);
-    pl->nseg = S;
+    // Segmentation of every block into runs of at most kSegLen + 1 rows:
+    // uniform partitions use S = ceil(m / kSegLen) segments for every block
+    // (the FUSED kernel's thread map; block sizes m-1, m, m+1); others use
+    // S_t = max(1, ceil((m_t - 1) / kSegLen)). The last segment of a block
+    // absorbs the remainder (<= kSegLen + 1 rows).
+    std::vector<int32_t> off(P + 1, 0);
+    for (int64_t t = 0; t < P; ++t) {
+        const int64_t mt = pl->blk[2 * t + 1] - pl->blk[2 * t];
+        const int64_t St = pl->uniform ? (m + kSegLen - 1) / kSegLen
+                                       : std::max<int64_t>(1, (mt - 1 + kSegLen - 1) / kSegLen);
+        off[t + 1] = off[t] + int32_t(St);
+    }
+    pl->nseg = pl->uniform ? int((m + kSegLen - 1) / kSegLen) : 0;
+    pl->seg_off = off;
+    const int64_t NS = off[P];
     std::vector<FusedFwd<double>> ff(n);
     std::vector<FusedBwd<double>> fb(n);
-    std::vector<SegCoef> seg(size_t(P) * S);
+    std::vector<SegCoef> seg(NS);
+    std::vector<SegDesc> desc(NS);
     for (int64_t t = 0; t < P; ++t) {
         const int64_t s = pl->blk[2 * t], e = pl->blk[2 * t + 1];
+        const int S = off[t + 1] - off[t];
         for (int sg = 0; sg < S; ++sg) {
             int64_t a = std::min(e, s + int64_t(sg) * kSegLen);
             int64_t b = sg == S - 1 ? e : std::min(e, a + kSegLen);
@@ -739,9 +696,15 @@ int build_fused_tables(psw_plan* pl, const std::vector<double>& rp, const std::v
                 k2 += lam * w[q];
                 lam *= al[q];                       // prod_{u=a..q} al_u
             }
-            seg[size_t(t) * S + sg] = {mu, k1, k2, lam};
+            seg[off[t] + sg] = {mu, k1, k2, lam};
+            desc[off[t] + sg] = {int32_t(a), int32_t(b), int32_t(t), 0};
         }
     }
+    PSW_CUDA_TRY(cudaMalloc(&pl->d_segdesc, sizeof(SegDesc) * NS));
+    PSW_CUDA_TRY(cudaMemcpy(pl->d_segdesc, desc.data(), sizeof(SegDesc) * NS, cudaMemcpyHostToDevice));
+    PSW_CUDA_TRY(cudaMalloc(&pl->d_segoff, sizeof(int32_t) * (P + 1)));
+    PSW_CUDA_TRY(cudaMemcpy(pl->d_segoff, off.data(), sizeof(int32_t) * (P + 1), cudaMemcpyHostToDevice));
+    pl->info.device_bytes += int64_t(sizeof(SegDesc) * NS + sizeof(int32_t) * (P + 1));
     return pl->dtype == PSW_F64 ? upload_fused<double>(pl, ff, fb, seg)
                                 : upload_fused<float>(pl, ff, fb, seg);
 }
@@ -749,7 +712,7 @@ int build_fused_tables(psw_plan* pl, const std::vector<double>& rp, const std::v
 int set_trace(void* buf) {
     unsigned long long* p = static_cast<unsigned long long*>(buf);
     PSW_CUDA_TRY(cudaMemcpyToSymbol(g_trace, &p, sizeof(p)));
-    return PSW_OK;
+    return set_pipe_trace(buf);
 }
 
 bool fused_supported(const psw_plan* pl, int layout, int64_t N, const void* F, int64_t ldf) {

@@ -63,6 +63,7 @@ struct CombineItem {
 // sum_q lam_q c_q = Lam + D_{a-1} K1 + x_l K2 (Lam = sum lam_q d~_q is
 // accumulated by the forward sweep, K1 = sum lam mu, K2 = sum lam w).
 constexpr int kSegLen = 32;
+constexpr int kCoefPad = 64;  // zero rows appended to FwdCoef/BwdCoef tables
 template <typename T>
 struct alignas(16) FusedFwd {
     T rp, ma, gr, gl, lam, pad;
@@ -73,6 +74,9 @@ struct alignas(16) FusedBwd {
 };
 struct alignas(32) SegCoef {
     double mu_end, k1, k2, nu;
+};
+struct SegDesc {  // rows [a, b) of block t
+    int32_t a, b, t, pad;
 };
 
 }  // namespace psw
@@ -104,7 +108,10 @@ struct psw_plan {
     double* d_cmat = nullptr;          // [p][2P] combination matrix (see build_fused_tables)
     void* d_ffwd = nullptr;            // FusedFwd<T>[n]
     void* d_fbwd = nullptr;            // FusedBwd<T>[n]
-    psw::SegCoef* d_seg = nullptr;     // [P][nseg]
+    psw::SegCoef* d_seg = nullptr;     // per segment (block-major, see seg_off)
+    psw::SegDesc* d_segdesc = nullptr; // per segment rows / block
+    int32_t* d_segoff = nullptr;       // [P+1] first segment of every block
+    std::vector<int32_t> seg_off;      // host copy
 
     // multi-GPU row shard (psw_shard_*); world == 1 for a full plan
     int rank = 0, world = 1;
@@ -139,6 +146,10 @@ int build_fused_tables(psw_plan* pl, const std::vector<double>& rp, const std::v
 // no FP contraction).
 std::vector<double> combine_matrix(const psw_plan* pl, const std::vector<double>& zr,
                                    const std::vector<double>& zl);
+bool pipe_supported(const psw_plan* plan, int layout, int64_t N, const void* F, int64_t ldf,
+                    const void* X, int64_t ldx);
+int solve_pipe(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx, int64_t N,
+               int layout, cudaStream_t s, void** events, int nevents);
 int solve_fused(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
                 int64_t N, int layout, cudaStream_t s, void** events, int nevents);
 // records events[i] (if present) on s
@@ -149,7 +160,8 @@ int shard_forward(const psw_plan* plan, const void* F, int64_t ldf, void* X, int
                   int64_t N, double* partials, cudaStream_t s);
 int shard_backward(const psw_plan* plan, void* X, int64_t ldx, int64_t N, const double* partials,
                    cudaStream_t s);
-int set_trace(void* buf);  // psw_debug_trace (FUSED kernel phase stamps)
+int set_trace(void* buf);  // psw_debug_trace (FUSED kernel phase stamps, PIPE item trace)
+int set_pipe_trace(void* buf);
 int fill_uniform(void* dst, int dtype, int64_t count, uint64_t seed, uint64_t offset, double lo,
                  double hi, cudaStream_t s);
 int fill_normal(void* dst, int dtype, int64_t count, uint64_t seed, uint64_t offset,

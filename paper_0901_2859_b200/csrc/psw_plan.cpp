@@ -18,6 +18,10 @@
 
 #include "psw_internal.h"
 
+namespace {
+thread_local int t_last_path = 0;  // psw_last_path
+}  // namespace
+
 namespace psw {
 
 namespace {
@@ -128,16 +132,18 @@ int upload(psw_plan* pl, const std::vector<double>& rp, const std::vector<double
            const std::vector<double>& w, const std::vector<double>& al,
            const std::vector<double>& zr, const std::vector<double>& zl) {
     const int64_t n = pl->n, p = pl->p;
-    std::vector<FwdCoef<T>> fwd(n);
-    std::vector<BwdCoef<T>> bwd(n);
+    // kCoefPad zero rows past n: the PIPE path bulk-copies whole 32-row stages
+    const int64_t na = n + kCoefPad;
+    std::vector<FwdCoef<T>> fwd(na, FwdCoef<T>{});
+    std::vector<BwdCoef<T>> bwd(na, BwdCoef<T>{});
     for (int64_t q = 0; q < n; ++q) {
         fwd[q] = {T(rp[q]), T(ma[q]), T(gr[q]), T(gl[q])};
         bwd[q] = {T(w[q]), T(al[q])};
     }
-    PSW_CUDA_TRY(cudaMalloc(&pl->d_fwd, sizeof(FwdCoef<T>) * n));
-    PSW_CUDA_TRY(cudaMalloc(&pl->d_bwd, sizeof(BwdCoef<T>) * n));
-    PSW_CUDA_TRY(cudaMemcpy(pl->d_fwd, fwd.data(), sizeof(FwdCoef<T>) * n, cudaMemcpyHostToDevice));
-    PSW_CUDA_TRY(cudaMemcpy(pl->d_bwd, bwd.data(), sizeof(BwdCoef<T>) * n, cudaMemcpyHostToDevice));
+    PSW_CUDA_TRY(cudaMalloc(&pl->d_fwd, sizeof(FwdCoef<T>) * na));
+    PSW_CUDA_TRY(cudaMalloc(&pl->d_bwd, sizeof(BwdCoef<T>) * na));
+    PSW_CUDA_TRY(cudaMemcpy(pl->d_fwd, fwd.data(), sizeof(FwdCoef<T>) * na, cudaMemcpyHostToDevice));
+    PSW_CUDA_TRY(cudaMemcpy(pl->d_bwd, bwd.data(), sizeof(BwdCoef<T>) * na, cudaMemcpyHostToDevice));
     PSW_CUDA_TRY(cudaMalloc(&pl->d_blk, sizeof(int32_t) * pl->blk.size()));
     PSW_CUDA_TRY(cudaMemcpy(pl->d_blk, pl->blk.data(), sizeof(int32_t) * pl->blk.size(),
                             cudaMemcpyHostToDevice));
@@ -170,6 +176,7 @@ void free_plan(psw_plan* pl) {
     cudaSetDevice(pl->device);
     void* ptrs[] = {pl->d_fwd, pl->d_bwd, pl->d_blk, pl->d_zr, pl->d_zl, pl->d_items,
                     pl->d_lvl_off, pl->d_ffwd, pl->d_fbwd, pl->d_seg, pl->d_cmat,
+                    pl->d_segdesc, pl->d_segoff,
                     pl->d_partial_spec, pl->d_coarse_items, pl->d_local_items, pl->d_partial_index};
     for (void* q : ptrs)
         if (q) cudaFree(q);
@@ -428,8 +435,9 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
     }
     int rc = (dtype == PSW_F64) ? upload<double>(pl, rp, ma, gr, gl, w, alv, zr, zl)
                                 : upload<float>(pl, rp, ma, gr, gl, w, alv, zr, zl);
-    if (rc == PSW_OK && pl->uniform && world == 1)
-        rc = build_fused_tables(pl, rp, ma, gr, gl, w, alv, combine_matrix(pl, zr, zl));
+    if (rc == PSW_OK && world == 1)
+        rc = build_fused_tables(pl, rp, ma, gr, gl, w, alv,
+                                pl->P <= 1024 ? combine_matrix(pl, zr, zl) : std::vector<double>());
     if (rc == PSW_OK && shard) rc = build_shard_tables(pl, combine_matrix(pl, zr, zl));
     cudaSetDevice(prev_dev);
     if (rc != PSW_OK) {
@@ -613,6 +621,8 @@ static int check_solve_args(const psw_plan* plan, const void* F, int64_t ldf, co
     return PSW_OK;
 }
 
+int psw_last_path(void) { return t_last_path; }
+
 int psw_solve_ex(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
                  int64_t nrhs, int layout, void* stream, const psw_solve_opts* opts) {
     psw::clear_error();
@@ -627,14 +637,26 @@ int psw_solve_ex(const psw_plan* plan, const void* F, int64_t ldf, void* X, int6
     const bool want_intermediates =
         opts && (opts->betas_left || opts->betas_right || opts->boundary_values);
     int rc;
-    if (path == PSW_PATH_FUSED && !psw::fused_supported(plan, layout, nrhs, F, ldf)) {
+    t_last_path = 0;
+    if (path == PSW_PATH_PIPE) {
+        t_last_path = PSW_PATH_PIPE;
+        if (want_intermediates || !psw::pipe_supported(plan, layout, nrhs, F, ldf, X, ldx)) {
+            psw::set_error(PSW_NOT_SUPPORTED, "pipe path does not support this plan/shape");
+            rc = PSW_NOT_SUPPORTED;
+        } else {
+            rc = psw::solve_pipe(plan, F, ldf, X, ldx, nrhs, layout, s,
+                                 opts ? opts->events : nullptr, opts ? opts->nevents : 0);
+        }
+    } else if (path == PSW_PATH_FUSED && !psw::fused_supported(plan, layout, nrhs, F, ldf)) {
         psw::set_error(PSW_NOT_SUPPORTED, "fused path does not support this plan/shape");
         rc = PSW_NOT_SUPPORTED;
     } else if ((path == PSW_PATH_FUSED || path == PSW_PATH_AUTO) && !want_intermediates &&
                psw::fused_supported(plan, layout, nrhs, F, ldf)) {
+        t_last_path = PSW_PATH_FUSED;
         rc = psw::solve_fused(plan, F, ldf, X, ldx, nrhs, layout, s, opts ? opts->events : nullptr,
                               opts ? opts->nevents : 0);
     } else {
+        t_last_path = PSW_PATH_STAGED;
         rc = psw::solve_staged(plan, F, ldf, X, ldx, nrhs, layout, s,
                                opts ? opts->betas_left : nullptr,
                                opts ? opts->betas_right : nullptr,
