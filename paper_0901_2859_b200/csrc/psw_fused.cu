@@ -31,6 +31,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -94,25 +95,31 @@ struct FusedGeom {
 // Shared-memory carve-up (bytes), identical on host and device: the slab
 // (TMA landing zone, handed back to the producer right after the forward
 // sweep), the plan tables loaded once, per-tile-parity scan buffers and beta
-// exchange buffers. The d~ of the tile awaiting its back substitution is
-// parked in tensor memory (TMEM), not here.
+// exchange buffers.
 struct FusedLayout {
-    size_t ff, fb, segc, cm, seg0, seg_b, part, all0, all_b, vals, bars, total;
+    size_t slab_b, ff, fb, segc, cm, seg0, seg_b, part, all0, all_b, vals, bars, total;
+    int nslab, nall;
     __host__ __device__ FusedLayout(int rows_alloc, int nchunks, int G, int S, int P, int W,
-                                    int es) {
+                                    int es, bool lag) {
         auto up = [](size_t x) { return (x + 127) & ~size_t(127); };
-        ff = up(size_t(rows_alloc) * W * es);                       // FusedFwd rows
+        // LAG: two slabs (tile k+1 loads while tile k is swept and its d~
+        // parked in place) and four exchange buffers (a peer may run up to
+        // three tiles ahead of a CTA's combination, see FusedTile::step_lag)
+        nslab = lag ? 2 : 1;
+        nall = lag ? 4 : 2;
+        slab_b = up(size_t(rows_alloc) * W * es);
+        ff = nslab * slab_b;                                        // FusedFwd rows
         fb = up(ff + size_t(rows_alloc) * (es == 8 ? 48 : 32));     // FusedBwd rows
         segc = up(fb + size_t(rows_alloc) * (es == 8 ? 32 : 16));   // G*S SegCoef
         cm = up(segc + size_t(G) * S * sizeof(SegCoef));            // (G+1) x 2P doubles
         seg0 = up(cm + size_t(G + 1) * 2 * P * sizeof(double));     // 3 x G*S*W doubles / parity
         seg_b = up(size_t(3) * G * S * W * sizeof(double));
         part = seg0 + 2 * seg_b;                                    // 2 x G*S*W beta partials
-        all0 = up(part + size_t(2) * G * S * W * sizeof(double));   // P x W x (R,L) / parity
+        all0 = up(part + size_t(2) * G * S * W * sizeof(double));   // P x W x (R,L) / buffer
         all_b = up(size_t(2) * P * W * sizeof(double));
-        vals = all0 + 2 * all_b;                                    // P x W doubles
-        bars = up(vals + size_t(P) * W * sizeof(double));           // nchunks + 4, TMEM addr
-        total = bars + size_t(nchunks + 3) * sizeof(uint64_t);
+        vals = all0 + nall * all_b;                                 // P x W doubles
+        bars = up(vals + size_t(P) * W * sizeof(double));           // slab chunks, plan, exchange
+        total = bars + size_t(nslab * nchunks + 1 + nall) * sizeof(uint64_t);
     }
 };
 
@@ -202,7 +209,7 @@ struct FusedCtx {
 // tile k. A tile's DSMEM beta exchange therefore overlaps a back
 // substitution and a forward sweep, and its HBM load overlaps a combination
 // and a back substitution.
-template <typename T, int W>
+template <typename T, int W, bool LAG>
 struct FusedTile {
     const FusedGeom& g;
     const FusedCtx& x;
@@ -222,19 +229,30 @@ struct FusedTile {
     int nfull, rem;
 
     // TMA of tile k's rows into the slab (one thread)
+    __device__ __forceinline__ T* slab(int64_t k) const {
+        return reinterpret_cast<T*>(smem + (LAG ? (k & 1) * L.slab_b : 0));
+    }
+    __device__ __forceinline__ uint64_t* slab_bars(int64_t k) const {
+        return bars + (LAG ? (k & 1) * (nfull + (rem > 0)) : 0);
+    }
+    // mbarrier phase of tile k's slab barriers
+    __device__ __forceinline__ uint32_t slab_phase(int64_t k) const {
+        return uint32_t(LAG ? (k >> 1) : k) & 1u;
+    }
     __device__ __forceinline__ void issue(int64_t k) const {
-        T* slab = reinterpret_cast<T*>(smem);
+        T* sl = slab(k);
+        uint64_t* bs = slab_bars(k);
         const int k0 = int((cluster_id + k * nclusters) * W);
         constexpr uint32_t box_bytes = uint32_t(W * kChunk * sizeof(T));
         for (int c = 0; c < nfull; ++c) {
-            mbar_expect_tx(&bars[c], box_bytes);
-            tma_load_2d(slab + size_t(c) * kChunk * W, tmF, k0, x.row0 + c * kChunk, &bars[c]);
+            mbar_expect_tx(&bs[c], box_bytes);
+            tma_load_2d(sl + size_t(c) * kChunk * W, tmF, k0, x.row0 + c * kChunk, &bs[c]);
         }
         if (rem) {  // tail rows through the one-row box
-            mbar_expect_tx(&bars[nfull], uint32_t(rem * W * sizeof(T)));
+            mbar_expect_tx(&bs[nfull], uint32_t(rem * W * sizeof(T)));
             for (int r = 0; r < rem; ++r)
-                tma_load_2d(slab + size_t(nfull * kChunk + r) * W, tmF1, k0,
-                            x.row0 + nfull * kChunk + r, &bars[nfull]);
+                tma_load_2d(sl + size_t(nfull * kChunk + r) * W, tmF1, k0,
+                            x.row0 + nfull * kChunk + r, &bs[nfull]);
         }
     }
 
@@ -242,20 +260,32 @@ struct FusedTile {
         return reinterpret_cast<double*>(smem + L.seg0 + (k & 1) * L.seg_b);
     }
     __device__ __forceinline__ double* allx(int64_t k) const {
-        return reinterpret_cast<double*>(smem + L.all0 + (k & 1) * L.all_b);
+        return reinterpret_cast<double*>(smem + L.all0 + (k & (LAG ? 3 : 1)) * L.all_b);
+    }
+    __device__ __forceinline__ uint64_t* xb(int64_t k) const { return &xbar[k & (LAG ? 3 : 1)]; }
+    __device__ __forceinline__ uint32_t xphase(int64_t k) const {
+        return uint32_t(k >> (LAG ? 2 : 1)) & 1u;
     }
 
     // forward sweep of tile k into dr; betas pushed after the scan
     __device__ __forceinline__ void forward(int64_t k, T (&dr)[kSegMax]) const {
         const int GSW = x.nc;
-        if (x.tid == 0) mbar_expect_tx(&xbar[k & 1], uint32_t(g.P * W * 2 * sizeof(double)));
-        for (int c = x.c_lo; c <= x.c_hi; ++c) mbar_wait(&bars[c], uint32_t(k) & 1u);
-        const T* col = reinterpret_cast<const T*>(smem) + x.lane + (x.a - x.row0) * W;
+        if (x.tid == 0) mbar_expect_tx(xb(k), uint32_t(g.P * W * 2 * sizeof(double)));
+        uint64_t* bs = slab_bars(k);
+        for (int c = x.c_lo; c <= x.c_hi; ++c) mbar_wait(&bs[c], slab_phase(k));
+        T* col = slab(k) + x.lane + (x.a - x.row0) * W;
         T d = T(0), sr = T(0), sl = T(0), sx = T(0);
-        if (x.len == kSegLen)
-            fwd_rows<T, W, kSegLen>(cf, col, dr, d, sr, sl, sx, kSegLen);
-        else
-            fwd_rows<T, W, kSegMax>(cf, col, dr, d, sr, sl, sx, x.len);
+        if constexpr (LAG) {  // d~ parked in place in the slab
+            if (x.len == kSegLen)
+                fwd_rows_smem<T, W, kSegLen>(cf, col, d, sr, sl, sx, kSegLen);
+            else
+                fwd_rows_smem<T, W, kSegMax>(cf, col, d, sr, sl, sx, x.len);
+        } else {
+            if (x.len == kSegLen)
+                fwd_rows<T, W, kSegLen>(cf, col, dr, d, sr, sl, sx, kSegLen);
+            else
+                fwd_rows<T, W, kSegMax>(cf, col, dr, d, sr, sl, sx, x.len);
+        }
         double* sk = seg(k);
         double* part = reinterpret_cast<double*>(smem + L.part);
         sk[x.tid] = double(d);         // d~ at the segment end
@@ -286,14 +316,14 @@ struct FusedTile {
     __device__ __forceinline__ void push(int64_t k, double R, double Lsum) const {
         if (x.sg != 0) return;
         const uint32_t src = smem_u32(allx(k)) + uint32_t((x.t * W + x.lane) * 16);
-        const uint32_t bar = smem_u32(&xbar[k & 1]);
+        const uint32_t bar = smem_u32(xb(k));
         for (int dst = 0; dst < C; ++dst) st_async_f64x2(mapa(src, dst), R, Lsum, mapa(bar, dst));
     }
 
     // boundary values of tile k this CTA needs: v = MR right + ML left, each
     // dot product split over 4 lanes and reduced with shuffles
     __device__ __forceinline__ void combine(int64_t k) const {
-        mbar_wait(&xbar[k & 1], uint32_t(k >> 1) & 1u);
+        mbar_wait(xb(k), xphase(k));
         const double* ax = allx(k);
         double* vals = reinterpret_cast<double*>(smem + L.vals);
         const int P = g.P, nout = (x.jb1 - x.jb0) * W;
@@ -351,6 +381,50 @@ struct FusedTile {
         if (tr && k == 2 && x.tid == 0) tr[blockIdx.x * 16 + slot] = clock64();
     }
 
+    // LAG schedule, iteration k: forward sweep of tile k (d~ parked in its
+    // slab) and push of its betas, then the combination and back
+    // substitution of tile k-1, whose betas were pushed one iteration ago:
+    // the cluster exchange no longer sits between a tile's two sweeps. Then
+    // tile k's d~ moves to registers and its slab receives tile k+2.
+    __device__ __forceinline__ void step_lag(int64_t k, int64_t ntl, T (&dr)[kSegMax]) const {
+        stamp(k, 0);
+        if (k < ntl) {
+            forward(k, dr);
+            stamp(k, 1);
+            cta_sync(x.nc);
+            double R, Lsum;
+            fwd_scan(k, R, Lsum);
+            push(k, R, Lsum);
+        }
+        stamp(k, 2);
+        if (k >= 1) {
+            combine(k - 1);
+            stamp(k, 3);
+            cta_sync(x.nc);
+            stamp(k, 4);
+            backward(k - 1, dr);
+        }
+        stamp(k, 5);
+        if (k < ntl) {
+            const T* col = slab(k) + x.lane + (x.a - x.row0) * W;
+#pragma unroll
+            for (int q = 0; q < kSegMax; ++q)
+                if (q < x.len) dr[q] = col[q * W];
+            cta_sync(x.nc);
+            if (x.tid == 0 && k + 2 < ntl) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue(k + 2);
+            }
+        }
+        stamp(k, 6);
+        unsigned long long* tr = g_trace;
+        if (tr && x.tid == 0) {
+            if (k == 0) tr[blockIdx.x * 16 + 10] = gtimer();
+            tr[blockIdx.x * 16 + 11] = gtimer();
+            tr[blockIdx.x * 16 + 12] = (unsigned long long)(k + 1);
+        }
+    }
+
     // iteration k: tile k end to end. The slab is handed back to the
     // producer right after the forward sweep (d~ stays in registers), so the
     // HBM load of tile k+1 overlaps the exchange, the combination and the
@@ -387,7 +461,7 @@ struct FusedTile {
     }
 };
 
-template <typename T, int W>
+template <typename T, int W, bool LAG>
 __global__ void __launch_bounds__(kMaxThreads) fused_r_kernel(
     const __grid_constant__ CUtensorMap tmF, const __grid_constant__ CUtensorMap tmF1, T* X,
     FusedGeom g, const FusedFwd<T>* __restrict__ gff, const FusedBwd<T>* __restrict__ gfb,
@@ -403,10 +477,10 @@ __global__ void __launch_bounds__(kMaxThreads) fused_r_kernel(
     const int row0 = crank * G * m - 1;
     const int row1 = crank == C - 1 ? g.n : (crank + 1) * G * m - 1;
     const int crow0 = row0 < 0 ? 0 : row0;  // first coefficient row
-    const FusedLayout L(g.rows_alloc, g.nchunks, G, S, P, W, int(sizeof(T)));
+    const FusedLayout L(g.rows_alloc, g.nchunks, G, S, P, W, int(sizeof(T)), LAG);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
-    uint64_t* cbar = &bars[g.nchunks];      // plan tables
-    uint64_t* xbar = &bars[g.nchunks + 1];  // [parity]: betas of a tile from every peer
+    uint64_t* cbar = &bars[L.nslab * g.nchunks];      // plan tables
+    uint64_t* xbar = &bars[L.nslab * g.nchunks + 1];  // [buffer]: betas of a tile from every peer
     const int nc = G * S * W;               // threads
     const int tid = threadIdx.x;
     const int nrows = row1 - row0;
@@ -431,7 +505,7 @@ __global__ void __launch_bounds__(kMaxThreads) fused_r_kernel(
     x.len = x.b - x.a;  // 0..kSegMax
     x.c_lo = x.len ? (x.a - row0) / kChunk : 0;
     x.c_hi = x.len ? (x.b - 1 - row0) / kChunk : -1;
-    const FusedTile<T, W> ft{g, x, smem, L,
+    const FusedTile<T, W, LAG> ft{g, x, smem, L,
                              reinterpret_cast<const FusedFwd<T>*>(smem + L.ff) - crow0 + x.a,
                              reinterpret_cast<const FusedBwd<T>*>(smem + L.fb) - crow0 + x.a,
                              reinterpret_cast<const SegCoef*>(smem + L.segc) - crank * G * S,
@@ -440,10 +514,9 @@ __global__ void __launch_bounds__(kMaxThreads) fused_r_kernel(
                              &tmF, &tmF1, nrows / kChunk, nrows % kChunk};
 
     if (tid == 0) {
-        for (int c = 0; c < ft.nfull + (ft.rem > 0); ++c) mbar_init(&bars[c], 1);
+        for (int c = 0; c < L.nslab * (ft.nfull + (ft.rem > 0)); ++c) mbar_init(&bars[c], 1);
         mbar_init(cbar, 1);
-        mbar_init(&xbar[0], 1);
-        mbar_init(&xbar[1], 1);
+        for (int i = 0; i < L.nall; ++i) mbar_init(&xbar[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -461,10 +534,15 @@ __global__ void __launch_bounds__(kMaxThreads) fused_r_kernel(
         bulk_load(smem + L.segc, gsegc + crank * G * S, segb, cbar);
         if (cmb) bulk_load(smem + L.cm, gcmat + size_t(x.jb0) * 2 * P, cmb, cbar);
         if (ntl > 0) ft.issue(0);
+        if (LAG && ntl > 1) ft.issue(1);
     }
     mbar_wait(cbar, 0);
     T dr[kSegMax];
-    for (int64_t k = 0; k < ntl; ++k) ft.step(k, ntl, dr);
+    if constexpr (LAG) {
+        for (int64_t k = 0; k <= ntl; ++k) ft.step_lag(k, ntl, dr);
+    } else {
+        for (int64_t k = 0; k < ntl; ++k) ft.step(k, ntl, dr);
+    }
 }
 
 // ---------------------------------------------------------------- host side
@@ -477,9 +555,22 @@ struct Choice {
 int tile_row_bytes() {
     static int rb = [] {
         const char* e = std::getenv("PSW_FUSED_ROW_BYTES");
-        return (e && std::atoi(e) == 256) ? 256 : 128;
+        const int v = e ? std::atoi(e) : 128;
+        return v == 256 ? 256 : 128;
     }();
     return rb;
+}
+
+// LAG schedule (FusedTile::step_lag) with PSW_FUSED_LAG=1. Measured on C1
+// (tools/trace_fused.py): it removes the exchange wait (4956 -> 978 cycles
+// per tile) but its second slab cuts co-resident clusters from 22 to 15, a
+// net loss (124.6 vs 92.5 us), so the default is the single-slab schedule.
+bool fused_lag() {
+    static bool lag = [] {
+        const char* e = std::getenv("PSW_FUSED_LAG");
+        return e && std::atoi(e) == 1;
+    }();
+    return lag;
 }
 
 // Smallest G (blocks per CTA) whose cluster C = P/G fits (<= 16 CTAs), then
@@ -495,7 +586,7 @@ Choice choose_w(const psw_plan* pl, int es, int row_bytes) {
         if (C > kMaxCluster) continue;
         const int rows_alloc = G * m + 1;
         const int nchunks = (rows_alloc + kChunk - 1) / kChunk;
-        const size_t smem = FusedLayout(rows_alloc, nchunks, G, S, P, W, es).total;
+        const size_t smem = FusedLayout(rows_alloc, nchunks, G, S, P, W, es, fused_lag()).total;
         if (smem > kSmemMax || G * S * W > kMaxThreads) break;
         if ((G * S * W) % 32) continue;  // consumer warps must be full
         if (ch.G == 0 || smem <= kSmemTarget) {
@@ -545,7 +636,7 @@ bool encode_maps(CUtensorMap* tm, CUtensorMap* tm1, const void* F, int64_t N, in
     return true;
 }
 
-template <typename T, int W>
+template <typename T, int W, bool LAG>
 int launch_w(const psw_plan* pl, const Choice& ch, const void* F, int64_t ldf, void* X,
              int64_t ldx, int64_t N, cudaStream_t s, void** ev, int nev) {
     CUtensorMap tm, tm1;
@@ -562,7 +653,7 @@ int launch_w(const psw_plan* pl, const Choice& ch, const void* F, int64_t ldf, v
     g.nchunks = ch.nchunks;
     g.N = N;
     g.ldx = ldx;
-    auto kern = fused_r_kernel<T, W>;
+    auto kern = fused_r_kernel<T, W, LAG>;
     PSW_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ch.smem)));
     if (ch.C > 8) PSW_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     const int64_t tiles = (N + W - 1) / W;
@@ -588,8 +679,9 @@ int launch_w(const psw_plan* pl, const Choice& ch, const void* F, int64_t ldf, v
     cfg.numAttrs = 2;
     // persistent: as many clusters as can be co-resident (cached per config)
     static std::mutex mu;
-    static std::vector<std::pair<std::array<int64_t, 5>, int>> cache;
-    const std::array<int64_t, 5> key = {int64_t(sizeof(T)), W, ch.C, int64_t(ch.smem), pl->device};
+    static std::vector<std::pair<std::array<int64_t, 6>, int>> cache;
+    const std::array<int64_t, 6> key = {int64_t(sizeof(T)), W, ch.C, int64_t(ch.smem), pl->device,
+                                        int64_t(LAG)};
     int maxc = 0;
     {
         std::lock_guard<std::mutex> lk(mu);
@@ -606,6 +698,9 @@ int launch_w(const psw_plan* pl, const Choice& ch, const void* F, int64_t ldf, v
     if (const char* e = std::getenv("PSW_FUSED_CLUSTERS"))  // tuning override
         nclusters = std::max<int64_t>(1, std::min<int64_t>(nclusters, std::atoll(e)));
     cfg.gridDim = dim3(unsigned(nclusters * ch.C), 1, 1);
+    if (std::getenv("PSW_FUSED_VERBOSE"))
+        std::fprintf(stderr, "fused: W=%d G=%d C=%d S=%d smem=%zu lag=%d max_clusters=%d clusters=%lld\n",
+                     W, ch.G, ch.C, g.S, ch.smem, int(LAG), maxc, (long long)nclusters);
     mark(ev, nev, 0, s);
     PSW_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tm, tm1, static_cast<T*>(X), g,
                                     static_cast<const FusedFwd<T>*>(pl->d_ffwd),
@@ -620,9 +715,14 @@ template <typename T>
 int launch_fused(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_t ldx, int64_t N,
                  cudaStream_t s, void** ev, int nev) {
     const Choice ch = choose(pl, int(sizeof(T)));
+    if (fused_lag()) {
+        if (ch.W * int(sizeof(T)) == 256)
+            return launch_w<T, 256 / sizeof(T), true>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
+        return launch_w<T, 128 / sizeof(T), true>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
+    }
     if (ch.W * int(sizeof(T)) == 256)
-        return launch_w<T, 256 / sizeof(T)>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
-    return launch_w<T, 128 / sizeof(T)>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
+        return launch_w<T, 256 / sizeof(T), false>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
+    return launch_w<T, 128 / sizeof(T), false>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
 }
 
 template <typename T>
@@ -661,7 +761,6 @@ int build_fused_tables(psw_plan* pl, const std::vector<double>& rp, const std::v
                                 cudaMemcpyHostToDevice));
         pl->info.device_bytes += int64_t(sizeof(double) * cmat.size());
     }
-    if (!pl->uniform || m < 1) return PSW_OK;
     // Segmentation of every block into runs of at most kSegLen + 1 rows:
     // uniform partitions use S = ceil(m / kSegLen) segments for every block
     // (the FUSED kernel's thread map; block sizes m-1, m, m+1); others use

@@ -62,7 +62,10 @@ struct CombineItem {
 // lam_q = prod_{u=a..q-1} al_u, nu = prod_{u=a..b-1} al_u, and
 // sum_q lam_q c_q = Lam + D_{a-1} K1 + x_l K2 (Lam = sum lam_q d~_q is
 // accumulated by the forward sweep, K1 = sum lam mu, K2 = sum lam w).
-constexpr int kSegLen = 32;
+#ifndef PSW_SEGLEN
+#define PSW_SEGLEN 32
+#endif
+constexpr int kSegLen = PSW_SEGLEN;  // rows per segment (the last one of a block: + 1)
 constexpr int kCoefPad = 64;  // zero rows appended to FwdCoef/BwdCoef tables
 template <typename T>
 struct alignas(16) FusedFwd {

@@ -22,136 +22,216 @@ namespace psw {
 namespace {
 
 constexpr int kThreads = 128;
-constexpr int kUnroll = 8;
+constexpr int kCoefChunk = 256;  // block rows whose coefficients are staged in shared memory
+
+// rows per register batch: the next batch is loaded while the current one is
+// swept, so 2 * kBatch rows per thread are in flight or in registers
+template <typename T>
+constexpr int kBatch = 16;
 
 template <typename T>
 __device__ __forceinline__ T ld_stream(const T* p) {
     return __ldcs(p);  // F is read exactly once: evict-first
 }
 
+// Cooperative copy of coefficient rows [c0, c1) into shared memory.
+template <typename C>
+__device__ __forceinline__ void stage_rows(C* dst, const C* __restrict__ src, int c0, int c1) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < c1 - c0; i += blockDim.x) dst[i] = src[c0 + i];
+    __syncthreads();
+}
 
 // ---------------------------------------------------------------- layout R
-// Blocks t0 + blockIdx.y; F/X row 0 is global row row_off (row shards,
-// psw_shard.cu); betas land at [(t - t0) * N + k].
+// One thread per (rhs k, block t0 + blockIdx.y). F/X row 0 is global row
+// row_off (row shards, psw_shard.cpp); betas land at [(t - t0) * N + k].
+// The block's sweep coefficients are staged in shared memory (warp-uniform
+// broadcasts), F rows stream through double-buffered register batches.
 template <typename T>
 __global__ void __launch_bounds__(kThreads) fwd_r_kernel(
     const T* F, int64_t ldf, T* X, int64_t ldx, int64_t N, const int32_t* __restrict__ blk,
     const FwdCoef<T>* __restrict__ cf, double* __restrict__ bl_out, double* __restrict__ br_out,
     int p, int t0, int row_off) {
+    constexpr int U = kBatch<T>;
+    __shared__ FwdCoef<T> cs[kCoefChunk];
     const int t = t0 + blockIdx.y;
     const int64_t k = int64_t(blockIdx.x) * kThreads + threadIdx.x;
-    if (k >= N) return;
+    const bool kv = k < N;
     const int s = blk[2 * t], e = blk[2 * t + 1];
-    const T* f = F + k - int64_t(row_off) * ldf;  // f[q * ldf] = global row q
-    T* x = X + k - int64_t(row_off) * ldx;
+    const T* f = F + (kv ? k : 0) - int64_t(row_off) * ldf;  // f[q * ldf] = global row q
+    T* x = X + (kv ? k : 0) - int64_t(row_off) * ldx;
     T d = T(0);
     double br = 0.0, bl = 0.0;
-    int q = s;
-    for (; q + kUnroll <= e; q += kUnroll) {
-        T fv[kUnroll];
+    for (int c0 = s; c0 < e; c0 += kCoefChunk) {
+        const int c1 = min(e, c0 + kCoefChunk);
+        stage_rows(cs, cf, c0, c1);
+        if (!kv) continue;
+        const int nb = (c1 - c0) / U;
+        T cur[U], nxt[U];
+        if (nb > 0) {
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) fv[u] = ld_stream(f + int64_t(q + u) * ldf);
+            for (int u = 0; u < U; ++u) cur[u] = ld_stream(f + int64_t(c0 + u) * ldf);
+        }
+        int q = c0;
+        for (int bi = 0; bi < nb; ++bi, q += U) {
+            if (bi + 1 < nb) {
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            const FwdCoef<T> c = cf[q + u];
-            d = fma(c.ma, d, fv[u] * c.rp);
-            br = madd_rn(br, double(fv[u]), double(c.gr));
-            bl = madd_rn(bl, double(fv[u]), double(c.gl));
-            x[int64_t(q + u) * ldx] = d;
+                for (int u = 0; u < U; ++u) nxt[u] = ld_stream(f + int64_t(q + U + u) * ldf);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const FwdCoef<T> c = cs[q - c0 + u];
+                d = fma(c.ma, d, cur[u] * c.rp);
+                br = madd_rn(br, double(cur[u]), double(c.gr));
+                bl = madd_rn(bl, double(cur[u]), double(c.gl));
+                x[int64_t(q + u) * ldx] = d;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+        }
+        for (; q < c1; ++q) {
+            const T fv = ld_stream(f + int64_t(q) * ldf);
+            const FwdCoef<T> c = cs[q - c0];
+            d = fma(c.ma, d, fv * c.rp);
+            br = madd_rn(br, double(fv), double(c.gr));
+            bl = madd_rn(bl, double(fv), double(c.gl));
+            x[int64_t(q) * ldx] = d;
         }
     }
-    for (; q < e; ++q) {
-        const T fv = ld_stream(f + int64_t(q) * ldf);
-        const FwdCoef<T> c = cf[q];
-        d = fma(c.ma, d, fv * c.rp);
-        br = madd_rn(br, double(fv), double(c.gr));
-        bl = madd_rn(bl, double(fv), double(c.gl));
-        x[int64_t(q) * ldx] = d;
+    if (kv) {
+        if (t < p) br_out[int64_t(t - t0) * N + k] = br;
+        if (t > 0) bl_out[int64_t(t - t0) * N + k] = bl;
     }
-    if (t < p) br_out[int64_t(t - t0) * N + k] = br;
-    if (t > 0) bl_out[int64_t(t - t0) * N + k] = bl;
 }
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads) bwd_r_kernel(
     T* X, int64_t ldx, int64_t N, const int32_t* __restrict__ blk,
     const BwdCoef<T>* __restrict__ cb, const double* __restrict__ V, int p, int t0, int row_off) {
+    constexpr int U = kBatch<T>;
+    __shared__ BwdCoef<T> cs[kCoefChunk];
     const int t = t0 + blockIdx.y;
     const int64_t k = int64_t(blockIdx.x) * kThreads + threadIdx.x;
-    if (k >= N) return;
+    const bool kv = k < N;
     const int s = blk[2 * t], e = blk[2 * t + 1];
-    const T xl = t > 0 ? T(V[int64_t(t - 1) * N + k]) : T(0);
-    T xn = t < p ? T(V[int64_t(t) * N + k]) : T(0);
-    T* x = X + k - int64_t(row_off) * ldx;
-    int q = e - 1;
-    for (; q - kUnroll + 1 >= s; q -= kUnroll) {
-        T dv[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) dv[u] = x[int64_t(q - u) * ldx];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            const BwdCoef<T> c = cb[q - u];
-            xn = fma(c.al, xn, fma(xl, c.w, dv[u]));
-            __stcs(x + int64_t(q - u) * ldx, xn);
-        }
+    T xl = T(0), xn = T(0);
+    if (kv) {
+        xl = t > 0 ? T(V[int64_t(t - 1) * N + k]) : T(0);
+        xn = t < p ? T(V[int64_t(t) * N + k]) : T(0);
     }
-    for (; q >= s; --q) {
-        const BwdCoef<T> c = cb[q];
-        xn = fma(c.al, xn, fma(xl, c.w, x[int64_t(q) * ldx]));
-        __stcs(x + int64_t(q) * ldx, xn);
+    T* x = X + (kv ? k : 0) - int64_t(row_off) * ldx;
+    for (int c1 = e; c1 > s; c1 -= kCoefChunk) {
+        const int c0 = max(s, c1 - kCoefChunk);
+        stage_rows(cs, cb, c0, c1);
+        if (!kv) continue;
+        const int nb = (c1 - c0) / U;
+        T cur[U], nxt[U];
+        if (nb > 0) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) cur[u] = x[int64_t(c1 - 1 - u) * ldx];
+        }
+        int q = c1 - 1;  // rows q, q-1, ..., q-U+1 form the current batch
+        for (int bi = 0; bi < nb; ++bi, q -= U) {
+            if (bi + 1 < nb) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) nxt[u] = x[int64_t(q - U - u) * ldx];
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const BwdCoef<T> c = cs[q - u - c0];
+                xn = fma(c.al, xn, fma(xl, c.w, cur[u]));
+                __stcs(x + int64_t(q - u) * ldx, xn);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+        }
+        for (; q >= c0; --q) {
+            const BwdCoef<T> c = cs[q - c0];
+            xn = fma(c.al, xn, fma(xl, c.w, x[int64_t(q) * ldx]));
+            __stcs(x + int64_t(q) * ldx, xn);
+        }
     }
 }
 
 // ---------------------------------------------------------------- layout S
 // One warp per (32 RHS, block): chunks of 32 rows are read coalesced along
 // the system (each RHS contiguous), transposed through shared memory so each
-// lane sweeps its own RHS, and written back the same way.
+// lane sweeps its own RHS, and written back the same way. Two tiles per warp:
+// the next chunk's loads are in flight while the current one is swept.
 constexpr int kWarps = kThreads / 32;
+
+template <typename T>
+__device__ __forceinline__ void tile_load(T (*tile)[33], const T* src, int64_t ld, int cnt,
+                                          int nk, int lane, bool streaming) {
+    if (lane < cnt) {
+        const T* p = src + lane;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (j < nk) tile[j][lane] = streaming ? ld_stream(p + int64_t(j) * ld) : p[int64_t(j) * ld];
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void tile_store(T (*tile)[33], T* dst, int64_t ld, int cnt, int nk,
+                                           int lane, bool streaming) {
+    if (lane < cnt) {
+        T* p = dst + lane;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (j < nk) {
+                if (streaming) __stcs(p + int64_t(j) * ld, tile[j][lane]);
+                else p[int64_t(j) * ld] = tile[j][lane];
+            }
+    }
+}
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads) fwd_s_kernel(
     const T* F, int64_t ldf, T* X, int64_t ldx, int64_t N, const int32_t* __restrict__ blk,
     const FwdCoef<T>* __restrict__ cf, double* __restrict__ bl_out, double* __restrict__ br_out,
     int p) {
-    __shared__ T tiles[kWarps][32][33];
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    FwdCoef<T>* cs = reinterpret_cast<FwdCoef<T>*>(s_raw);
+    auto tiles = reinterpret_cast<T(*)[2][32][33]>(s_raw + kCoefChunk * sizeof(FwdCoef<T>));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    T(*tile)[33] = tiles[warp];
     const int t = blockIdx.y;
     const int64_t k0 = (int64_t(blockIdx.x) * kWarps + warp) * 32;
-    if (k0 >= N) return;
-    const int nk = int(N - k0 < 32 ? N - k0 : 32);
+    const bool wv = k0 < N;
+    const int nk = wv ? int(N - k0 < 32 ? N - k0 : 32) : 0;
     const int s = blk[2 * t], e = blk[2 * t + 1];
+    const T* src = F + (wv ? k0 : 0) * ldf;
+    T* dst = X + (wv ? k0 : 0) * ldx;
     T d = T(0);
     double br = 0.0, bl = 0.0;
-    for (int q0 = s; q0 < e; q0 += 32) {
-        const int cnt = e - q0 < 32 ? e - q0 : 32;
-        if (lane < cnt) {
-            const T* src = F + k0 * ldf + q0 + lane;
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-                if (j < nk) tile[j][lane] = ld_stream(src + int64_t(j) * ldf);
-        }
-        __syncwarp();
-        if (lane < nk) {
-            for (int r = 0; r < cnt; ++r) {
-                const FwdCoef<T> c = cf[q0 + r];
-                const T fv = tile[lane][r];
-                d = fma(c.ma, d, fv * c.rp);
-                br = madd_rn(br, double(fv), double(c.gr));
-                bl = madd_rn(bl, double(fv), double(c.gl));
-                tile[lane][r] = d;
+    for (int c0 = s; c0 < e; c0 += kCoefChunk) {
+        const int c1 = min(e, c0 + kCoefChunk);
+        stage_rows(cs, cf, c0, c1);
+        if (!wv) continue;
+        int buf = 0;
+        tile_load(tiles[warp][0], src + c0, ldf, min(32, c1 - c0), nk, lane, true);
+        for (int q0 = c0; q0 < c1; q0 += 32, buf ^= 1) {
+            const int cnt = min(32, c1 - q0);
+            if (q0 + 32 < c1)  // next chunk in flight while this one is swept
+                tile_load(tiles[warp][buf ^ 1], src + q0 + 32, ldf, min(32, c1 - q0 - 32), nk,
+                          lane, true);
+            __syncwarp();
+            T(*tile)[33] = tiles[warp][buf];
+            if (lane < nk) {
+                for (int r = 0; r < cnt; ++r) {
+                    const FwdCoef<T> c = cs[q0 - c0 + r];
+                    const T fv = tile[lane][r];
+                    d = fma(c.ma, d, fv * c.rp);
+                    br = madd_rn(br, double(fv), double(c.gr));
+                    bl = madd_rn(bl, double(fv), double(c.gl));
+                    tile[lane][r] = d;
+                }
             }
+            __syncwarp();
+            tile_store(tile, dst + q0, ldx, cnt, nk, lane, false);
+            __syncwarp();
         }
-        __syncwarp();
-        if (lane < cnt) {
-            T* dst = X + k0 * ldx + q0 + lane;
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-                if (j < nk) dst[int64_t(j) * ldx] = tile[j][lane];
-        }
-        __syncwarp();
     }
-    if (lane < nk) {
+    if (wv && lane < nk) {
         if (t < p) br_out[int64_t(t) * N + k0 + lane] = br;
         if (t > 0) bl_out[int64_t(t) * N + k0 + lane] = bl;
     }
@@ -161,45 +241,56 @@ template <typename T>
 __global__ void __launch_bounds__(kThreads) bwd_s_kernel(
     T* X, int64_t ldx, int64_t N, const int32_t* __restrict__ blk,
     const BwdCoef<T>* __restrict__ cb, const double* __restrict__ V, int p) {
-    __shared__ T tiles[kWarps][32][33];
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    BwdCoef<T>* cs = reinterpret_cast<BwdCoef<T>*>(s_raw);
+    auto tiles = reinterpret_cast<T(*)[2][32][33]>(s_raw + kCoefChunk * sizeof(BwdCoef<T>));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    T(*tile)[33] = tiles[warp];
     const int t = blockIdx.y;
     const int64_t k0 = (int64_t(blockIdx.x) * kWarps + warp) * 32;
-    if (k0 >= N) return;
-    const int nk = int(N - k0 < 32 ? N - k0 : 32);
+    const bool wv = k0 < N;
+    const int nk = wv ? int(N - k0 < 32 ? N - k0 : 32) : 0;
     const int s = blk[2 * t], e = blk[2 * t + 1];
+    T* xs = X + (wv ? k0 : 0) * ldx;
     T xl = T(0), xn = T(0);
-    if (lane < nk) {
+    if (wv && lane < nk) {
         if (t > 0) xl = T(V[int64_t(t - 1) * N + k0 + lane]);
         if (t < p) xn = T(V[int64_t(t) * N + k0 + lane]);
     }
-    for (int q1 = e; q1 > s; q1 -= 32) {
-        const int q0 = q1 - 32 > s ? q1 - 32 : s;
-        const int cnt = q1 - q0;
-        if (lane < cnt) {
-            const T* src = X + k0 * ldx + q0 + lane;
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-                if (j < nk) tile[j][lane] = src[int64_t(j) * ldx];
+    for (int c1 = e; c1 > s; c1 -= kCoefChunk) {
+        const int c0 = max(s, c1 - kCoefChunk);
+        stage_rows(cs, cb, c0, c1);
+        if (!wv) continue;
+        int buf = 0;
+        {
+            const int q0 = max(c0, c1 - 32);
+            tile_load(tiles[warp][0], xs + q0, ldx, c1 - q0, nk, lane, false);
         }
-        __syncwarp();
-        if (lane < nk) {
-            for (int r = cnt - 1; r >= 0; --r) {
-                const BwdCoef<T> c = cb[q0 + r];
-                xn = fma(c.al, xn, fma(xl, c.w, tile[lane][r]));
-                tile[lane][r] = xn;
+        for (int q1 = c1; q1 > c0; q1 -= 32, buf ^= 1) {
+            const int q0 = max(c0, q1 - 32);
+            const int cnt = q1 - q0;
+            if (q0 > c0) {
+                const int n0 = max(c0, q0 - 32);
+                tile_load(tiles[warp][buf ^ 1], xs + n0, ldx, q0 - n0, nk, lane, false);
             }
+            __syncwarp();
+            T(*tile)[33] = tiles[warp][buf];
+            if (lane < nk) {
+                for (int r = cnt - 1; r >= 0; --r) {
+                    const BwdCoef<T> c = cs[q0 - c0 + r];
+                    xn = fma(c.al, xn, fma(xl, c.w, tile[lane][r]));
+                    tile[lane][r] = xn;
+                }
+            }
+            __syncwarp();
+            tile_store(tile, xs + q0, ldx, cnt, nk, lane, true);
+            __syncwarp();
         }
-        __syncwarp();
-        if (lane < cnt) {
-            T* dst = X + k0 * ldx + q0 + lane;
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-                if (j < nk) __stcs(dst + int64_t(j) * ldx, tile[j][lane]);
-        }
-        __syncwarp();
     }
+}
+
+template <typename T, typename C>
+constexpr size_t s_smem() {
+    return kCoefChunk * sizeof(C) + size_t(kWarps) * 2 * 32 * 33 * sizeof(T);
 }
 
 // --------------------------------------------------------------- combine
@@ -268,8 +359,13 @@ int launch_staged(const psw_plan* pl, const void* Fv, int64_t ldf, void* Xv, int
         mark(ev, nev, 3, s);
     } else {
         dim3 grid(unsigned((N + 32 * kWarps - 1) / (32 * kWarps)), unsigned(pl->P));
+        constexpr size_t sf = s_smem<T, FwdCoef<T>>(), sb = s_smem<T, BwdCoef<T>>();
+        PSW_CUDA_TRY(cudaFuncSetAttribute(fwd_s_kernel<T>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(sf)));
+        PSW_CUDA_TRY(cudaFuncSetAttribute(bwd_s_kernel<T>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(sb)));
         mark(ev, nev, 0, s);
-        fwd_s_kernel<T><<<grid, kThreads, 0, s>>>(F, ldf, X, ldx, N, pl->d_blk, cf, bl, br, p);
+        fwd_s_kernel<T><<<grid, kThreads, sf, s>>>(F, ldf, X, ldx, N, pl->d_blk, cf, bl, br, p);
         ++launches;
         mark(ev, nev, 1, s);
         if (p > 0) {
@@ -279,7 +375,7 @@ int launch_staged(const psw_plan* pl, const void* Fv, int64_t ldf, void* Xv, int
             ++launches;
         }
         mark(ev, nev, 2, s);
-        bwd_s_kernel<T><<<grid, kThreads, 0, s>>>(X, ldx, N, pl->d_blk, cb, V, p);
+        bwd_s_kernel<T><<<grid, kThreads, sb, s>>>(X, ldx, N, pl->d_blk, cb, V, p);
         ++launches;
         mark(ev, nev, 3, s);
     }

@@ -14,8 +14,8 @@ import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-PHASES = ["forward k+1 (chunk wait + sweep)", "sync + fwd scan", "exchange wait + combine k",
-          "push k+1 + sync", "backward k (scan + sweep)", "sync + park d~"]
+PHASES = ["forward (chunk wait + sweep)", "sync + issue + scan + push", "exchange wait + combine",
+          "sync", "backward (carries + sweep)", "reload d~ + sync + issue (LAG)"]
 
 
 def main():

@@ -26,25 +26,27 @@ layout = psw.LAYOUT_R if lay == "R" else psw.LAYOUT_S
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 for _ in range(3):
     plan.solve(F, X, layout=layout, path=psw.PATH_PIPE)
-tr = torch.zeros(4 << 22, dtype=torch.int64, device="cuda")
+tr = torch.zeros(8 << 22, dtype=torch.int64, device="cuda")
 psw.lib().psw_debug_trace(psw._ptr(tr))
 psw.l2_flush(flush)
 torch.cuda.synchronize()
 plan.solve(F, X, layout=layout, path=psw.PATH_PIPE)
 torch.cuda.synchronize()
 psw.lib().psw_debug_trace(None)
-t = tr.cpu().numpy().reshape(-1, 4)
+t = tr.cpu().numpy().reshape(-1, 8)
 t = t[(t[:, 2] > 0) & (t[:, 1] > 0)]  # executed items (skipped tickets have no ready stamp)
 t0 = t[:, 0].min()
 start, ready, end = (t[:, 0] - t0) / 1e3, (t[:, 1] - t0) / 1e3, (t[:, 2] - t0) / 1e3
 typ = (t[:, 3] >> 32) & 0xff
 print(f"{cfg.name} {lay}: {len(t)} items, span {end.max():.1f} us")
-for k, nm in enumerate("ABC"):
+for k, nm in enumerate("ABC"):  # B is unused (combination runs inside A items)
     m = typ == k
     if m.any():
         w, d = ready[m] - start[m], end[m] - ready[m]
+        tw = t[m, 4] / 1e3
         print(f"  {nm}: n={m.sum():5d} wait mean {w.mean():7.2f} max {w.max():7.2f} us | "
-              f"work mean {d.mean():7.2f} p50 {np.median(d):7.2f} max {d.max():7.2f} us | "
+              f"work mean {d.mean():7.2f} p50 {np.median(d):7.2f} max {d.max():7.2f} us "
+              f"(tma wait mean {tw.mean():6.2f}) | "
               f"first start {start[m].min():7.1f} last end {end[m].max():7.1f}")
 # activity histogram (busy warps per 5 us bin, by type)
 bins = np.arange(0, end.max() + 5, 5.0)
