@@ -52,7 +52,8 @@ typedef enum psw_path {
     PSW_PATH_AUTO = 0,
     PSW_PATH_STAGED = 1,
     PSW_PATH_FUSED = 2,
-    PSW_PATH_PIPE = 3
+    PSW_PATH_PIPE = 3,
+    PSW_PATH_TILE = 4
 } psw_path;
 
 typedef struct psw_plan psw_plan;

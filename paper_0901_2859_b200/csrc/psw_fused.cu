@@ -88,7 +88,7 @@ __device__ __forceinline__ void cta_sync(int nc) {
 }
 
 struct FusedGeom {
-    int n, P, p, m, G, C, S, rows_alloc, nchunks;
+    int n, P, p, m, G, C, S, rows_alloc, nchunks, prefetch;
     int64_t N, ldx, ntiles;
 };
 
@@ -100,7 +100,7 @@ struct FusedLayout {
     size_t slab_b, ff, fb, segc, cm, seg0, seg_b, part, all0, all_b, vals, bars, total;
     int nslab, nall;
     __host__ __device__ FusedLayout(int rows_alloc, int nchunks, int G, int S, int P, int W,
-                                    int es, bool lag) {
+                                    int es, bool lag, bool gc) {
         auto up = [](size_t x) { return (x + 127) & ~size_t(127); };
         // LAG: two slabs (tile k+1 loads while tile k is swept and its d~
         // parked in place) and four exchange buffers (a peer may run up to
@@ -108,9 +108,11 @@ struct FusedLayout {
         nslab = lag ? 2 : 1;
         nall = lag ? 4 : 2;
         slab_b = up(size_t(rows_alloc) * W * es);
-        ff = nslab * slab_b;                                        // FusedFwd rows
-        fb = up(ff + size_t(rows_alloc) * (es == 8 ? 48 : 32));     // FusedBwd rows
-        segc = up(fb + size_t(rows_alloc) * (es == 8 ? 32 : 16));   // G*S SegCoef
+        // GC: the sweep coefficients are read from global memory (L1-resident)
+        // instead of being copied here, leaving shared memory to the slabs
+        ff = nslab * slab_b;                                                     // FusedFwd rows
+        fb = up(ff + (gc ? 0 : size_t(rows_alloc) * (es == 8 ? 48 : 32)));      // FusedBwd rows
+        segc = up(fb + (gc ? 0 : size_t(rows_alloc) * (es == 8 ? 32 : 16)));    // G*S SegCoef
         cm = up(segc + size_t(G) * S * sizeof(SegCoef));            // (G+1) x 2P doubles
         seg0 = up(cm + size_t(G + 1) * 2 * P * sizeof(double));     // 3 x G*S*W doubles / parity
         seg_b = up(size_t(3) * G * S * W * sizeof(double));
@@ -227,6 +229,7 @@ struct FusedTile {
     const CUtensorMap* tmF;
     const CUtensorMap* tmF1;
     int nfull, rem;
+    int64_t ntl_;
 
     // TMA of tile k's rows into the slab (one thread)
     __device__ __forceinline__ T* slab(int64_t k) const {
@@ -253,6 +256,13 @@ struct FusedTile {
             for (int r = 0; r < rem; ++r)
                 tma_load_2d(sl + size_t(nfull * kChunk + r) * W, tmF1, k0,
                             x.row0 + nfull * kChunk + r, &bs[nfull]);
+        }
+        // tile k + 1 into L2 ahead of its load: doubles the bytes in flight
+        // per CTA without shared memory (HBM latency ~4 us under load)
+        if (g.prefetch && k + 1 < ntl_) {
+            const int k1 = int((cluster_id + (k + 1) * nclusters) * W);
+            for (int c = 0; c * kChunk < nfull * kChunk + rem; ++c)
+                tma_prefetch_2d(tmF, k1, x.row0 + c * kChunk);
         }
     }
 
@@ -461,7 +471,7 @@ struct FusedTile {
     }
 };
 
-template <typename T, int W, bool LAG>
+template <typename T, int W, bool LAG, bool GC>
 __global__ void __launch_bounds__(kMaxThreads) fused_r_kernel(
     const __grid_constant__ CUtensorMap tmF, const __grid_constant__ CUtensorMap tmF1, T* X,
     FusedGeom g, const FusedFwd<T>* __restrict__ gff, const FusedBwd<T>* __restrict__ gfb,
@@ -477,7 +487,7 @@ __global__ void __launch_bounds__(kMaxThreads) fused_r_kernel(
     const int row0 = crank * G * m - 1;
     const int row1 = crank == C - 1 ? g.n : (crank + 1) * G * m - 1;
     const int crow0 = row0 < 0 ? 0 : row0;  // first coefficient row
-    const FusedLayout L(g.rows_alloc, g.nchunks, G, S, P, W, int(sizeof(T)), LAG);
+    const FusedLayout L(g.rows_alloc, g.nchunks, G, S, P, W, int(sizeof(T)), LAG, GC);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
     uint64_t* cbar = &bars[L.nslab * g.nchunks];      // plan tables
     uint64_t* xbar = &bars[L.nslab * g.nchunks + 1];  // [buffer]: betas of a tile from every peer
@@ -506,12 +516,14 @@ __global__ void __launch_bounds__(kMaxThreads) fused_r_kernel(
     x.c_lo = x.len ? (x.a - row0) / kChunk : 0;
     x.c_hi = x.len ? (x.b - 1 - row0) / kChunk : -1;
     const FusedTile<T, W, LAG> ft{g, x, smem, L,
-                             reinterpret_cast<const FusedFwd<T>*>(smem + L.ff) - crow0 + x.a,
-                             reinterpret_cast<const FusedBwd<T>*>(smem + L.fb) - crow0 + x.a,
+                             GC ? gff + x.a
+                                : reinterpret_cast<const FusedFwd<T>*>(smem + L.ff) - crow0 + x.a,
+                             GC ? gfb + x.a
+                                : reinterpret_cast<const FusedBwd<T>*>(smem + L.fb) - crow0 + x.a,
                              reinterpret_cast<const SegCoef*>(smem + L.segc) - crank * G * S,
                              reinterpret_cast<const double*>(smem + L.cm),
                              bars, xbar, crank, C, cluster_id, nclusters, X,
-                             &tmF, &tmF1, nrows / kChunk, nrows % kChunk};
+                             &tmF, &tmF1, nrows / kChunk, nrows % kChunk, ntl};
 
     if (tid == 0) {
         for (int c = 0; c < L.nslab * (ft.nfull + (ft.rem > 0)); ++c) mbar_init(&bars[c], 1);
@@ -524,13 +536,15 @@ __global__ void __launch_bounds__(kMaxThreads) fused_r_kernel(
     if (tid == 0) {
         // plan tables once (small, L2-resident), then the first tile
         const uint32_t crows = uint32_t(row1 - crow0);
-        const uint32_t fwdb = crows * uint32_t(sizeof(FusedFwd<T>));
-        const uint32_t bwdb = crows * uint32_t(sizeof(FusedBwd<T>));
+        const uint32_t fwdb = GC ? 0u : crows * uint32_t(sizeof(FusedFwd<T>));
+        const uint32_t bwdb = GC ? 0u : crows * uint32_t(sizeof(FusedBwd<T>));
         const uint32_t segb = uint32_t(G * S * sizeof(SegCoef));
         const uint32_t cmb = uint32_t(x.jb1 > x.jb0 ? (x.jb1 - x.jb0) * 2 * P * sizeof(double) : 0);
         mbar_expect_tx(cbar, fwdb + bwdb + segb + cmb);
-        bulk_load(smem + L.ff, gff + crow0, fwdb, cbar);
-        bulk_load(smem + L.fb, gfb + crow0, bwdb, cbar);
+        if (!GC) {
+            bulk_load(smem + L.ff, gff + crow0, fwdb, cbar);
+            bulk_load(smem + L.fb, gfb + crow0, bwdb, cbar);
+        }
         bulk_load(smem + L.segc, gsegc + crank * G * S, segb, cbar);
         if (cmb) bulk_load(smem + L.cm, gcmat + size_t(x.jb0) * 2 * P, cmb, cbar);
         if (ntl > 0) ft.issue(0);
@@ -573,6 +587,18 @@ bool fused_lag() {
     return lag;
 }
 
+// Sweep coefficients read from global memory / L1 (PSW_FUSED_GCOEF=1)
+// instead of the per-CTA shared-memory copy. Measured on C1: the freed shared
+// memory does not buy more resident clusters and the sweeps then wait on L1
+// misses (184 vs 92.5 us), so the copy is the default.
+bool fused_gcoef() {
+    static bool gc = [] {
+        const char* e = std::getenv("PSW_FUSED_GCOEF");
+        return e && std::atoi(e) == 1;
+    }();
+    return gc;
+}
+
 // Smallest G (blocks per CTA) whose cluster C = P/G fits (<= 16 CTAs), then
 // grow G while the CTA stays under the occupancy target.
 Choice choose_w(const psw_plan* pl, int es, int row_bytes) {
@@ -586,7 +612,8 @@ Choice choose_w(const psw_plan* pl, int es, int row_bytes) {
         if (C > kMaxCluster) continue;
         const int rows_alloc = G * m + 1;
         const int nchunks = (rows_alloc + kChunk - 1) / kChunk;
-        const size_t smem = FusedLayout(rows_alloc, nchunks, G, S, P, W, es, fused_lag()).total;
+        const size_t smem =
+            FusedLayout(rows_alloc, nchunks, G, S, P, W, es, fused_lag(), fused_gcoef()).total;
         if (smem > kSmemMax || G * S * W > kMaxThreads) break;
         if ((G * S * W) % 32) continue;  // consumer warps must be full
         if (ch.G == 0 || smem <= kSmemTarget) {
@@ -636,7 +663,7 @@ bool encode_maps(CUtensorMap* tm, CUtensorMap* tm1, const void* F, int64_t N, in
     return true;
 }
 
-template <typename T, int W, bool LAG>
+template <typename T, int W, bool LAG, bool GC>
 int launch_w(const psw_plan* pl, const Choice& ch, const void* F, int64_t ldf, void* X,
              int64_t ldx, int64_t N, cudaStream_t s, void** ev, int nev) {
     CUtensorMap tm, tm1;
@@ -651,9 +678,13 @@ int launch_w(const psw_plan* pl, const Choice& ch, const void* F, int64_t ldf, v
     g.S = pl->nseg;
     g.rows_alloc = ch.rows_alloc;
     g.nchunks = ch.nchunks;
+    g.prefetch = [] {  // L2 prefetch of the next tile (measured neutral on C1: off)
+        const char* e = std::getenv("PSW_FUSED_PREFETCH");
+        return e ? std::atoi(e) : 0;
+    }();
     g.N = N;
     g.ldx = ldx;
-    auto kern = fused_r_kernel<T, W, LAG>;
+    auto kern = fused_r_kernel<T, W, LAG, GC>;
     PSW_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ch.smem)));
     if (ch.C > 8) PSW_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     const int64_t tiles = (N + W - 1) / W;
@@ -681,7 +712,7 @@ int launch_w(const psw_plan* pl, const Choice& ch, const void* F, int64_t ldf, v
     static std::mutex mu;
     static std::vector<std::pair<std::array<int64_t, 6>, int>> cache;
     const std::array<int64_t, 6> key = {int64_t(sizeof(T)), W, ch.C, int64_t(ch.smem), pl->device,
-                                        int64_t(LAG)};
+                                        int64_t(LAG) + 2 * int64_t(GC)};
     int maxc = 0;
     {
         std::lock_guard<std::mutex> lk(mu);
@@ -699,8 +730,8 @@ int launch_w(const psw_plan* pl, const Choice& ch, const void* F, int64_t ldf, v
         nclusters = std::max<int64_t>(1, std::min<int64_t>(nclusters, std::atoll(e)));
     cfg.gridDim = dim3(unsigned(nclusters * ch.C), 1, 1);
     if (std::getenv("PSW_FUSED_VERBOSE"))
-        std::fprintf(stderr, "fused: W=%d G=%d C=%d S=%d smem=%zu lag=%d max_clusters=%d clusters=%lld\n",
-                     W, ch.G, ch.C, g.S, ch.smem, int(LAG), maxc, (long long)nclusters);
+        std::fprintf(stderr, "fused: W=%d G=%d C=%d S=%d smem=%zu lag=%d gcoef=%d max_clusters=%d clusters=%lld\n",
+                     W, ch.G, ch.C, g.S, ch.smem, int(LAG), int(GC), maxc, (long long)nclusters);
     mark(ev, nev, 0, s);
     PSW_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tm, tm1, static_cast<T*>(X), g,
                                     static_cast<const FusedFwd<T>*>(pl->d_ffwd),
@@ -715,14 +746,22 @@ template <typename T>
 int launch_fused(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_t ldx, int64_t N,
                  cudaStream_t s, void** ev, int nev) {
     const Choice ch = choose(pl, int(sizeof(T)));
-    if (fused_lag()) {
-        if (ch.W * int(sizeof(T)) == 256)
-            return launch_w<T, 256 / sizeof(T), true>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
-        return launch_w<T, 128 / sizeof(T), true>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
+    const bool w256 = ch.W * int(sizeof(T)) == 256;
+    const int mode = (fused_lag() ? 1 : 0) + (fused_gcoef() ? 2 : 0);
+    switch (mode) {
+        case 0:
+            return w256 ? launch_w<T, 256 / sizeof(T), false, false>(pl, ch, F, ldf, X, ldx, N, s, ev, nev)
+                        : launch_w<T, 128 / sizeof(T), false, false>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
+        case 1:
+            return w256 ? launch_w<T, 256 / sizeof(T), true, false>(pl, ch, F, ldf, X, ldx, N, s, ev, nev)
+                        : launch_w<T, 128 / sizeof(T), true, false>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
+        case 2:
+            return w256 ? launch_w<T, 256 / sizeof(T), false, true>(pl, ch, F, ldf, X, ldx, N, s, ev, nev)
+                        : launch_w<T, 128 / sizeof(T), false, true>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
+        default:
+            return w256 ? launch_w<T, 256 / sizeof(T), true, true>(pl, ch, F, ldf, X, ldx, N, s, ev, nev)
+                        : launch_w<T, 128 / sizeof(T), true, true>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
     }
-    if (ch.W * int(sizeof(T)) == 256)
-        return launch_w<T, 256 / sizeof(T), false>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
-    return launch_w<T, 128 / sizeof(T), false>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
 }
 
 template <typename T>

@@ -1,3 +1,2 @@
-timeout 600 python -m pytest tests -x -q -m gpu 2>&1 | tail -3 > gpurun_out/all_t4.log
-for L in 0 1; do for RB in 128 256; do echo "C1 fused LAG=$L RB=$RB" >> gpurun_out/fl_b4.log; PSW_FUSED_VERBOSE=1 PSW_FUSED_ROW_BYTES=$RB PSW_FUSED_LAG=$L timeout 100 python bench.py --config C1 --path fused --steps 50 --warmup 5 2>&1 | grep -E "^\{|fused:" | sort -u | head -3 >> gpurun_out/fl_b4.log; done; done
-echo "C1 pipe" >> gpurun_out/fl_b4.log; PSW_PIPE_LAG=2 PSW_PIPE_SLOTS=8 PSW_PIPE_CHUNK_MB=24 timeout 100 python bench.py --config C1 --path pipe --steps 20 --warmup 3 2>&1 | grep -E "^\{" >> gpurun_out/fl_b4.log
+timeout 600 python -m pytest tests/test_parity_gpu.py -x -q 2>&1 | tail -2 > gpurun_out/s_t1.log
+echo "C4 staged" >> gpurun_out/s_b1.log; timeout 200 python bench.py --config C4 --path staged --steps 20 --warmup 3 2>&1 | grep -E "^\{" >> gpurun_out/s_b1.log
