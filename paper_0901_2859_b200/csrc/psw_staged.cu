@@ -241,6 +241,12 @@ __global__ void __launch_bounds__(kThreads) fwd_s_kernel(
             if (q0 + 32 < c1) {  // next chunk in flight while this one is swept
                 tile_load(tiles[warp][buf ^ 1], src + q0 + 32, ldf, min(32, c1 - q0 - 32), nk,
                           lane, true);
+                // the chunk after that into L2 (no shared memory needed)
+                if (q0 + 64 + lane < e) {
+#pragma unroll 8
+                    for (int j = 0; j < 32; ++j)
+                        if (j < nk) prefetch_l2(src + int64_t(j) * ldf + q0 + 64 + lane);
+                }
                 tile_wait<1>();
             } else {
                 tile_wait<0>();
@@ -307,6 +313,13 @@ __global__ void __launch_bounds__(kThreads) bwd_s_kernel(
             if (q0 > c0) {
                 const int n0 = max(c0, q0 - 32);
                 tile_load(tiles[warp][buf ^ 1], xs + n0, ldx, q0 - n0, nk, lane, false);
+                // the chunk after that into L2 (no shared memory needed)
+                const int p0 = max(c0, n0 - 32);
+                if (p0 < n0 && lane < n0 - p0) {
+#pragma unroll 8
+                    for (int j = 0; j < 32; ++j)
+                        if (j < nk) prefetch_l2(xs + int64_t(j) * ldx + p0 + lane);
+                }
                 tile_wait<1>();
             } else {
                 tile_wait<0>();

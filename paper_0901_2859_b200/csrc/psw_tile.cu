@@ -36,6 +36,7 @@ struct TileGeom {
     int n, P, p, NS, W, NW;
     int part_smem;  // 1: segment partials in shared memory, 0: per-CTA global scratch
     int coef_off;   // per-worker coefficient staging (bytes into shared memory)
+    int prefetch;   // L2 prefetch of the worker's next segment in pass 1
     int64_t N, ldf, ldx, ntiles;
 };
 
@@ -72,6 +73,10 @@ __device__ __forceinline__ float ld_hint<float>(const float* p, uint64_t pol) {
     float v;
     asm volatile("ld.global.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
     return v;
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* q) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
 }
 
 // a segment's rows of this thread's RHS into registers
@@ -133,6 +138,17 @@ __global__ void __launch_bounds__(kMaxThreads) tile_kernel(const T* F, T* X, con
             const int len = sd.b - sd.a;
             T v[kSegMax];
             load_seg<T, LAYOUT>(F, g.ldf, k, sd.a, len, kv, keep, v);
+            if (g.prefetch && s + NW < NS) {
+                // the worker's next segment into L2 while this one is in flight
+                const SegDesc sn = tb.desc[s + NW];
+                if (LAYOUT == PSW_LAYOUT_R) {
+                    if (lane == 0)
+                        for (int r = 0; r < sn.b - sn.a; ++r)
+                            prefetch_l2(F + int64_t(sn.a + r) * g.ldf + tile * W);
+                } else if (kv) {
+                    for (int r = 0; r < sn.b - sn.a; r += 16) prefetch_l2(F + k * g.ldf + sn.a + r);
+                }
+            }
             const FusedFwd<T>* cf = stage(ffw + sd.a, len, lane, W, sff);
             __syncwarp(wmask);
             T d = T(0);
@@ -264,19 +280,31 @@ int launch_tile(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_t
     g.ldf = ldf;
     g.ldx = ldx;
     g.ntiles = (N + g.W - 1) / g.W;
+    g.prefetch = env_int("PSW_TILE_PREFETCH", 0);  // measured neutral on C1
     const size_t fixed = (size_t(g.P) * g.W * 2 + size_t(std::max(g.p, 1)) * g.W) * sizeof(double);
     const size_t partb = size_t(g.NS) * g.W * 4 * sizeof(double);
+    constexpr size_t kSmemCap = 227 * 1024;
+    // fewer workers when the per-worker coefficient staging does not fit
+    while (g.NW > 1 && fixed + size_t(g.NW) * coef_stage_bytes<T>() > kSmemCap) g.NW /= 2;
     const size_t coefb = size_t(g.NW) * coef_stage_bytes<T>();
-    g.part_smem = fixed + partb + coefb <= size_t(env_int("PSW_TILE_SMEM_KB", 200)) * 1024 ? 1 : 0;
+    if (fixed + coefb > kSmemCap) {
+        set_error(PSW_NOT_SUPPORTED, "tile path: too many blocks for shared memory");
+        return PSW_NOT_SUPPORTED;
+    }
+    g.part_smem = fixed + partb + coefb <=
+                          std::min(kSmemCap, size_t(env_int("PSW_TILE_SMEM_KB", 200)) * 1024)
+                      ? 1
+                      : 0;
     g.coef_off = int((fixed + (g.part_smem ? partb : 0) + 15) & ~size_t(15));
     const size_t smem = size_t(g.coef_off) + coefb;
 
+    const int nthreads = g.NW * g.W;
     auto kern = tile_kernel<T, LAYOUT>;
     PSW_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int dev = 0, nsm = 0, occ = 0;
     PSW_CUDA_TRY(cudaGetDevice(&dev));
     PSW_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    PSW_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+    PSW_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nthreads, smem));
     if (occ < 1) {
         set_error(PSW_NOT_SUPPORTED, "tile path: kernel does not fit on an SM");
         return PSW_NOT_SUPPORTED;
@@ -304,7 +332,7 @@ int launch_tile(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_t
         std::fprintf(stderr, "tile: W=%d NW=%d NS=%d smem=%zu part_smem=%d occ=%d grid=%lld tiles=%lld\n",
                      g.W, g.NW, g.NS, smem, g.part_smem, occ, (long long)grid, (long long)g.ntiles);
     mark(ev, nev, 0, s);
-    kern<<<unsigned(grid), unsigned(threads), smem, s>>>(static_cast<const T*>(F),
+    kern<<<unsigned(grid), unsigned(nthreads), smem, s>>>(static_cast<const T*>(F),
                                                          static_cast<T*>(X), g, tb);
     const cudaError_t e = cudaGetLastError();
     mark(ev, nev, 1, s);
@@ -319,7 +347,8 @@ int launch_tile(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_t
 bool tile_supported(const psw_plan* pl, int layout, int64_t N) {
     if (pl->world != 1 || N < 1 || N >= (int64_t{1} << 31) || pl->n >= (int64_t{1} << 31))
         return false;
-    if (!pl->d_segdesc || pl->seg_off.empty() || !pl->d_cmat) return false;
+    if (!pl->d_segdesc || pl->seg_off.empty() || (pl->p > 0 && !pl->d_cmat) || pl->P > 256)
+        return false;
     return layout == PSW_LAYOUT_R || layout == PSW_LAYOUT_S;
 }
 
