@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define PSW_ABI_VERSION 1
+#define PSW_ABI_VERSION 2
 
 /* Status codes. The C++ wrapper (parsweep_b200.hpp) maps them back onto the
  * reference exception types of core/errors.hpp:9-62. */
@@ -39,8 +39,22 @@ typedef enum psw_status {
     PSW_NOT_SUPPORTED = 4,    /* e.g. non-symmetric A (Symmetrize route, preliminary.hpp:111-132) */
     PSW_CUDA_ERROR = 5,
     PSW_NCCL_ERROR = 6,
-    PSW_OUT_OF_MEMORY = 7
+    PSW_OUT_OF_MEMORY = 7,
+    PSW_NOT_SYMMETRIZABLE = 8,       /* NotSymmetrizable(k): errors.hpp:29-38; k in last_error_index */
+    PSW_ORACLE_FALLBACK_REQUIRED = 9 /* OracleFallbackRequired: errors.hpp:40-43 */
 } psw_status;
+
+/* GRowStrategy (dichotomy/preliminary.hpp:18-24): how the inverse-matrix
+ * rows of the setup are obtained. AUTO picks DIRECT_SYMMETRIC for
+ * sub == super, otherwise SYMMETRIZE with the reference's automatic
+ * fallbacks to EXPLICIT_INVERSE and TRANSPOSE_SOLVE (preliminary.hpp:111-132). */
+typedef enum psw_grow_strategy {
+    PSW_GROW_AUTO = 0,
+    PSW_GROW_DIRECT_SYMMETRIC = 1,
+    PSW_GROW_SYMMETRIZE = 2,
+    PSW_GROW_EXPLICIT_INVERSE = 3,
+    PSW_GROW_TRANSPOSE_SOLVE = 4
+} psw_grow_strategy;
 
 typedef enum psw_dtype { PSW_F64 = 0, PSW_F32 = 1 } psw_dtype;
 typedef enum psw_layout { PSW_LAYOUT_R = 0, PSW_LAYOUT_S = 1 } psw_layout;
@@ -71,6 +85,8 @@ typedef struct psw_plan_info_t {
     int64_t comm_rounds;    /* RunStats::comm_rounds (run.hpp:93-94) */
     double setup_seconds;   /* host time of the preliminary phase */
     double max_z_norm;      /* PreliminaryData::max_z_norm (preliminary.hpp:75-83) */
+    int32_t strategy_used;  /* psw_grow_strategy: PreliminaryData::strategy_used (:65) */
+    int32_t reserved;
 } psw_plan_info_t;
 
 /* ---- errors ------------------------------------------------------------ */
@@ -91,8 +107,7 @@ int psw_partition_validate(int64_t n, int64_t p, const int64_t* boundaries);
 
 /* ---- setup ------------------------------------------------------------ */
 /* Replaces compute_preliminary(A, part, GRowStrategy::Auto, exec)
- * (dichotomy/preliminary.hpp:171-199) for symmetric A (sub == super,
- * tridiag.hpp:43 -> DirectSymmetric route :110-112). `sub`/`sup` hold n-1
+ * (dichotomy/preliminary.hpp:171-199). `sub`/`sup` hold n-1
  * entries (a_2..a_n / c_1..c_{n-1}), `diag` n entries, all host fp64 (the
  * reference's TridiagMatrix, tridiag.hpp:31-34). `boundaries` are the p
  * one-based interior rows of the reference `Partition` (partition.hpp:16-18).
@@ -103,6 +118,13 @@ int psw_partition_validate(int64_t n, int64_t p, const int64_t* boundaries);
 int psw_plan_create(psw_plan** out, int64_t n, const double* sub, const double* diag,
                     const double* sup, int64_t p, const int64_t* boundaries, int dtype,
                     int device);
+/* compute_preliminary(A, part, strategy) (preliminary.hpp:171-173) with an
+ * explicit psw_grow_strategy. An explicit strategy that cannot be applied
+ * fails like the reference: PSW_NOT_SYMMETRIZABLE (index k) for SYMMETRIZE,
+ * PSW_ORACLE_FALLBACK_REQUIRED for EXPLICIT_INVERSE (core/inverse_rows.hpp:46-80). */
+int psw_plan_create_ex(psw_plan** out, int64_t n, const double* sub, const double* diag,
+                       const double* sup, int64_t p, const int64_t* boundaries, int dtype,
+                       int device, int strategy);
 int psw_plan_destroy(psw_plan* plan);
 int psw_plan_info(const psw_plan* plan, psw_plan_info_t* info);
 

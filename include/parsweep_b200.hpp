@@ -11,7 +11,8 @@
 //     (dichotomy/batch.hpp:57-75)
 //   decompose(n, p).induced_partition().boundaries    decompose_boundaries(n, p)
 //     (runtime/decompose.hpp:23-47)
-//   SolverError / PivotBreakdown / TooManyPEs          same names, same fields
+//   SolverError / PivotBreakdown / TooManyPEs /        same names, same fields
+//   NotSymmetrizable / OracleFallbackRequired
 //     (core/errors.hpp:9-62); invalid input -> std::invalid_argument
 //
 // The matrix and partition parameters are templates: any type with the
@@ -44,6 +45,13 @@ struct PivotBreakdown : SolverError {
 struct TooManyPEs : SolverError {
     using SolverError::SolverError;
 };
+struct NotSymmetrizable : SolverError {  // core/errors.hpp:29-38
+    NotSymmetrizable(std::size_t k, const std::string& msg) : SolverError(msg), index(k) {}
+    std::size_t index;
+};
+struct OracleFallbackRequired : SolverError {  // core/errors.hpp:40-43
+    using SolverError::SolverError;
+};
 struct NotSupported : SolverError {
     using SolverError::SolverError;
 };
@@ -61,6 +69,9 @@ inline void check(int rc) {
             throw PivotBreakdown(static_cast<std::size_t>(psw_last_error_index()), msg);
         case PSW_TOO_MANY_PES: throw TooManyPEs(msg);
         case PSW_NOT_SUPPORTED: throw NotSupported(msg);
+        case PSW_NOT_SYMMETRIZABLE:
+            throw NotSymmetrizable(static_cast<std::size_t>(psw_last_error_index()), msg);
+        case PSW_ORACLE_FALLBACK_REQUIRED: throw OracleFallbackRequired(msg);
         case PSW_OUT_OF_MEMORY: throw std::bad_alloc();
         default: throw CudaError(msg);
     }
@@ -76,16 +87,19 @@ inline std::vector<std::size_t> decompose_boundaries(std::size_t n, std::size_t 
 // dichotomy/preliminary.hpp:53-101, reduced to what the kernels read).
 class Plan {
 public:
+    // strategy: psw_grow_strategy (the reference's GRowStrategy, preliminary.hpp:18-24)
     template <class Matrix, class PartitionT>
-    Plan(const Matrix& A, const PartitionT& part, int dtype = PSW_F64, int device = 0) {
+    Plan(const Matrix& A, const PartitionT& part, int dtype = PSW_F64, int device = 0,
+         int strategy = PSW_GROW_AUTO) {
         const auto n = static_cast<int64_t>(A.diag.size());
         if (A.sub.size() + 1 != A.diag.size() || A.super.size() + 1 != A.diag.size())
             throw std::invalid_argument("TridiagMatrix: off-diagonal lengths must be n-1");
         std::vector<int64_t> b(part.boundaries.begin(), part.boundaries.end());
         if (static_cast<int64_t>(part.n) != n)
             throw std::invalid_argument("Partition order does not match the matrix");
-        check(psw_plan_create(&h_, n, A.sub.data(), A.diag.data(), A.super.data(),
-                              static_cast<int64_t>(b.size()), b.data(), dtype, device));
+        check(psw_plan_create_ex(&h_, n, A.sub.data(), A.diag.data(), A.super.data(),
+                                 static_cast<int64_t>(b.size()), b.data(), dtype, device,
+                                 strategy));
         n_ = n;
     }
     ~Plan() {
@@ -137,8 +151,8 @@ private:
 };
 
 template <class Matrix, class PartitionT>
-Plan compute_preliminary(const Matrix& A, const PartitionT& part) {
-    return Plan(A, part);
+Plan compute_preliminary(const Matrix& A, const PartitionT& part, int strategy = PSW_GROW_AUTO) {
+    return Plan(A, part, PSW_F64, 0, strategy);
 }
 
 // dichotomy/batch.hpp:20-51 for one host RHS (end to end through the GPU).

@@ -111,11 +111,148 @@ uint64_t orc_comm_rounds(int64_t p) {
 /* dichotomy/preliminary.hpp:171-199 with the DirectSymmetric provider
  * (:139-143: g = thomas(A, e_r)); one-sided systems b_left_matrix (:29-37)
  * and b_right_matrix (:41-49); samples as in build_samples (:85-96). */
+/* ------------------------------------------------------------------------ */
+/* GRowProvider (dichotomy/preliminary.hpp:108-157): inverse rows under a
+ * strategy, with the Auto fallbacks of its constructor (:111-132). */
+#define ORC_INVERSE_SCALE_LIMIT 1e280 /* core/inverse_rows.hpp:14 */
+
+typedef struct {
+    int strategy;
+    double *scale, *ssub, *ssup;      /* Symmetrize: core/symmetrize.hpp:21-37 */
+    double *y, *z, *y_rho, *z_rho;    /* ExplicitInverse: core/inverse_rows.hpp:21-80 */
+} grow_ctx;
+
+static void grow_free(grow_ctx* c) {
+    free(c->scale); free(c->ssub); free(c->ssup);
+    free(c->y); free(c->z); free(c->y_rho); free(c->z_rho);
+    memset(c, 0, sizeof(*c));
+}
+
+/* core/symmetrize.hpp:21-37; returns the failing k or -1 */
+static int64_t symmetrize_into(int64_t n, const double* sub, const double* sup, grow_ctx* c) {
+    c->scale[0] = 1.0;
+    for (int64_t k = 1; k < n; ++k) c->scale[k] = 1.0;
+    for (int64_t k = 0; k + 1 < n; ++k) {
+        const double product = sub[k] * sup[k];
+        if (!(product > 0.0)) return k;
+        c->scale[k + 1] = c->scale[k] * sqrt(sub[k] / sup[k]);
+        const double off = copysign(sqrt(product), sup[k]);
+        c->ssub[k] = off;
+        c->ssup[k] = off;
+    }
+    return -1;
+}
+
+/* core/inverse_rows.hpp:46-80; ORC_OK, ORC_ORACLE_FALLBACK or a pivot breakdown */
+static int inverse_factors(int64_t n, const double* sub, const double* diag, const double* sup,
+                           grow_ctx* c, double* e, double* al, double* be, int64_t* bad) {
+    for (int64_t k = 0; k + 1 < n; ++k)
+        if (sub[k] == 0.0 || sup[k] == 0.0) return ORC_ORACLE_FALLBACK;
+    memset(e, 0, sizeof(double) * (size_t)n);
+    e[n - 1] = 1.0;
+    int rc = thomas_scratch(n, sub, diag, sup, e, c->y, al, be, bad);
+    if (rc) return rc;
+    if (!(fabs(c->y[0]) >= 1.0 / ORC_INVERSE_SCALE_LIMIT)) return ORC_ORACLE_FALLBACK;
+    memset(e, 0, sizeof(double) * (size_t)n);
+    e[0] = 1.0 / c->y[0];
+    rc = thomas_scratch(n, sub, diag, sup, e, c->z, al, be, bad);
+    if (rc) return rc;
+    double rho = 1.0;
+    for (int64_t j = 0; j < n; ++j) {
+        if (j > 0) rho *= sup[j - 1] / sub[j - 1];
+        if (!(fabs(rho) <= ORC_INVERSE_SCALE_LIMIT && fabs(rho) >= 1.0 / ORC_INVERSE_SCALE_LIMIT))
+            return ORC_ORACLE_FALLBACK;
+        c->y_rho[j] = c->y[j] * rho;
+        c->z_rho[j] = c->z[j] * rho;
+        if (!isfinite(c->y_rho[j]) || !isfinite(c->z_rho[j])) return ORC_ORACLE_FALLBACK;
+    }
+    return ORC_OK;
+}
+
+static int grow_init(int64_t n, const double* sub, const double* diag, const double* sup,
+                     int requested, grow_ctx* c, double* e, double* al, double* be,
+                     int64_t* bad) {
+    memset(c, 0, sizeof(*c));
+    int s = requested;
+    if (s == ORC_GROW_AUTO) {
+        int sym = 1;
+        for (int64_t k = 0; k + 1 < n && sym; ++k) sym = sub[k] == sup[k];
+        s = sym ? ORC_GROW_DIRECT_SYMMETRIC : ORC_GROW_SYMMETRIZE;
+    }
+    const size_t sz = (size_t)n;
+    if (s == ORC_GROW_SYMMETRIZE) {
+        c->scale = (double*)malloc(sizeof(double) * sz);
+        c->ssub = (double*)malloc(sizeof(double) * sz);
+        c->ssup = (double*)malloc(sizeof(double) * sz);
+        if (!c->scale || !c->ssub || !c->ssup) return ORC_NO_MEMORY;
+        int64_t k = symmetrize_into(n, sub, sup, c);
+        if (k < 0)
+            for (int64_t i = 0; i < n; ++i)
+                if (!(isfinite(c->scale[i]) && c->scale[i] > 0.0)) { k = 0; break; }
+        if (k >= 0) {
+            if (requested != ORC_GROW_AUTO) {
+                if (bad) *bad = k;
+                return ORC_NOT_SYMMETRIZABLE;
+            }
+            s = ORC_GROW_EXPLICIT_INVERSE;
+        }
+    }
+    if (s == ORC_GROW_EXPLICIT_INVERSE) {
+        c->y = (double*)malloc(sizeof(double) * sz);
+        c->z = (double*)malloc(sizeof(double) * sz);
+        c->y_rho = (double*)malloc(sizeof(double) * sz);
+        c->z_rho = (double*)malloc(sizeof(double) * sz);
+        if (!c->y || !c->z || !c->y_rho || !c->z_rho) return ORC_NO_MEMORY;
+        const int rc = inverse_factors(n, sub, diag, sup, c, e, al, be, bad);
+        if (rc == ORC_ORACLE_FALLBACK) {
+            if (requested != ORC_GROW_AUTO) return ORC_ORACLE_FALLBACK;
+            s = ORC_GROW_TRANSPOSE_SOLVE;
+        } else if (rc) {
+            return rc;
+        }
+    }
+    c->strategy = s;
+    return ORC_OK;
+}
+
+/* GRowProvider::row (preliminary.hpp:136-156): row r0 (0-based) of inv(A) */
+static int grow_row(const grow_ctx* c, int64_t n, const double* sub, const double* diag,
+                    const double* sup, int64_t r0, double* g, double* e, double* al, double* be,
+                    int64_t* bad) {
+    switch (c->strategy) {
+        case ORC_GROW_DIRECT_SYMMETRIC:
+            memset(e, 0, sizeof(double) * (size_t)n);
+            e[r0] = 1.0;
+            return thomas_scratch(n, sub, diag, sup, e, g, al, be, bad);
+        case ORC_GROW_SYMMETRIZE: {
+            memset(e, 0, sizeof(double) * (size_t)n);
+            e[r0] = 1.0;
+            const int rc = thomas_scratch(n, c->ssub, diag, c->ssup, e, g, al, be, bad);
+            if (rc) return rc;
+            for (int64_t j = 0; j < n; ++j) g[j] *= c->scale[r0] / c->scale[j];
+            return ORC_OK;
+        }
+        case ORC_GROW_EXPLICIT_INVERSE:
+            for (int64_t j = 0; j < r0; ++j) g[j] = c->z[r0] * c->y_rho[j];
+            for (int64_t j = r0; j < n; ++j) g[j] = c->y[r0] * c->z_rho[j];
+            return ORC_OK;
+        default: /* TransposeSolve: inverse_row_transpose (core/inverse_rows.hpp:99-104) */
+            memset(e, 0, sizeof(double) * (size_t)n);
+            e[r0] = 1.0;
+            return thomas_scratch(n, sup, diag, sub, e, g, al, be, bad);
+    }
+}
+
 int orc_preliminary(int64_t n, const double* sub, const double* diag, const double* sup,
                     int64_t p, const int64_t* bnd, double* g, double* zr_s, double* zl_s,
                     double* max_z, int64_t* bad) {
-    for (int64_t k = 0; k + 1 < n; ++k)
-        if (sub[k] != sup[k]) return ORC_NOT_SUPPORTED; /* Auto -> Symmetrize route */
+    return orc_preliminary_ex(n, sub, diag, sup, p, bnd, ORC_GROW_AUTO, NULL, g, zr_s, zl_s,
+                              max_z, bad);
+}
+
+int orc_preliminary_ex(int64_t n, const double* sub, const double* diag, const double* sup,
+                       int64_t p, const int64_t* bnd, int strategy, int* used, double* g,
+                       double* zr_s, double* zl_s, double* max_z, int64_t* bad) {
     size_t sz = (size_t)n;
     double* e = (double*)malloc(sizeof(double) * sz);
     double* al = (double*)malloc(sizeof(double) * sz);
@@ -127,14 +264,17 @@ int orc_preliminary(int64_t n, const double* sub, const double* diag, const doub
     double* zr_all = (double*)malloc(sizeof(double) * sz * (size_t)(p > 0 ? p : 1));
     int rc = ORC_OK;
     double mz = 0.0;
+    grow_ctx gc;
+    memset(&gc, 0, sizeof(gc));
     if (!e || !al || !be || !bd || !bs || !bu || !zl_all || !zr_all) { rc = ORC_NO_MEMORY; goto out; }
+    rc = grow_init(n, sub, diag, sup, strategy, &gc, e, al, be, bad);
+    if (rc) goto out;
+    if (used) *used = gc.strategy;
 
     for (int64_t j = 0; j < p; ++j) {
         const int64_t r = bnd[j];
         /* inverse row r (0-based r-1) */
-        memset(e, 0, sizeof(double) * sz);
-        e[r - 1] = 1.0;
-        rc = thomas_scratch(n, sub, diag, sup, e, g + (size_t)j * sz, al, be, bad);
+        rc = grow_row(&gc, n, sub, diag, sup, r - 1, g + (size_t)j * sz, e, al, be, bad);
         if (rc) goto out;
 
         /* z_left: rows 1..r, row r unit, rhs e_last */
@@ -176,6 +316,7 @@ int orc_preliminary(int64_t n, const double* sub, const double* diag, const doub
     }
     if (max_z) *max_z = mz;
 out:
+    grow_free(&gc);
     free(e); free(al); free(be); free(bd); free(bs); free(bu); free(zl_all); free(zr_all);
     return rc;
 }
@@ -383,9 +524,29 @@ static double now_s(void) {
     return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
 }
 
+static int solve_batch_impl(int64_t n, const double* sub, const double* diag, const double* sup,
+                            int64_t p, const int64_t* bnd, int strategy, int64_t nrhs,
+                            const double* F, int64_t ldf, double* X, int64_t ldx, int nthreads,
+                            double* setup_s, double* solve_s, int64_t* bad);
+
 int orc_solve_batch_threads(int64_t n, const double* sub, const double* diag, const double* sup,
                             int64_t p, const int64_t* bnd, int64_t nrhs, const double* F,
                             int64_t ldf, double* X, int64_t ldx, int nthreads,
+                            double* setup_s, double* solve_s, int64_t* bad) {
+    return solve_batch_impl(n, sub, diag, sup, p, bnd, ORC_GROW_AUTO, nrhs, F, ldf, X, ldx,
+                            nthreads, setup_s, solve_s, bad);
+}
+
+int orc_solve_batch_ex(int64_t n, const double* sub, const double* diag, const double* sup,
+                       int64_t p, const int64_t* bnd, int strategy, int64_t nrhs,
+                       const double* F, int64_t ldf, double* X, int64_t ldx, int64_t* bad) {
+    return solve_batch_impl(n, sub, diag, sup, p, bnd, strategy, nrhs, F, ldf, X, ldx, 1, NULL,
+                            NULL, bad);
+}
+
+static int solve_batch_impl(int64_t n, const double* sub, const double* diag, const double* sup,
+                            int64_t p, const int64_t* bnd, int strategy, int64_t nrhs,
+                            const double* F, int64_t ldf, double* X, int64_t ldx, int nthreads,
                             double* setup_s, double* solve_s, int64_t* bad) {
     int rc = orc_partition_validate(n, p, bnd);
     if (rc) return rc;
@@ -394,7 +555,7 @@ int orc_solve_batch_threads(int64_t n, const double* sub, const double* diag, co
     double* zr = (double*)malloc(sizeof(double) * (size_t)(p * p + 1));
     double* zl = (double*)malloc(sizeof(double) * (size_t)(p * p + 1));
     if (!g || !zr || !zl) { free(g); free(zr); free(zl); return ORC_NO_MEMORY; }
-    rc = orc_preliminary(n, sub, diag, sup, p, bnd, g, zr, zl, NULL, bad);
+    rc = orc_preliminary_ex(n, sub, diag, sup, p, bnd, strategy, NULL, g, zr, zl, NULL, bad);
     const double t1 = now_s();
     if (rc == ORC_OK) {
         if (nthreads < 1) nthreads = 1;

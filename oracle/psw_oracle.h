@@ -31,7 +31,18 @@ enum {
     ORC_PIVOT_BREAKDOWN = 2,
     ORC_TOO_MANY_PES = 3,
     ORC_NOT_SUPPORTED = 4,
-    ORC_NO_MEMORY = 7
+    ORC_NO_MEMORY = 7,
+    ORC_NOT_SYMMETRIZABLE = 8,  /* NotSymmetrizable(k), core/errors.hpp:29-38; k in *bad */
+    ORC_ORACLE_FALLBACK = 9     /* OracleFallbackRequired, core/errors.hpp:40-43 */
+};
+
+/* GRowStrategy (dichotomy/preliminary.hpp:18-24) */
+enum {
+    ORC_GROW_AUTO = 0,
+    ORC_GROW_DIRECT_SYMMETRIC = 1,
+    ORC_GROW_SYMMETRIZE = 2,
+    ORC_GROW_EXPLICIT_INVERSE = 3,
+    ORC_GROW_TRANSPOSE_SOLVE = 4
 };
 
 /* core/thomas.hpp:14 */
@@ -52,12 +63,21 @@ int orc_partition_validate(int64_t n, int64_t p, const int64_t* boundaries);
  * level order; level_off[0..depth] the level offsets. Returns depth. */
 int64_t orc_level_sets(int64_t p, int64_t* order, int64_t* level_off);
 
-/* dichotomy/preliminary.hpp:171-199, DirectSymmetric route (:139-143).
+/* dichotomy/preliminary.hpp:171-199 with GRowStrategy Auto (:111-132).
  * g: p*n full inverse rows; zr_s/zl_s: p*p samples (:85-96);
  * max_z (optional): PreliminaryData::max_z_norm (:75-83). */
 int orc_preliminary(int64_t n, const double* sub, const double* diag, const double* sup,
                     int64_t p, const int64_t* bnd, double* g, double* zr_s, double* zl_s,
                     double* max_z, int64_t* bad);
+
+/* Same with an explicit strategy (preliminary.hpp:108-164: Auto picks
+ * DirectSymmetric for sub == super, else Symmetrize -> ExplicitInverse ->
+ * TransposeSolve fallbacks; an explicit strategy that fails reports
+ * ORC_NOT_SYMMETRIZABLE / ORC_ORACLE_FALLBACK). *used receives the
+ * strategy actually used (PreliminaryData::strategy_used). */
+int orc_preliminary_ex(int64_t n, const double* sub, const double* diag, const double* sup,
+                       int64_t p, const int64_t* bnd, int strategy, int* used, double* g,
+                       double* zr_s, double* zl_s, double* max_z, int64_t* bad);
 
 /* dichotomy/betas.hpp:34-59. left/right have p+1 entries. */
 void orc_betas(int64_t n, int64_t p, const int64_t* bnd, const double* g, const double* f,
@@ -89,6 +109,11 @@ int orc_solve_with_preliminary(int64_t n, const double* sub, const double* diag,
 int orc_solve_batch(int64_t n, const double* sub, const double* diag, const double* sup,
                     int64_t p, const int64_t* bnd, int64_t nrhs, const double* F, int64_t ldf,
                     double* X, int64_t ldx, int64_t* bad);
+
+/* orc_solve_batch with an explicit GRowStrategy (batch.hpp:57-61). */
+int orc_solve_batch_ex(int64_t n, const double* sub, const double* diag, const double* sup,
+                       int64_t p, const int64_t* bnd, int strategy, int64_t nrhs,
+                       const double* F, int64_t ldf, double* X, int64_t ldx, int64_t* bad);
 
 /* Same as orc_solve_batch but uses `nthreads` POSIX threads over disjoint RHS
  * slices with one shared preliminary (the labelled harness-level RHS-parallel

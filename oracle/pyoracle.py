@@ -22,6 +22,9 @@ REF_SO = os.path.join(HERE, "_ref", "libpsw_ref.so")            # parity build (
 REF_PERF_SO = os.path.join(HERE, "_ref", "libpsw_ref_perf.so")  # CMake Release flags, CPU baseline
 
 OK, INVALID_ARGUMENT, PIVOT_BREAKDOWN, TOO_MANY_PES, NOT_SUPPORTED = 0, 1, 2, 3, 4
+NOT_SYMMETRIZABLE, ORACLE_FALLBACK = 8, 9
+# GRowStrategy (dichotomy/preliminary.hpp:18-24)
+AUTO, DIRECT_SYMMETRIC, SYMMETRIZE, EXPLICIT_INVERSE, TRANSPOSE_SOLVE = 0, 1, 2, 3, 4
 
 _d = C.POINTER(C.c_double)
 _i64 = C.POINTER(C.c_int64)
@@ -76,6 +79,12 @@ class _Base:
         self._batch = getattr(L, p + "solve_batch")
         self._batch.argtypes = [C.c_int64, _d, _d, _d, C.c_int64, _i64, C.c_int64, _d, C.c_int64,
                                 _d, C.c_int64, _i64]
+        self._prelim_ex = getattr(L, p + "preliminary_ex")
+        self._prelim_ex.argtypes = [C.c_int64, _d, _d, _d, C.c_int64, _i64, C.c_int,
+                                    C.POINTER(C.c_int), _d, _d, _d, _d, _i64]
+        self._batch_ex = getattr(L, p + "solve_batch_ex")
+        self._batch_ex.argtypes = [C.c_int64, _d, _d, _d, C.c_int64, _i64, C.c_int, C.c_int64, _d,
+                                   C.c_int64, _d, C.c_int64, _i64]
 
     @staticmethod
     def _check(rc: int, bad: np.ndarray | None = None):
@@ -103,7 +112,7 @@ class _Base:
         depth = self._levels(p, _ip(order), _ip(off))
         return [order[off[l]: off[l + 1]].tolist() for l in range(depth)]
 
-    def preliminary(self, sub, diag, sup, bnd):
+    def preliminary(self, sub, diag, sup, bnd, strategy: int = AUTO):
         sub, diag, sup = map(_f64, (sub, diag, sup))
         bnd = np.ascontiguousarray(bnd, dtype=np.int64)
         n, p = diag.size, bnd.size
@@ -112,12 +121,14 @@ class _Base:
         zl = np.zeros_like(zr)
         mz = np.zeros(1)
         bad = np.zeros(1, np.int64)
-        rc = self._prelim(n, _dp(sub), _dp(diag), _dp(sup), p, _ip(bnd), _dp(g), _dp(zr), _dp(zl),
-                          _dp(mz), _ip(bad))
+        used = C.c_int(-1)
+        rc = self._prelim_ex(n, _dp(sub), _dp(diag), _dp(sup), p, _ip(bnd), strategy,
+                             C.byref(used), _dp(g), _dp(zr), _dp(zl), _dp(mz), _ip(bad))
         self._check(rc, bad)
-        return {"g": g[:p], "zr": zr[:p, :p], "zl": zl[:p, :p], "max_z": float(mz[0])}
+        return {"g": g[:p], "zr": zr[:p, :p], "zl": zl[:p, :p], "max_z": float(mz[0]),
+                "strategy_used": int(used.value)}
 
-    def solve_batch(self, sub, diag, sup, bnd, F):
+    def solve_batch(self, sub, diag, sup, bnd, F, strategy: int = AUTO):
         """F: (N, n) system-contiguous series; returns X (N, n)."""
         sub, diag, sup = map(_f64, (sub, diag, sup))
         F = _f64(F)
@@ -125,8 +136,8 @@ class _Base:
         N, n = F.shape
         X = np.empty_like(F)
         bad = np.zeros(1, np.int64)
-        rc = self._batch(n, _dp(sub), _dp(diag), _dp(sup), bnd.size, _ip(bnd), N, _dp(F), n,
-                         _dp(X), n, _ip(bad))
+        rc = self._batch_ex(n, _dp(sub), _dp(diag), _dp(sup), bnd.size, _ip(bnd), strategy, N,
+                            _dp(F), n, _dp(X), n, _ip(bad))
         self._check(rc, bad)
         return X
 

@@ -61,12 +61,19 @@ int guarded(F&& body, int64_t* bad) {
     } catch (const parsweep::TooManyPEs& e) {
         g_msg = e.what();
         return 3;
+    } catch (const parsweep::NotSymmetrizable& e) {
+        if (bad) *bad = static_cast<int64_t>(e.index);
+        g_msg = e.what();
+        return 8;
+    } catch (const parsweep::OracleFallbackRequired& e) {
+        g_msg = e.what();
+        return 9;
     } catch (const std::invalid_argument& e) {
         g_msg = e.what();
         return 1;
     } catch (const std::exception& e) {
         g_msg = e.what();
-        return 9;
+        return 10;
     }
 }
 
@@ -105,13 +112,15 @@ int64_t ref_level_sets(int64_t p, int64_t* order, int64_t* level_off) {
     return static_cast<int64_t>(sets.levels.size());
 }
 
-int ref_preliminary(int64_t n, const double* sub, const double* diag, const double* sup,
-                    int64_t p, const int64_t* bnd, double* g, double* zr_s, double* zl_s,
-                    double* max_z, int64_t* bad) {
+int ref_preliminary_ex(int64_t n, const double* sub, const double* diag, const double* sup,
+                       int64_t p, const int64_t* bnd, int strategy, int* used, double* g,
+                       double* zr_s, double* zl_s, double* max_z, int64_t* bad) {
     return guarded([&] {
         auto A = make_matrix(n, sub, diag, sup);
         auto part = make_partition(n, p, bnd);
-        auto prelim = parsweep::compute_preliminary(A, part);
+        auto prelim = parsweep::compute_preliminary(A, part,
+                                                    static_cast<parsweep::GRowStrategy>(strategy));
+        if (used) *used = static_cast<int>(prelim.strategy_used);
         for (int64_t j = 0; j < p; ++j) {
             std::memcpy(g + j * n, prelim.at[j].g_row.data(), sizeof(double) * static_cast<std::size_t>(n));
             for (int64_t i = 0; i < p; ++i) {
@@ -123,20 +132,33 @@ int ref_preliminary(int64_t n, const double* sub, const double* diag, const doub
     }, bad);
 }
 
+int ref_preliminary(int64_t n, const double* sub, const double* diag, const double* sup,
+                    int64_t p, const int64_t* bnd, double* g, double* zr_s, double* zl_s,
+                    double* max_z, int64_t* bad) {
+    return ref_preliminary_ex(n, sub, diag, sup, p, bnd, 0, nullptr, g, zr_s, zl_s, max_z, bad);
+}
+
 // Solve through the reference's production entry point (batch.hpp:57-75),
-// layout S (one contiguous system per RHS).
-int ref_solve_batch(int64_t n, const double* sub, const double* diag, const double* sup,
-                    int64_t p, const int64_t* bnd, int64_t nrhs, const double* F, int64_t ldf,
-                    double* X, int64_t ldx, int64_t* bad) {
+// layout S (one contiguous system per RHS), with a GRowStrategy.
+int ref_solve_batch_ex(int64_t n, const double* sub, const double* diag, const double* sup,
+                       int64_t p, const int64_t* bnd, int strategy, int64_t nrhs,
+                       const double* F, int64_t ldf, double* X, int64_t ldx, int64_t* bad) {
     return guarded([&] {
         auto A = make_matrix(n, sub, diag, sup);
         auto part = make_partition(n, p, bnd);
         std::vector<std::vector<double>> series(static_cast<std::size_t>(nrhs));
         for (int64_t k = 0; k < nrhs; ++k) series[k].assign(F + k * ldf, F + k * ldf + n);
-        auto sol = parsweep::solve_batch(A, part, series);
+        auto sol = parsweep::solve_batch(A, part, series,
+                                         static_cast<parsweep::GRowStrategy>(strategy));
         for (int64_t k = 0; k < nrhs; ++k)
             std::memcpy(X + k * ldx, sol[k].data(), sizeof(double) * static_cast<std::size_t>(n));
     }, bad);
+}
+
+int ref_solve_batch(int64_t n, const double* sub, const double* diag, const double* sup,
+                    int64_t p, const int64_t* bnd, int64_t nrhs, const double* F, int64_t ldf,
+                    double* X, int64_t ldx, int64_t* bad) {
+    return ref_solve_batch_ex(n, sub, diag, sup, p, bnd, 0, nrhs, F, ldf, X, ldx, bad);
 }
 
 // Per-RHS intermediates of one solve: betas and boundary values.

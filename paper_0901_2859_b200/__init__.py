@@ -31,7 +31,7 @@ import numpy as np
 
 __all__ = [
     "TridiagMatrix", "Partition", "Decomposition", "decompose", "compute_preliminary", "Plan",
-    "solve_batch", "SolverError", "PivotBreakdown", "TooManyPEs", "NotSupported", "CudaError",
+    "solve_batch", "SolverError", "PivotBreakdown", "TooManyPEs", "NotSupported", "NotSymmetrizable", "OracleFallbackRequired", "CudaError",
     "F64", "F32", "LAYOUT_R", "LAYOUT_S", "PATH_AUTO", "PATH_STAGED", "PATH_FUSED", "PATH_PIPE", "PATH_TILE", "last_path", "lib",
     "library_path",
 ]
@@ -43,6 +43,9 @@ F64, F32 = 0, 1
 LAYOUT_R, LAYOUT_S = 0, 1
 PATH_AUTO, PATH_STAGED, PATH_FUSED, PATH_PIPE, PATH_TILE = 0, 1, 2, 3, 4
 OK, INVALID_ARGUMENT, PIVOT_BREAKDOWN, TOO_MANY_PES, NOT_SUPPORTED, CUDA_ERROR, NCCL_ERROR, OOM = range(8)
+NOT_SYMMETRIZABLE, ORACLE_FALLBACK_REQUIRED = 8, 9
+# GRowStrategy (dichotomy/preliminary.hpp:18-24)
+GROW_AUTO, GROW_DIRECT_SYMMETRIC, GROW_SYMMETRIZE, GROW_EXPLICIT_INVERSE, GROW_TRANSPOSE_SOLVE = range(5)
 
 
 # ---------------------------------------------------------------- errors
@@ -60,6 +63,18 @@ class PivotBreakdown(SolverError):
 
 class TooManyPEs(SolverError):
     """core/errors.hpp:42-47"""
+
+
+class NotSymmetrizable(SolverError):
+    """core/errors.hpp:29-38 (index = the failing off-diagonal k)"""
+
+    def __init__(self, index: int, msg: str | None = None):
+        super().__init__(msg or f"off-diagonal product sub[{index}]*super[{index}] is not positive")
+        self.index = index
+
+
+class OracleFallbackRequired(SolverError):
+    """core/errors.hpp:40-43"""
 
 
 class NotSupported(SolverError):
@@ -96,6 +111,8 @@ def lib() -> C.CDLL:
         L.psw_decompose.argtypes = [C.c_int64, C.c_int64, i64]
         L.psw_partition_validate.argtypes = [C.c_int64, C.c_int64, i64]
         L.psw_plan_create.argtypes = [C.POINTER(vp), C.c_int64, d, d, d, C.c_int64, i64, C.c_int, C.c_int]
+        L.psw_plan_create_ex.argtypes = [C.POINTER(vp), C.c_int64, d, d, d, C.c_int64, i64, C.c_int,
+                                         C.c_int, C.c_int]
         L.psw_shard_plan_create.argtypes = [C.POINTER(vp), C.c_int64, d, d, d, C.c_int64, i64,
                                             C.c_int, C.c_int, C.c_int, C.c_int]
         L.psw_plan_destroy.argtypes = [vp]
@@ -131,6 +148,10 @@ def _raise(rc: int):
         raise TooManyPEs(msg)
     if rc == NOT_SUPPORTED:
         raise NotSupported(msg)
+    if rc == NOT_SYMMETRIZABLE:
+        raise NotSymmetrizable(idx, msg)
+    if rc == ORACLE_FALLBACK_REQUIRED:
+        raise OracleFallbackRequired(msg)
     if rc == OOM:
         raise MemoryError(msg)
     raise CudaError(f"status {rc}: {msg}")
@@ -272,7 +293,8 @@ class _Info(C.Structure):
     _fields_ = [("n", C.c_int64), ("p", C.c_int64), ("dtype", C.c_int32), ("device", C.c_int32),
                 ("uniform", C.c_int32), ("fused_ok", C.c_int32), ("device_bytes", C.c_int64),
                 ("combine_terms", C.c_int64), ("comm_rounds", C.c_int64),
-                ("setup_seconds", C.c_double), ("max_z_norm", C.c_double)]
+                ("setup_seconds", C.c_double), ("max_z_norm", C.c_double),
+                ("strategy_used", C.c_int32), ("reserved", C.c_int32)]
 
 
 class _Opts(C.Structure):
@@ -297,7 +319,8 @@ class Plan:
     dichotomy/preliminary.hpp:53-101, restricted to what the kernels read)."""
 
     def __init__(self, A: TridiagMatrix, part: Partition, dtype: int = F64, device: int = 0,
-                 rank: int | None = None, world: int | None = None):
+                 rank: int | None = None, world: int | None = None,
+                 strategy: int = GROW_AUTO):
         L = lib()
         A.validate() if A.n() >= 2 else None
         self.n = A.n()
@@ -315,7 +338,7 @@ class Plan:
                 A.super.ctypes.data_as(dp), len(part.boundaries),
                 b.ctypes.data_as(C.POINTER(C.c_int64)), dtype, device)
         if not shard:
-            _check(L.psw_plan_create(*args))
+            _check(L.psw_plan_create_ex(*args, strategy))
         else:  # row shard of a multi-GPU solve (psw_shard_*)
             _check(L.psw_shard_plan_create(*args, self.rank, self.world))
         self._h = h

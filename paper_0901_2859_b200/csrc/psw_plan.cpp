@@ -70,6 +70,153 @@ int64_t thomas(int64_t n, const double* sub, const double* diag, const double* s
     return -1;
 }
 
+// ---- GRowProvider (dichotomy/preliminary.hpp:108-157) --------------------
+// Inverse rows of A under a GRowStrategy; the constructor's Auto fallbacks
+// (:111-132) and failure reports are the reference's, arithmetic included
+// (core/symmetrize.hpp:21-37, core/inverse_rows.hpp:46-104; this file is
+// compiled without FP contraction).
+constexpr double kInverseScaleLimit = 1e280;  // core/inverse_rows.hpp:14
+
+struct GRow {
+    int strategy = PSW_GROW_DIRECT_SYMMETRIC;
+    std::vector<double> scale, ssub, ssup;   // Symmetrize
+    std::vector<double> y, z, y_rho, z_rho;  // ExplicitInverse
+};
+
+// core/inverse_rows.hpp:46-80: PSW_OK, PSW_ORACLE_FALLBACK_REQUIRED (msg) or
+// a pivot breakdown (*bad)
+int inverse_factors(int64_t n, const double* sub, const double* diag, const double* sup, GRow& g,
+                    std::string& msg, int64_t& bad) {
+    for (int64_t k = 0; k + 1 < n; ++k)
+        if (sub[k] == 0.0 || sup[k] == 0.0) {
+            msg = "zero off-diagonal entry: explicit inverse representation is undefined";
+            return PSW_ORACLE_FALLBACK_REQUIRED;
+        }
+    std::vector<double> e(n, 0.0), al(n), be(n);
+    g.y.assign(n, 0.0);
+    g.z.assign(n, 0.0);
+    e[n - 1] = 1.0;
+    bad = thomas(n, sub, diag, sup, e.data(), g.y.data(), al.data(), be.data());
+    if (bad >= 0) return PSW_PIVOT_BREAKDOWN;
+    if (!(std::fabs(g.y[0]) >= 1.0 / kInverseScaleLimit)) {
+        msg = "corner inverse entry underflows the usable scale";
+        return PSW_ORACLE_FALLBACK_REQUIRED;
+    }
+    std::fill(e.begin(), e.end(), 0.0);
+    e[0] = 1.0 / g.y[0];
+    bad = thomas(n, sub, diag, sup, e.data(), g.z.data(), al.data(), be.data());
+    if (bad >= 0) return PSW_PIVOT_BREAKDOWN;
+    g.y_rho.resize(n);
+    g.z_rho.resize(n);
+    double rho = 1.0;
+    for (int64_t j = 0; j < n; ++j) {
+        if (j > 0) rho *= sup[j - 1] / sub[j - 1];
+        if (!(std::fabs(rho) <= kInverseScaleLimit && std::fabs(rho) >= 1.0 / kInverseScaleLimit)) {
+            msg = "cumulative off-diagonal ratio product left [1e-280, 1e280]";
+            return PSW_ORACLE_FALLBACK_REQUIRED;
+        }
+        g.y_rho[j] = g.y[j] * rho;
+        g.z_rho[j] = g.z[j] * rho;
+        if (!std::isfinite(g.y_rho[j]) || !std::isfinite(g.z_rho[j])) {
+            msg = "inverse factor overflow";
+            return PSW_ORACLE_FALLBACK_REQUIRED;
+        }
+    }
+    return PSW_OK;
+}
+
+// GRowProvider constructor: resolves the strategy; sets the error on failure
+int grow_init(int64_t n, const double* sub, const double* diag, const double* sup, int requested,
+              GRow& g) {
+    int s = requested;
+    if (s == PSW_GROW_AUTO) {
+        bool sym = true;
+        for (int64_t k = 0; k + 1 < n && sym; ++k) sym = sub[k] == sup[k];
+        s = sym ? PSW_GROW_DIRECT_SYMMETRIC : PSW_GROW_SYMMETRIZE;
+    }
+    if (s == PSW_GROW_SYMMETRIZE) {  // core/symmetrize.hpp:21-37
+        g.scale.assign(n, 1.0);
+        g.ssub.assign(n > 1 ? n - 1 : 0, 0.0);
+        g.ssup.assign(n > 1 ? n - 1 : 0, 0.0);
+        int64_t fail = -1;
+        for (int64_t k = 0; k + 1 < n; ++k) {
+            const double product = sub[k] * sup[k];
+            if (!(product > 0.0)) {
+                fail = k;
+                break;
+            }
+            g.scale[k + 1] = g.scale[k] * std::sqrt(sub[k] / sup[k]);
+            const double off = std::copysign(std::sqrt(product), sup[k]);
+            g.ssub[k] = off;
+            g.ssup[k] = off;
+        }
+        if (fail < 0)
+            for (double t : g.scale)
+                if (!(std::isfinite(t) && t > 0.0)) {
+                    fail = 0;
+                    break;
+                }
+        if (fail >= 0) {
+            if (requested != PSW_GROW_AUTO) {
+                set_error(PSW_NOT_SYMMETRIZABLE,
+                          "off-diagonal product sub[" + std::to_string(fail) + "]*super[" +
+                              std::to_string(fail) +
+                              "] is not positive; no diagonal similarity transform exists",
+                          fail);
+                return PSW_NOT_SYMMETRIZABLE;
+            }
+            s = PSW_GROW_EXPLICIT_INVERSE;
+        }
+    }
+    if (s == PSW_GROW_EXPLICIT_INVERSE) {
+        std::string msg;
+        int64_t bad = -1;
+        const int rc = inverse_factors(n, sub, diag, sup, g, msg, bad);
+        if (rc == PSW_PIVOT_BREAKDOWN) {
+            set_error(PSW_PIVOT_BREAKDOWN,
+                      "pivot breakdown during forward elimination at row " + std::to_string(bad), bad);
+            return rc;
+        }
+        if (rc == PSW_ORACLE_FALLBACK_REQUIRED) {
+            if (requested != PSW_GROW_AUTO) {
+                set_error(PSW_ORACLE_FALLBACK_REQUIRED, msg);
+                return rc;
+            }
+            s = PSW_GROW_TRANSPOSE_SOLVE;
+        }
+    }
+    g.strategy = s;
+    return PSW_OK;
+}
+
+// GRowProvider::row (preliminary.hpp:136-156): row r0 (0-based) of inv(A)
+// into x; returns the pivot-breakdown row or -1
+int64_t grow_row(const GRow& g, int64_t n, const double* sub, const double* diag,
+                 const double* sup, int64_t r0, double* x, double* e, double* al, double* be) {
+    switch (g.strategy) {
+        case PSW_GROW_DIRECT_SYMMETRIC:
+            std::fill(e, e + n, 0.0);
+            e[r0] = 1.0;
+            return thomas(n, sub, diag, sup, e, x, al, be);
+        case PSW_GROW_SYMMETRIZE: {
+            std::fill(e, e + n, 0.0);
+            e[r0] = 1.0;
+            const int64_t bad = thomas(n, g.ssub.data(), diag, g.ssup.data(), e, x, al, be);
+            if (bad >= 0) return bad;
+            for (int64_t j = 0; j < n; ++j) x[j] *= g.scale[r0] / g.scale[j];
+            return -1;
+        }
+        case PSW_GROW_EXPLICIT_INVERSE:
+            for (int64_t j = 0; j < r0; ++j) x[j] = g.z[r0] * g.y_rho[j];
+            for (int64_t j = r0; j < n; ++j) x[j] = g.y[r0] * g.z_rho[j];
+            return -1;
+        default:  // TransposeSolve: inverse_row_transpose (core/inverse_rows.hpp:99-104)
+            std::fill(e, e + n, 0.0);
+            e[r0] = 1.0;
+            return thomas(n, sup, diag, sub, e, x, al, be);
+    }
+}
+
 // Forward pivots only (for p == 0 the reference fails in the first solve's
 // sweep of A itself, local_solve.hpp:49 -> thomas.hpp:32,38).
 int64_t forward_breakdown(int64_t n, const double* sub, const double* diag, const double* sup) {
@@ -219,13 +366,14 @@ int validate_inputs(int64_t n, const double* sub, const double* diag, const doub
 // the preliminary and returns the combination matrix (psw_combine_matrix).
 int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
                const double* sup, int64_t p, const int64_t* bnd, int dtype, int device,
-               int rank, int world, std::vector<double>* cmat_host = nullptr, bool shard = false);
+               int rank, int world, std::vector<double>* cmat_host = nullptr, bool shard = false,
+               int strategy = PSW_GROW_AUTO);
 
 int build_shard_tables(psw_plan* pl, const std::vector<double>& cmat);  // psw_shard.cu
 
 int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
                const double* sup, int64_t p, const int64_t* bnd, int dtype, int device,
-               int rank, int world, std::vector<double>* cmat_host, bool shard) {
+               int rank, int world, std::vector<double>* cmat_host, bool shard, int strategy) {
     clear_error();
     if (!out) {
         set_error(PSW_INVALID_ARGUMENT, "null plan output");
@@ -242,13 +390,10 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
                   "row sharding needs 0 <= rank < world and P = p+1 blocks divisible by world");
         return PSW_INVALID_ARGUMENT;
     }
-    for (int64_t i = 0; i + 1 < n; ++i)
-        if (sub[i] != sup[i]) {
-            set_error(PSW_NOT_SUPPORTED,
-                      "non-symmetric matrix: GRowStrategy Symmetrize/ExplicitInverse/"
-                      "TransposeSolve are not part of the GPU hot path (SURVEY §8 f4)");
-            return PSW_NOT_SUPPORTED;
-        }
+    if (strategy < PSW_GROW_AUTO || strategy > PSW_GROW_TRANSPOSE_SOLVE) {
+        set_error(PSW_INVALID_ARGUMENT, "unknown GRowStrategy");
+        return PSW_INVALID_ARGUMENT;
+    }
     const auto t0 = std::chrono::steady_clock::now();
 
     auto* pl = new (std::nothrow) psw_plan();
@@ -283,6 +428,12 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
     // ---- preliminary (preliminary.hpp:171-199) --------------------------
     std::vector<double> gr(n, 0.0), gl(n, 0.0), zr(p * p, 0.0), zl(p * p, 0.0);
     double max_z = 0.0;
+    GRow grow;  // the GRowProvider is constructed before any boundary (:179-180)
+    if (int rc = grow_init(n, sub, diag, sup, strategy, grow)) {
+        delete pl;
+        return rc;
+    }
+    pl->info.strategy_used = grow.strategy;
     if (p == 0) {
         int64_t bad = forward_breakdown(n, sub, diag, sup);
         if (bad >= 0) {
@@ -311,11 +462,10 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
                 if (j >= p) break;
                 const int64_t r = bnd[j];
                 Fail& f = fails[j];
-                // g_j = A^-1 e_r (DirectSymmetric, :139-143), restricted to
-                // blocks j and j+1 (the only rows betas.hpp:46-55 reads)
-                std::fill(e.begin(), e.end(), 0.0);
-                e[r - 1] = 1.0;
-                int64_t bad = thomas(n, sub, diag, sup, e.data(), x.data(), al.data(), be.data());
+                // g_j = row r of inv(A) by the resolved strategy (:136-156),
+                // restricted to blocks j and j+1 (the only rows betas.hpp:46-55 reads)
+                int64_t bad = grow_row(grow, n, sub, diag, sup, r - 1, x.data(), e.data(),
+                                       al.data(), be.data());
                 if (bad >= 0) { f = {j, 0, bad}; continue; }
                 for (int32_t q = pl->blk[2 * j]; q < pl->blk[2 * j + 1]; ++q) gr[q] = x[q];
                 for (int32_t q = pl->blk[2 * (j + 1)]; q < pl->blk[2 * (j + 1) + 1]; ++q) gl[q] = x[q];
@@ -577,6 +727,13 @@ int psw_plan_create(psw_plan** out, int64_t n, const double* sub, const double* 
                     const double* sup, int64_t p, const int64_t* boundaries, int dtype,
                     int device) {
     return psw::build_plan(out, n, sub, diag, sup, p, boundaries, dtype, device, 0, 1);
+}
+
+int psw_plan_create_ex(psw_plan** out, int64_t n, const double* sub, const double* diag,
+                       const double* sup, int64_t p, const int64_t* boundaries, int dtype,
+                       int device, int strategy) {
+    return psw::build_plan(out, n, sub, diag, sup, p, boundaries, dtype, device, 0, 1, nullptr,
+                           false, strategy);
 }
 
 int psw_plan_destroy(psw_plan* plan) {

@@ -38,11 +38,34 @@ def case(name, a, b, bnd, F, ref: Reference, extras: bool = True, sup=None):
         d.update(betas_left=np.array(L), betas_right=np.array(R), boundary=np.array(V),
                  combine_terms=np.int64(terms))
         pre = ref.preliminary(a, b, sup, bnd)
-        d.update(zr=pre["zr"], zl=pre["zl"], max_z=np.float64(pre["max_z"]))
+        d.update(zr=pre["zr"], zl=pre["zl"], max_z=np.float64(pre["max_z"]),
+                 strategy_used=np.int64(pre["strategy_used"]))
     _, stats = ref.run_batch(a, b, sup, bnd, F[:1])
     d["comm_rounds"] = np.int64(stats["comm_rounds"])
     np.savez_compressed(os.path.join(OUT, name + ".npz"), **d)
     print(f"{name}: n={b.size} p={len(bnd)} N={F.shape[0]} -> {os.path.getsize(os.path.join(OUT, name + '.npz'))} B")
+
+
+def nonsymmetric(ref: Reference, seed: int = 2026):
+    """Non-symmetric matrices through the reference's Auto GRowStrategy:
+    symmetrizable (-> Symmetrize), mixed off-diagonal signs (-> ExplicitInverse),
+    a zero super entry (-> TransposeSolve) (preliminary.hpp:111-132)."""
+    rng = np.random.default_rng(seed + 40)
+    n = 300
+    bnd = ref.decompose(n, 6)
+    F = configs.uniform(seed + 41, 5 * n, -1, 1).reshape(5, n)
+    sub = -rng.uniform(0.2, 1.0, n - 1)
+    sup = -rng.uniform(0.2, 1.0, n - 1)
+    diag = np.r_[0, np.abs(sub)] + np.r_[np.abs(sup), 0] + rng.uniform(0.5, 1.5, n)
+    case("nonsym_symmetrizable_n300_P6", sub, diag, bnd, F, ref, sup=sup)
+    sub = rng.uniform(-1, 1, n - 1)
+    sup = rng.uniform(-1, 1, n - 1)
+    sup[::3] = -np.sign(sub[::3]) * np.abs(sup[::3])
+    diag = np.r_[0, np.abs(sub)] + np.r_[np.abs(sup), 0] + rng.uniform(0.5, 1.5, n)
+    case("nonsym_mixed_n300_P6", sub, diag, bnd, F, ref, sup=sup)
+    sup = sup.copy()
+    sup[n // 3] = 0.0
+    case("nonsym_reducible_n300_P6", sub, diag, bnd, F, ref, sup=sup)
 
 
 def main():
@@ -50,6 +73,9 @@ def main():
     ref = Reference()
     os.makedirs(OUT, exist_ok=True)
     seed = 2026
+    if len(sys.argv) > 1 and sys.argv[1] == "--nonsymmetric":
+        nonsymmetric(ref, seed)
+        return
 
     # C0 shape: n=1024, P=4, dominant (slack U[0.1,1]), F ~ U[-1,1]
     c0 = configs.CONFIGS["C0"]
@@ -109,6 +135,7 @@ def main():
     bnd = ref.decompose(n, 8)
     F = configs.uniform(seed + 22, 5 * n, -1, 1).reshape(5, n)
     case("mixed_n96_P8", a, b, bnd, F, ref)
+    nonsymmetric(ref, seed)
 
 
 if __name__ == "__main__":

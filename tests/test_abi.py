@@ -39,7 +39,7 @@ def test_library_is_sm100a_cuda(psw):
 
 
 def test_abi_version(psw):
-    assert psw.lib().psw_abi_version() == 1
+    assert psw.lib().psw_abi_version() == 2
 
 
 def test_decompose_matches_reference(psw, orc):
@@ -74,9 +74,32 @@ def test_plan_rejects_invalid_inputs(psw):
         psw.Plan(A, psw.Partition(16, [1, 8]))
     with pytest.raises(ValueError):
         psw.Plan(psw.TridiagMatrix(np.ones(15), np.full(16, np.nan), np.ones(15)), psw.Partition(16, [8]))
-    nonsym = psw.TridiagMatrix(np.full(15, -1.0), np.full(16, 3.0), np.full(15, -0.5))
-    with pytest.raises(psw.NotSupported):
-        psw.Plan(nonsym, psw.Partition(16, [8]))
+    with pytest.raises(ValueError):  # unknown GRowStrategy
+        psw.Plan(A, psw.Partition(16, [8]), strategy=7)
+
+
+def test_plan_strategy_failures_like_reference(psw, orc):
+    """Explicit GRowStrategy failures surface at setup with the reference's
+    exception types and index, before any device is needed
+    (preliminary.hpp:111-132; errors.hpp:29-43)."""
+    from oracle.pyoracle import EXPLICIT_INVERSE, SYMMETRIZE, OracleError
+    rng = np.random.default_rng(5)
+    n = 40
+    sub, sup = rng.uniform(-1, 1, n - 1), rng.uniform(-1, 1, n - 1)
+    sup[::3] = -np.sign(sub[::3]) * np.abs(sup[::3])
+    diag = np.r_[0, np.abs(sub)] + np.r_[np.abs(sup), 0] + 1.0
+    A = psw.TridiagMatrix(sub, diag, sup)
+    part = psw.Partition(n, [10, 20, 30])
+    with pytest.raises(OracleError) as want:
+        orc.preliminary(sub, diag, sup, [10, 20, 30], strategy=SYMMETRIZE)
+    with pytest.raises(psw.NotSymmetrizable) as got:
+        psw.Plan(A, part, strategy=psw.GROW_SYMMETRIZE)
+    assert got.value.index == want.value.index
+    red = psw.TridiagMatrix(-np.ones(5), 2.0 * np.ones(6), np.array([-1.0, -1.0, 0.0, -1.0, -1.0]))
+    with pytest.raises(psw.OracleFallbackRequired):
+        psw.Plan(red, psw.Partition(6, [3]), strategy=psw.GROW_EXPLICIT_INVERSE)
+    with pytest.raises(OracleError):
+        orc.preliminary(red.sub, red.diag, red.super, [3], strategy=EXPLICIT_INVERSE)
 
 
 def test_plan_pivot_breakdown_like_reference(psw, orc):

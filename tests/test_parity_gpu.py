@@ -69,6 +69,8 @@ def test_golden_intermediates_bitwise(psw, cuda, name):
     assert np.array_equal(br[:, :p], g["betas_right"][:, :p])
     assert np.array_equal(V, g["boundary"])
     assert plan.info["combine_terms"] == int(g["combine_terms"])
+    if "strategy_used" in g:  # GRowStrategy resolved like the reference (Auto)
+        assert plan.info["strategy_used"] == int(g["strategy_used"])
     assert plan.info["comm_rounds"] == int(g["comm_rounds"])
     assert plan.info["max_z_norm"] == float(g["max_z"])
 
@@ -266,3 +268,30 @@ def test_config_C3_single_gpu_subset(psw, cuda):
     ks = np.array([0, 1, 511, 1023])
     err, _, _ = _config_run(psw, cuda, CONFIGS["C3"], check_rhs=ks)
     assert err <= FP64_TOL, err
+
+
+@pytest.mark.parametrize("kind", ["symmetrizable", "mixed", "reducible"])
+@pytest.mark.parametrize("strategy", [0, 1, 2, 3, 4])
+def test_nonsymmetric_strategies(psw, cuda, kind, strategy):
+    """GRowStrategy routes (preliminary.hpp:108-164) on the reference's
+    non-symmetric goldens: the same strategy resolves (or fails) like the
+    oracle, which is pinned bitwise to the reference (tests/test_strategies.py),
+    and every path solves within the fp64 gate."""
+    from oracle.pyoracle import Oracle, OracleError
+    g = load_golden(f"nonsym_{kind}_n300_P6")
+    A = psw.TridiagMatrix(g["sub"], g["diag"], g["super"])
+    part = psw.Partition(A.n(), [int(b) for b in g["bnd"]])
+    orc = Oracle()
+    try:
+        pre = orc.preliminary(g["sub"], g["diag"], g["super"], g["bnd"], strategy=strategy)
+        want = orc.solve_batch(g["sub"], g["diag"], g["super"], g["bnd"], g["F"], strategy=strategy)
+    except OracleError as e:
+        with pytest.raises((psw.NotSymmetrizable, psw.OracleFallbackRequired)):
+            psw.Plan(A, part, strategy=strategy)
+        return
+    plan = psw.Plan(A, part, strategy=strategy)
+    assert plan.info["strategy_used"] == pre["strategy_used"]
+    for path in (psw.PATH_STAGED, psw.PATH_AUTO, psw.PATH_TILE):
+        for layout in (0, 1):
+            X = gpu_solve(psw, cuda, plan, g["F"], layout, path=path)
+            assert rel_l2(X, want) <= FP64_TOL, (path, layout, rel_l2(X, want))
