@@ -165,6 +165,23 @@ int psw_solve_host(const psw_plan* plan, const void* F, int64_t ldf, void* X, in
 /* Device kernels launched by the last successful psw_solve* on this thread
  * (launch accounting for the benchmark). */
 int64_t psw_last_launch_count(void);
+/* ---- ADI consumer (poisson/adi.hpp) ----------------
+ * Peaceman-Rachford half-step right-hand sides on the reference's Grid2D
+ * layout ((n1+1) x (n2+1) fp64 nodes, row-major, j contiguous, zero
+ * boundary), device pointers, stream-ordered:
+ *   dir 1: rhs[(i-1)*ldr + (j-1)] = -h1^2 (u/tau + L2 u + f)   (adi.hpp:143-158)
+ *          -> the direction-1 systems (along i) in layout R;
+ *   dir 2: rhs[(i-1)*ldr + (j-1)] = -h2^2 (u/tau + L1 u + f)   (adi.hpp:160-175)
+ *          -> the direction-2 systems (along j) in layout S.
+ * Same operation order as the reference. The driver (AdiWorkspace /
+ * AdiIteration / adi_solve) is paper_0901_2859_b200/adi.py. */
+int psw_adi_rhs(int dir, const double* u, const double* f, double* rhs, int64_t ldr, int64_t n1,
+                int64_t n2, double h1, double h2, double tau, void* stream);
+/* out2[0] = max |a - b|, out2[1] = max |b| over `count` doubles (device
+ * pointers; max_abs_diff / max_abs of poisson/grid2d.hpp:43-53). */
+int psw_grid_max_abs_diff(const double* a, const double* b, int64_t count, double* out2,
+                          void* stream);
+
 /* psw_path taken by the last psw_solve/psw_solve_ex on this thread (0 before any). */
 int psw_last_path(void);
 

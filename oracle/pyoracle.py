@@ -243,6 +243,45 @@ class Reference(_Base):
         L.ref_solve_rhs_parallel.argtypes = [C.c_int64, _d, _d, _d, C.c_int64, _i64, C.c_int64,
                                              _d, C.c_int64, _d, C.c_int64, C.c_int, _d, _d, _i64]
         L.ref_hardware_concurrency.restype = C.c_int
+        L.ref_adi_iteration_bound.argtypes = [C.c_int64, C.c_double]
+        L.ref_adi_iteration_bound.restype = C.c_int64
+        L.ref_adi_parameters.argtypes = [C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int64,
+                                         C.c_int64, _d]
+        L.ref_adi_steps.argtypes = [C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int64,
+                                    C.c_int64, _d, _d, C.c_int64]
+        L.ref_adi_solve.argtypes = [C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int64,
+                                    C.c_int64, C.c_double, _d, _d, _d, _d, _i64]
+        L.ref_model_problem.argtypes = [C.c_int64, C.c_int64, _d, _d]
+
+    # ---- poisson/adi.hpp (the ADI consumer) -------------
+    def adi_iteration_bound(self, n: int, eps: float) -> int:
+        return int(self.lib.ref_adi_iteration_bound(n, eps))
+
+    def adi_parameters(self, n1, n2, h1, h2, cycle, pes=1):
+        taus = np.zeros(max(cycle, 1))
+        self._check(self.lib.ref_adi_parameters(n1, n2, h1, h2, cycle, pes, _dp(taus)))
+        return taus
+
+    def adi_steps(self, n1, n2, h1, h2, cycle, pes, f, u, steps):
+        f, u = _f64(f), _f64(u).copy()
+        self._check(self.lib.ref_adi_steps(n1, n2, h1, h2, cycle, pes, _dp(f), _dp(u), steps))
+        return u
+
+    def adi_solve(self, n1, n2, h1, h2, cycle, pes, eps, f, u0, exact=None):
+        f, u0 = _f64(f), _f64(u0)
+        u = np.empty_like(u0)
+        its = np.zeros(1, np.int64)
+        ex = _f64(exact) if exact is not None else None
+        rc = self.lib.ref_adi_solve(n1, n2, h1, h2, cycle, pes, eps, _dp(f), _dp(u0),
+                                    _dp(ex) if ex is not None else None, _dp(u), _ip(its))
+        self._check(rc)
+        return u, int(its[0])
+
+    def model_problem(self, n1, n2):
+        f = np.zeros((n1 + 1, n2 + 1))
+        ex = np.zeros_like(f)
+        self.lib.ref_model_problem(n1, n2, _dp(f), _dp(ex))
+        return f, ex
 
     def betas_boundaries(self, sub, diag, sup, bnd, f):
         sub, diag, sup, f = map(_f64, (sub, diag, sup, f))

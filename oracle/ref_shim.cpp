@@ -25,6 +25,8 @@
 #include "parsweep/dichotomy/preliminary.hpp"
 #include "parsweep/runtime/decompose.hpp"
 #include "parsweep/runtime/run.hpp"
+#include "parsweep/poisson/adi.hpp"
+#include "parsweep/poisson/model_problem.hpp"
 
 namespace {
 
@@ -68,6 +70,9 @@ int guarded(F&& body, int64_t* bad) {
     } catch (const parsweep::OracleFallbackRequired& e) {
         g_msg = e.what();
         return 9;
+    } catch (const parsweep::NonConvergence& e) {
+        g_msg = e.what();
+        return 11;
     } catch (const std::invalid_argument& e) {
         g_msg = e.what();
         return 1;
@@ -240,6 +245,72 @@ int ref_solve_rhs_parallel(int64_t n, const double* sub, const double* diag, con
         for (auto& e : errs)
             if (e) std::rethrow_exception(e);
     }, bad);
+}
+
+// ---- ADI consumer (poisson/adi.hpp), §8(f) rank 1 -----------------------
+namespace {
+parsweep::poisson::Grid2D make_grid(int64_t n1, int64_t n2, double h1, double h2, const double* v) {
+    parsweep::poisson::Grid2D g(static_cast<std::size_t>(n1), static_cast<std::size_t>(n2), h1, h2);
+    if (v) std::memcpy(g.values.data(), v, sizeof(double) * g.values.size());
+    return g;
+}
+}  // namespace
+
+int64_t ref_adi_iteration_bound(int64_t n, double eps) {
+    return static_cast<int64_t>(parsweep::poisson::adi_iteration_bound(static_cast<std::size_t>(n), eps));
+}
+
+// AdiWorkspace(n1, n2, h1, h2, cycle, pes).parameters() -> taus[cycle]
+int ref_adi_parameters(int64_t n1, int64_t n2, double h1, double h2, int64_t cycle, int64_t pes,
+                       double* taus) {
+    return guarded([&] {
+        parsweep::poisson::AdiWorkspace ws(static_cast<std::size_t>(n1), static_cast<std::size_t>(n2),
+                                           h1, h2, static_cast<std::size_t>(cycle),
+                                           static_cast<std::size_t>(pes));
+        for (std::size_t k = 0; k < ws.parameters().size(); ++k) taus[k] = ws.parameters()[k];
+    }, nullptr);
+}
+
+// `steps` AdiIteration steps k = 0..steps-1 on u (in place)
+int ref_adi_steps(int64_t n1, int64_t n2, double h1, double h2, int64_t cycle, int64_t pes,
+                  const double* f, double* u, int64_t steps) {
+    return guarded([&] {
+        parsweep::poisson::AdiWorkspace ws(static_cast<std::size_t>(n1), static_cast<std::size_t>(n2),
+                                           h1, h2, static_cast<std::size_t>(cycle),
+                                           static_cast<std::size_t>(pes));
+        auto fg = make_grid(n1, n2, h1, h2, f);
+        auto ug = make_grid(n1, n2, h1, h2, u);
+        parsweep::poisson::AdiIteration it(ws, fg);
+        for (int64_t k = 0; k < steps; ++k) it.step(ug, static_cast<std::size_t>(k));
+        std::memcpy(u, ug.values.data(), sizeof(double) * ug.values.size());
+    }, nullptr);
+}
+
+// adi_solve(f, eps, u0, ws, serial, exact?) -> u, iterations
+int ref_adi_solve(int64_t n1, int64_t n2, double h1, double h2, int64_t cycle, int64_t pes,
+                  double eps, const double* f, const double* u0, const double* exact, double* u,
+                  int64_t* iterations) {
+    return guarded([&] {
+        parsweep::poisson::AdiWorkspace ws(static_cast<std::size_t>(n1), static_cast<std::size_t>(n2),
+                                           h1, h2, static_cast<std::size_t>(cycle),
+                                           static_cast<std::size_t>(pes));
+        auto fg = make_grid(n1, n2, h1, h2, f);
+        auto ug = make_grid(n1, n2, h1, h2, u0);
+        parsweep::poisson::Grid2D ex;
+        if (exact) ex = make_grid(n1, n2, h1, h2, exact);
+        auto r = parsweep::poisson::adi_solve(fg, eps, ug, ws, parsweep::serial_executor(),
+                                              exact ? &ex : nullptr);
+        std::memcpy(u, r.u.values.data(), sizeof(double) * r.u.values.size());
+        *iterations = static_cast<int64_t>(r.iterations);
+    }, nullptr);
+}
+
+// model_problem(n1, n2) -> f, exact
+void ref_model_problem(int64_t n1, int64_t n2, double* f, double* exact) {
+    auto [fg, eg] = parsweep::poisson::model_problem(static_cast<std::size_t>(n1),
+                                                     static_cast<std::size_t>(n2));
+    std::memcpy(f, fg.values.data(), sizeof(double) * fg.values.size());
+    std::memcpy(exact, eg.values.data(), sizeof(double) * eg.values.size());
 }
 
 int ref_hardware_concurrency(void) { return static_cast<int>(std::thread::hardware_concurrency()); }

@@ -1,0 +1,118 @@
+// ADI line-sweep consumer (poisson/adi.hpp): the
+// Peaceman-Rachford half-step right-hand sides and the convergence norms.
+//
+// A half step along direction 1 solves, for every interior line j,
+//   (T - (h1^2/tau) I) u+ = -h1^2 (u/tau + L2 u + f)      (adi.hpp:143-158)
+// and along direction 2, for every interior line i,
+//   (T - (h2^2/tau) I) u' = -h2^2 (u+/tau + L1 u+ + f)    (adi.hpp:160-175).
+// The grid is the reference's Grid2D: (n1+1) x (n2+1) nodes, row-major with
+// j contiguous, zero Dirichlet boundary. Direction-1 systems run along i, so
+// their right-hand sides are written RHS-contiguous (layout R: row i - 1,
+// RHS j - 1) and solved straight into the interior of the half-step grid;
+// direction-2 systems run along j (layout S: system i - 1 contiguous). The
+// stencil arithmetic is the reference's, operation for operation.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "parsweep_b200.h"
+#include "psw_internal.h"
+
+namespace psw {
+namespace {
+
+__global__ void adi_rhs_kernel(const double* __restrict__ u, const double* __restrict__ f,
+                               double* __restrict__ rhs, int64_t ldr, int64_t n1, int64_t n2,
+                               double h1, double h2, double tau, int dir) {
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x + 1;
+    const int64_t i = int64_t(blockIdx.y) + 1;
+    if (j >= n2 || i >= n1) return;
+    const int64_t ld = n2 + 1;
+    const int64_t c = i * ld + j;
+    const double uc = u[c];
+    double lam, hs;
+    if (dir == 1) {  // adi.hpp:148-150
+        lam = __ddiv_rn(__dadd_rn(__dsub_rn(u[c + 1], __dmul_rn(2.0, uc)), u[c - 1]),
+                        __dmul_rn(h2, h2));
+        hs = __dmul_rn(-h1, h1);
+    } else {  // adi.hpp:165-167
+        lam = __ddiv_rn(__dadd_rn(__dsub_rn(u[c + ld], __dmul_rn(2.0, uc)), u[c - ld]),
+                        __dmul_rn(h1, h1));
+        hs = __dmul_rn(-h2, h2);
+    }
+    rhs[(i - 1) * ldr + (j - 1)] = __dmul_rn(hs, __dadd_rn(__dadd_rn(__ddiv_rn(uc, tau), lam), f[c]));
+}
+
+// out[0] = max |a - b|, out[1] = max |b| (non-negative doubles order like
+// their bit patterns, so an integer atomicMax reduces them exactly)
+__global__ void max_abs_diff_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                    int64_t count, unsigned long long* out) {
+    double md = 0.0, mb = 0.0;
+    for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < count;
+         k += int64_t(gridDim.x) * blockDim.x) {
+        const double bv = b[k];
+        md = fmax(md, fabs(a[k] - bv));
+        mb = fmax(mb, fabs(bv));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        md = fmax(md, __shfl_xor_sync(0xffffffffu, md, o));
+        mb = fmax(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(md)));
+        atomicMax(out + 1, static_cast<unsigned long long>(__double_as_longlong(mb)));
+    }
+}
+
+}  // namespace
+
+int adi_rhs(int dir, const double* u, const double* f, double* rhs, int64_t ldr, int64_t n1,
+            int64_t n2, double h1, double h2, double tau, cudaStream_t s) {
+    if (n1 < 2 || n2 < 2) return PSW_OK;
+    const dim3 grid(unsigned((n2 - 1 + 127) / 128), unsigned(n1 - 1));
+    adi_rhs_kernel<<<grid, 128, 0, s>>>(u, f, rhs, ldr, n1, n2, h1, h2, tau, dir);
+    PSW_CUDA_TRY(cudaGetLastError());
+    note_launches(1);
+    return PSW_OK;
+}
+
+int grid_max_abs_diff(const double* a, const double* b, int64_t count, double* out2,
+                      cudaStream_t s) {
+    PSW_CUDA_TRY(cudaMemsetAsync(out2, 0, 2 * sizeof(double), s));
+    if (count <= 0) return PSW_OK;
+    const int64_t blocks = std::min<int64_t>((count + 255) / 256, 148 * 8);
+    max_abs_diff_kernel<<<unsigned(blocks), 256, 0, s>>>(
+        a, b, count, reinterpret_cast<unsigned long long*>(out2));
+    PSW_CUDA_TRY(cudaGetLastError());
+    note_launches(1);
+    return PSW_OK;
+}
+
+}  // namespace psw
+
+extern "C" {
+
+int psw_adi_rhs(int dir, const double* u, const double* f, double* rhs, int64_t ldr, int64_t n1,
+                int64_t n2, double h1, double h2, double tau, void* stream) {
+    psw::clear_error();
+    psw::reset_launches();
+    if ((dir != 1 && dir != 2) || !u || !f || !rhs || ldr < n2 - 1 || !(tau > 0.0)) {
+        psw::set_error(PSW_INVALID_ARGUMENT, "psw_adi_rhs: invalid arguments");
+        return PSW_INVALID_ARGUMENT;
+    }
+    return psw::adi_rhs(dir, u, f, rhs, ldr, n1, n2, h1, h2, tau, static_cast<cudaStream_t>(stream));
+}
+
+int psw_grid_max_abs_diff(const double* a, const double* b, int64_t count, double* out2,
+                          void* stream) {
+    psw::clear_error();
+    psw::reset_launches();
+    if (!a || !b || !out2 || count < 0) {
+        psw::set_error(PSW_INVALID_ARGUMENT, "psw_grid_max_abs_diff: invalid arguments");
+        return PSW_INVALID_ARGUMENT;
+    }
+    return psw::grid_max_abs_diff(a, b, count, out2, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -68,6 +68,31 @@ def nonsymmetric(ref: Reference, seed: int = 2026):
     case("nonsym_reducible_n300_P6", sub, diag, bnd, F, ref, sup=sup)
 
 
+def adi(ref: Reference, seed: int = 2026):
+    """The ADI consumer (poisson/adi.hpp): three Peaceman-Rachford steps on a
+    non-square mesh with a random start (1 and 3 dichotomy PEs), and a full
+    adi_solve of the model problem."""
+    for n1, n2, pes in ((24, 18, 1), (40, 33, 3)):
+        h1, h2 = 1.0 / n1, 1.0 / n2
+        f, exact = ref.model_problem(n1, n2)
+        rng = np.random.default_rng(seed + n1)
+        u0 = np.zeros((n1 + 1, n2 + 1))
+        u0[1:-1, 1:-1] = rng.uniform(-1, 1, (n1 - 1, n2 - 1))
+        cycle = 5
+        u3 = ref.adi_steps(n1, n2, h1, h2, cycle, pes, f, u0, 3)
+        taus = ref.adi_parameters(n1, n2, h1, h2, cycle, pes)
+        np.savez_compressed(os.path.join(OUT, f"adi_steps_{n1}x{n2}_pes{pes}.npz"), n1=n1, n2=n2,
+                            pes=pes, cycle=cycle, f=f, u0=u0, u3=u3, taus=taus)
+        print(f"adi_steps_{n1}x{n2}_pes{pes}")
+    n, eps, pes = 32, 1e-5, 2
+    f, exact = ref.model_problem(n, n)
+    cycle = ref.adi_iteration_bound(n, eps)
+    u, its = ref.adi_solve(n, n, 1.0 / n, 1.0 / n, cycle, pes, eps, f, np.zeros_like(f))
+    np.savez_compressed(os.path.join(OUT, "adi_solve_32x32.npz"), n=n, eps=eps, pes=pes,
+                        cycle=cycle, f=f, exact=exact, u=u, iterations=its)
+    print(f"adi_solve_32x32: {its} iterations (cycle {cycle})")
+
+
 def main():
     build(ref=True)
     ref = Reference()
@@ -75,6 +100,9 @@ def main():
     seed = 2026
     if len(sys.argv) > 1 and sys.argv[1] == "--nonsymmetric":
         nonsymmetric(ref, seed)
+        return
+    if len(sys.argv) > 1 and sys.argv[1] == "--adi":
+        adi(ref, seed)
         return
 
     # C0 shape: n=1024, P=4, dominant (slack U[0.1,1]), F ~ U[-1,1]
@@ -136,6 +164,7 @@ def main():
     F = configs.uniform(seed + 22, 5 * n, -1, 1).reshape(5, n)
     case("mixed_n96_P8", a, b, bnd, F, ref)
     nonsymmetric(ref, seed)
+    adi(ref, seed)
 
 
 if __name__ == "__main__":
