@@ -606,10 +606,15 @@ Choice choose_w(const psw_plan* pl, int es, int row_bytes) {
     const int P = int(pl->P), m = int(pl->m), S = pl->nseg;
     const int W = row_bytes / es;
     if (S <= 0) return ch;
+    static const int force_g = [] {
+        const char* e = std::getenv("PSW_FUSED_G");  // tuning override
+        return e ? std::atoi(e) : 0;
+    }();
     for (int G = 1; G <= P; ++G) {
         if (P % G) continue;
         const int C = P / G;
         if (C > kMaxCluster) continue;
+        if (force_g > 0 && G != force_g) continue;
         const int rows_alloc = G * m + 1;
         const int nchunks = (rows_alloc + kChunk - 1) / kChunk;
         const size_t smem =
