@@ -717,7 +717,7 @@ int launch_w(const psw_plan* pl, const Choice& ch, const void* F, int64_t ldf, v
     static std::mutex mu;
     static std::vector<std::pair<std::array<int64_t, 6>, int>> cache;
     const std::array<int64_t, 6> key = {int64_t(sizeof(T)), W, ch.C, int64_t(ch.smem), pl->device,
-                                        int64_t(LAG) + 2 * int64_t(GC)};
+                                        int64_t(LAG) + 4 * int64_t(GC)};
     int maxc = 0;
     {
         std::lock_guard<std::mutex> lk(mu);
