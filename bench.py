@@ -45,7 +45,7 @@ def _args():
     ap.add_argument("--config", default="C1")
     ap.add_argument("--P", type=int, default=None, help="override the partition count")
     ap.add_argument("--layout", default=None, choices=[None, "R", "S"])
-    ap.add_argument("--path", default="auto", choices=["auto", "staged", "fused", "pipe", "tile"])
+    ap.add_argument("--path", default="auto", choices=["auto", "staged", "fused", "pipe", "tile", "chunked"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="cpu_baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -293,14 +293,16 @@ def main():
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(2 * l2 // 4 + 1, dtype=torch.float32, device=dev)
     path = {"auto": psw.PATH_AUTO, "staged": psw.PATH_STAGED, "fused": psw.PATH_FUSED,
-            "pipe": psw.PATH_PIPE, "tile": psw.PATH_TILE}[args.path]
+            "pipe": psw.PATH_PIPE, "tile": psw.PATH_TILE, "chunked": psw.PATH_CHUNKED}[args.path]
 
     # discover the kernel count of the chosen path
     plan.solve(F, X, layout=layout, path=path)
     torch.cuda.synchronize()
-    nk = psw.last_launch_count()
+    launches_per_solve = psw.last_launch_count()
     taken = psw.last_path()
-    names = [taken] if nk == 1 else (["fwd", "combine", "bwd"] if nk == 3 else ["fwd", "bwd"])
+    # event marks per path: STAGED brackets its three kernels, the others the whole solve
+    names = ["fwd", "combine", "bwd"] if taken == "staged" else [taken]
+    nk = len(names)
 
     def step(events=None):
         psw.l2_flush(flush)
@@ -319,7 +321,7 @@ def main():
         launches = 0
         for i in range(args.steps):
             step(evs[i])
-            launches += psw.last_launch_count()
+            launches += psw.last_launch_count()  # == launches_per_solve
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
     if dist:
@@ -342,6 +344,7 @@ def main():
     alg = {"fused": units * 2 * es + coef,      # read F, write X
            "pipe": units * 2 * es + coef,       # read F, write X (d round trip in L2)
            "tile": units * 2 * es + coef,       # read F, write X (second read from L2)
+           "chunked": units * 2 * es + coef,    # read F, write X (d~ round trip in L2)
            "fwd": units * 2 * es + coef,        # read F, write d0
            "bwd": units * 2 * es + coef,        # read d0, write X
            "combine": 2 * cfg.P * cfg.nrhs * 8 + max(cfg.P - 1, 1) * cfg.nrhs * 8}[kname]

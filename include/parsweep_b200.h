@@ -67,7 +67,8 @@ typedef enum psw_path {
     PSW_PATH_STAGED = 1,
     PSW_PATH_FUSED = 2,
     PSW_PATH_PIPE = 3,
-    PSW_PATH_TILE = 4
+    PSW_PATH_TILE = 4,
+    PSW_PATH_CHUNKED = 5
 } psw_path;
 
 typedef struct psw_plan psw_plan;

@@ -154,6 +154,9 @@ bool pipe_supported(const psw_plan* plan, int layout, int64_t N, const void* F, 
 int solve_pipe(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx, int64_t N,
                int layout, cudaStream_t s, void** events, int nevents);
 bool tile_supported(const psw_plan* plan, int layout, int64_t N);
+bool chunked_supported(const psw_plan* plan, int layout, int64_t N);
+int solve_chunked(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
+                  int64_t N, int layout, cudaStream_t s, void** events, int nevents);
 int solve_tile(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx, int64_t N,
                int layout, cudaStream_t s, void** events, int nevents);
 int solve_fused(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,

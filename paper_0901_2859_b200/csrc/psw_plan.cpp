@@ -795,7 +795,16 @@ int psw_solve_ex(const psw_plan* plan, const void* F, int64_t ldf, void* X, int6
         opts && (opts->betas_left || opts->betas_right || opts->boundary_values);
     int rc;
     t_last_path = 0;
-    if (path == PSW_PATH_TILE) {
+    if (path == PSW_PATH_CHUNKED) {
+        t_last_path = PSW_PATH_CHUNKED;
+        if (want_intermediates || !psw::chunked_supported(plan, layout, nrhs)) {
+            psw::set_error(PSW_NOT_SUPPORTED, "chunked path does not support this plan/shape");
+            rc = PSW_NOT_SUPPORTED;
+        } else {
+            rc = psw::solve_chunked(plan, F, ldf, X, ldx, nrhs, layout, s,
+                                    opts ? opts->events : nullptr, opts ? opts->nevents : 0);
+        }
+    } else if (path == PSW_PATH_TILE) {
         t_last_path = PSW_PATH_TILE;
         if (want_intermediates || !psw::tile_supported(plan, layout, nrhs)) {
             psw::set_error(PSW_NOT_SUPPORTED, "tile path does not support this plan/shape");
