@@ -356,12 +356,13 @@ constexpr size_t s_smem() {
 // values in shared memory; larger P reads betas from global/L2.
 constexpr int kCombineThreads = 32;
 constexpr int kStageP = 96;
+constexpr int kStageTables = 40;  // Z samples + items in shared memory up to this P
 
 __global__ void __launch_bounds__(kCombineThreads) combine_kernel(
     const double* __restrict__ bl, const double* __restrict__ br, int64_t N, int p,
     const CombineItem* __restrict__ items, const double* __restrict__ zr,
     const double* __restrict__ zl, double* __restrict__ V) {
-    extern __shared__ double sh[];  // [2][P][32] betas + [p][32] values
+    extern __shared__ double sh[];  // [2][P][32] betas + [p][32] values (+ tables)
     const int lane = threadIdx.x;
     const int64_t k0 = int64_t(blockIdx.x) * kCombineThreads;
     const int64_t k = k0 + lane;
@@ -370,6 +371,21 @@ __global__ void __launch_bounds__(kCombineThreads) combine_kernel(
         double* sl = sh;
         double* sr = sh + P * kCombineThreads;
         double* sv = sh + 2 * P * kCombineThreads;
+        if (P <= kStageTables) {
+            // the Z samples and the items as well: the level-order recurrence
+            // then never waits on a cached global load
+            double* szr = sv + p * kCombineThreads;
+            double* szl = szr + p * p;
+            CombineItem* sit = reinterpret_cast<CombineItem*>(szl + p * p);
+            for (int i = lane; i < p * p; i += kCombineThreads) {
+                szr[i] = zr[i];
+                szl[i] = zl[i];
+            }
+            for (int i = lane; i < p; i += kCombineThreads) sit[i] = items[i];
+            zr = szr;
+            zl = szl;
+            items = sit;
+        }
         for (int t = 0; t < P; ++t) {
             sl[t * kCombineThreads + lane] = k < N ? bl[int64_t(t) * N + k] : 0.0;
             sr[t * kCombineThreads + lane] = k < N ? br[int64_t(t) * N + k] : 0.0;
@@ -386,7 +402,11 @@ __global__ void __launch_bounds__(kCombineThreads) combine_kernel(
 }
 
 size_t combine_smem(int64_t P) {
-    return P <= kStageP ? size_t(sizeof(double) * kCombineThreads * (3 * P - 1)) : 0;
+    if (P > kStageP) return 0;
+    size_t b = sizeof(double) * kCombineThreads * (3 * P - 1);
+    if (P <= kStageTables)
+        b += sizeof(double) * 2 * size_t(P - 1) * size_t(P - 1) + sizeof(CombineItem) * size_t(P - 1);
+    return b;
 }
 
 template <typename T>

@@ -1,3 +1,2 @@
-PSW_FUSED_LAG=3 timeout 300 python -m pytest tests/test_parity_gpu.py -x -q -k "fused or golden" 2>&1 | tail -3 > gpurun_out/lt_b1.log
-for L in 3 0; do echo "C1 fused LAG=$L" >> gpurun_out/lt_b1.log; PSW_FUSED_VERBOSE=1 PSW_FUSED_LAG=$L timeout 100 python bench.py --config C1 --path fused --steps 50 --warmup 5 2>&1 | grep -E "^\{|fused:" | sort -u | head -2 >> gpurun_out/lt_b1.log; done
-PSW_FUSED_LAG=3 timeout 100 python tools/trace_fused.py >> gpurun_out/lt_b1.log 2>&1
+timeout 600 python -m pytest tests/test_parity_gpu.py -x -q 2>&1 | tail -2 > gpurun_out/cb_t1.log
+for c in C1 C4; do echo "$c staged" >> gpurun_out/cb_b1.log; timeout 100 python bench.py --config $c --path staged --steps 50 --warmup 5 2>&1 | grep -E "^\{" >> gpurun_out/cb_b1.log; done
