@@ -395,14 +395,14 @@ def run_rows(args, cfg):
     from paper_0901_2859_b200.sharded import ShardedSolver
     rank, world, local = _dist_env()
     torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        import torch.distributed as dist
+    import datetime
+    import torch.distributed as dist
+    if world > 1 or "MASTER_ADDR" in os.environ:  # launched by torchrun (its env:// store)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                                timeout=datetime.timedelta(seconds=120))
+    else:  # plain single process: a private one-rank group for the same code path
         dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % _port(), rank=0,
-                                world_size=1)
+                                world_size=1, timeout=datetime.timedelta(seconds=120))
     dev = torch.device("cuda", local)
     a, b = cfg.matrix_ab(0)
     A = psw.TridiagMatrix.symmetric(a, b)
@@ -431,7 +431,8 @@ def run_rows(args, cfg):
             ms.append((e0, e1))
         torch.cuda.synchronize()
     total = sum(a_.elapsed_time(b_) for a_, b_ in ms)
-    t = torch.tensor([total], dtype=torch.float64, device=dev if world > 1 else "cpu")
+    on_gpu = dist.get_backend() == "nccl"
+    t = torch.tensor([total], dtype=torch.float64, device=dev if on_gpu else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total = float(t.item())
     units = cfg.nrhs * cfg.n

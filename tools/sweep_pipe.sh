@@ -1,2 +1,2 @@
-timeout 600 python -m pytest tests/test_parity_gpu.py -x -q 2>&1 | tail -2 > gpurun_out/cb_t1.log
-for c in C1 C4; do echo "$c staged" >> gpurun_out/cb_b1.log; timeout 100 python bench.py --config $c --path staged --steps 50 --warmup 5 2>&1 | grep -E "^\{" >> gpurun_out/cb_b1.log; done
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29513 bench.py --gpus 1 --mode rows --config C3 --steps 3 --warmup 3 > gpurun_out/tr3.log 2>&1
+timeout 900 python -m pytest tests -q -m gpu 2>&1 | tail -3 > gpurun_out/final_t3.log
