@@ -45,7 +45,7 @@ def _args():
     ap.add_argument("--config", default="C1")
     ap.add_argument("--P", type=int, default=None, help="override the partition count")
     ap.add_argument("--layout", default=None, choices=[None, "R", "S"])
-    ap.add_argument("--path", default="auto", choices=["auto", "staged", "fused", "pipe", "tile", "chunked"])
+    ap.add_argument("--path", default="auto", choices=["auto", "staged", "fused", "pipe", "tile", "chunked", "resweep"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="cpu_baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -293,7 +293,8 @@ def main():
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(2 * l2 // 4 + 1, dtype=torch.float32, device=dev)
     path = {"auto": psw.PATH_AUTO, "staged": psw.PATH_STAGED, "fused": psw.PATH_FUSED,
-            "pipe": psw.PATH_PIPE, "tile": psw.PATH_TILE, "chunked": psw.PATH_CHUNKED}[args.path]
+            "pipe": psw.PATH_PIPE, "tile": psw.PATH_TILE, "chunked": psw.PATH_CHUNKED,
+            "resweep": psw.PATH_RESWEEP}[args.path]
 
     # discover the kernel count of the chosen path
     plan.solve(F, X, layout=layout, path=path)
@@ -301,7 +302,8 @@ def main():
     launches_per_solve = psw.last_launch_count()
     taken = psw.last_path()
     # event marks per path: STAGED brackets its three kernels, the others the whole solve
-    names = ["fwd", "combine", "bwd"] if taken == "staged" else [taken]
+    names = {"staged": ["fwd", "combine", "bwd"],
+             "resweep": ["part", "comb", "solve"]}.get(taken, [taken])
     nk = len(names)
 
     def step(events=None):
@@ -347,6 +349,9 @@ def main():
            "chunked": units * 2 * es + coef,    # read F, write X (d~ round trip in L2)
            "fwd": units * 2 * es + coef,        # read F, write d0
            "bwd": units * 2 * es + coef,        # read d0, write X
+           "part": units * es + coef,           # read F (segment checkpoints: small)
+           "solve": units * 2 * es + coef,      # read F again, write X
+           "comb": 2 * cfg.P * cfg.nrhs * 8 + max(cfg.P - 1, 1) * cfg.nrhs * 8,
            "combine": 2 * cfg.P * cfg.nrhs * 8 + max(cfg.P - 1, 1) * cfg.nrhs * 8}[kname]
     achieved = alg / (kern_ms[j] / 1e3) / 1e9
     solve_gbs = cfg.bytes_min() / (total_ms / args.steps / 1e3) / 1e9

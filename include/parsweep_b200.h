@@ -61,14 +61,18 @@ typedef enum psw_layout { PSW_LAYOUT_R = 0, PSW_LAYOUT_S = 1 } psw_layout;
 
 /* Solve-path selection (psw_solve_ex). AUTO picks the fastest path that
  * supports the plan/shape: FUSED keeps every RHS tile resident on chip and
- * reads F once; STAGED is the general three-kernel path. */
+ * reads F once (layout R, uniform partitions whose blocks fit a cluster);
+ * RESWEEP reads F twice and writes X once with per-segment checkpoints
+ * (fp64 layout R, P <= 64, e.g. the 2^20-row config); STAGED is the general
+ * three-kernel path (and the only one returning betas/boundary values). */
 typedef enum psw_path {
     PSW_PATH_AUTO = 0,
     PSW_PATH_STAGED = 1,
     PSW_PATH_FUSED = 2,
     PSW_PATH_PIPE = 3,
     PSW_PATH_TILE = 4,
-    PSW_PATH_CHUNKED = 5
+    PSW_PATH_CHUNKED = 5,
+    PSW_PATH_RESWEEP = 6
 } psw_path;
 
 typedef struct psw_plan psw_plan;

@@ -157,6 +157,12 @@ bool tile_supported(const psw_plan* plan, int layout, int64_t N);
 bool chunked_supported(const psw_plan* plan, int layout, int64_t N);
 int solve_chunked(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
                   int64_t N, int layout, cudaStream_t s, void** events, int nevents);
+bool resweep_supported(const psw_plan* plan, int layout, int64_t N);
+int solve_resweep(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
+                  int64_t N, int layout, cudaStream_t s, void** events, int nevents);
+// the STAGED dichotomy combination kernel (betas -> boundary values V, p x N)
+int launch_combine(const psw_plan* plan, const double* bl, const double* br, int64_t N, double* V,
+                   cudaStream_t s);
 int solve_tile(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx, int64_t N,
                int layout, cudaStream_t s, void** events, int nevents);
 int solve_fused(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,

@@ -463,6 +463,16 @@ int launch_staged(const psw_plan* pl, const void* Fv, int64_t ldf, void* Xv, int
 
 }  // namespace
 
+int launch_combine(const psw_plan* pl, const double* bl, const double* br, int64_t N, double* V,
+                   cudaStream_t s) {
+    const int p = int(pl->p);
+    if (p <= 0) return PSW_OK;
+    combine_kernel<<<unsigned((N + kCombineThreads - 1) / kCombineThreads), kCombineThreads,
+                     combine_smem(pl->P), s>>>(bl, br, N, p, pl->d_items, pl->d_zr, pl->d_zl, V);
+    PSW_CUDA_TRY(cudaGetLastError());
+    return PSW_OK;
+}
+
 int solve_staged(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_t ldx, int64_t N,
                  int layout, cudaStream_t s, double* ext_bl, double* ext_br, double* ext_v,
                  void** events, int nevents) {

@@ -1,0 +1,68 @@
+"""RESWEEP path (psw_resweep.cu): F read twice, X written once, per-segment
+checkpoints of the block sweeps. Betas and boundary values are the STAGED
+path's (bitwise the reference's), so X agrees with STAGED to rounding; the fp64
+gate against the reference on every golden case, both dtypes, ragged N,
+padded leading dimensions, in place and out of place."""
+import numpy as np
+import pytest
+
+from conftest import golden_cases, load_golden, rel_l2
+from test_parity_gpu import FP32_TOL, FP64_TOL, gpu_solve, plan_for
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_resweep_golden(psw, cuda, name):
+    g = load_golden(name)
+    plan = plan_for(psw, g)
+    ref = gpu_solve(psw, cuda, plan, g["F"], 0, path=psw.PATH_STAGED)
+    X = gpu_solve(psw, cuda, plan, g["F"], 0, path=psw.PATH_RESWEEP)
+    assert rel_l2(X, ref) <= 1e-12, (name, rel_l2(X, ref))
+    assert rel_l2(X, g["X"]) <= FP64_TOL, (name, rel_l2(X, g["X"]))
+
+
+@pytest.mark.parametrize("N", [1, 5, 127, 129, 1000])
+def test_resweep_ragged(psw, cuda, N):
+    g = load_golden("c1_n4096_P16")
+    plan = plan_for(psw, g)
+    F = np.random.default_rng(N).standard_normal((N, 4096))
+    ref = gpu_solve(psw, cuda, plan, F, 0, path=psw.PATH_STAGED)
+    X = gpu_solve(psw, cuda, plan, F, 0, path=psw.PATH_RESWEEP)
+    X2 = gpu_solve(psw, cuda, plan, F, 0, path=psw.PATH_RESWEEP, inplace=False, pad=3)
+    assert rel_l2(X, ref) <= 1e-13
+    assert np.array_equal(X, X2)
+
+
+@pytest.mark.parametrize("name", ["c2_n8192_P8", "c2_n8192_P64", "c2_n8192_P512"])
+def test_resweep_fp32(psw, cuda, name):
+    g = load_golden(name)
+    plan = plan_for(psw, g, dtype=psw.F32)
+    X = gpu_solve(psw, cuda, plan, g["F"], 0, path=psw.PATH_RESWEEP)
+    assert rel_l2(X, g["X"]) <= FP32_TOL
+
+
+def test_resweep_not_layout_s(psw, cuda):
+    g = load_golden("c0_n1024_P4")
+    plan = plan_for(psw, g)
+    with pytest.raises(psw.NotSupported):
+        gpu_solve(psw, cuda, plan, g["F"], 1, path=psw.PATH_RESWEEP)
+
+
+def test_resweep_config_C1(psw, cuda):
+    from paper_0901_2859_b200.configs import CONFIGS
+    from oracle.pyoracle import Oracle
+    cfg = CONFIGS["C1"]
+    a, b = cfg.matrix_ab(0)
+    A = psw.TridiagMatrix.symmetric(a, b)
+    part = psw.decompose(cfg.n, cfg.P).induced_partition()
+    plan = psw.Plan(A, part)
+    F = cuda.empty((cfg.n, cfg.nrhs), dtype=cuda.float64, device="cuda")
+    psw.fill_normal(F, 3)
+    X = cuda.empty_like(F)
+    plan.solve(F, X, path=psw.PATH_RESWEEP)
+    ks = np.arange(0, 4096, 7)
+    Fs = F[:, cuda.from_numpy(ks).cuda()].T.cpu().numpy()
+    Xs = X[:, cuda.from_numpy(ks).cuda()].T.cpu().numpy()
+    want = Oracle().solve_batch_threads(a, b, a, np.array(part.boundaries), Fs, 8)[0]
+    assert rel_l2(Xs, want) <= FP64_TOL
