@@ -1,28 +1,72 @@
 // psw_solve_host: the end-to-end solve_batch (dichotomy/batch.hpp:57-75) on
-// host buffers. RHS chunks are staged through two device slots so that the
-// host->device copy of chunk c+1 and the device->host copy of chunk c-1
-// overlap the solve of chunk c (three streams, event-ordered).
+// host buffers. RHS chunks are staged through kSlots device slots so that
+// the host->device copy of chunk c+1 and the device->host copy of chunk c-1
+// overlap the solve of chunk c (three streams, event-ordered; PCIe copies in
+// both directions run concurrently). Streams, events and the staging buffer
+// are created once per device and reused (a fresh stream-ordered allocation
+// per call is returned to the OS at every synchronisation and re-mapped on
+// the next call, which cost milliseconds per solve).
 #include <algorithm>
+#include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include "psw_internal.h"
 
 namespace {
 
-struct Streams {
+constexpr int kSlots = 3;
+constexpr size_t kChunkBytes = size_t(16) << 20;  // per chunk (>= 8 chunks when there is work)
+
+size_t chunk_bytes() {  // PSW_HOST_CHUNK_MB: tuning override
+    static const size_t b = [] {
+        const char* e = std::getenv("PSW_HOST_CHUNK_MB");
+        const int mb = e ? std::atoi(e) : 0;
+        return mb > 0 ? size_t(mb) << 20 : kChunkBytes;
+    }();
+    return b;
+}
+
+struct HostPipe {
+    std::mutex mu;
+    bool ready = false;
     cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
-    cudaEvent_t up[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr},
-                freed[2] = {nullptr, nullptr};
-    ~Streams() {
-        for (int i = 0; i < 2; ++i) {
-            if (up[i]) cudaEventDestroy(up[i]);
-            if (done[i]) cudaEventDestroy(done[i]);
-            if (freed[i]) cudaEventDestroy(freed[i]);
+    cudaEvent_t up[kSlots] = {}, done[kSlots] = {}, freed[kSlots] = {};
+    void* buf = nullptr;
+    size_t buf_bytes = 0;
+
+    int init() {
+        if (ready) return PSW_OK;
+        PSW_CUDA_TRY(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+        PSW_CUDA_TRY(cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking));
+        PSW_CUDA_TRY(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+        for (int i = 0; i < kSlots; ++i) {
+            PSW_CUDA_TRY(cudaEventCreateWithFlags(&up[i], cudaEventDisableTiming));
+            PSW_CUDA_TRY(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+            PSW_CUDA_TRY(cudaEventCreateWithFlags(&freed[i], cudaEventDisableTiming));
         }
-        if (h2d) cudaStreamDestroy(h2d);
-        if (comp) cudaStreamDestroy(comp);
-        if (d2h) cudaStreamDestroy(d2h);
+        ready = true;
+        return PSW_OK;
+    }
+    int reserve(size_t bytes) {
+        if (bytes <= buf_bytes) return PSW_OK;
+        if (buf) cudaFree(buf);
+        buf = nullptr;
+        buf_bytes = 0;
+        PSW_CUDA_TRY(cudaMalloc(&buf, bytes));
+        buf_bytes = bytes;
+        return PSW_OK;
     }
 };
+
+HostPipe& pipe_for(int dev) {
+    static std::mutex mu;
+    static std::vector<HostPipe*> pipes;
+    std::lock_guard<std::mutex> lk(mu);
+    if (size_t(dev) >= pipes.size()) pipes.resize(size_t(dev) + 1, nullptr);
+    if (!pipes[size_t(dev)]) pipes[size_t(dev)] = new HostPipe();  // lives for the process
+    return *pipes[size_t(dev)];
+}
 
 }  // namespace
 
@@ -45,34 +89,26 @@ extern "C" int psw_solve_host(const psw_plan* plan, const void* F, int64_t ldf, 
     PSW_CUDA_TRY(cudaSetDevice(plan->device));
     const int64_t n = plan->n;
     const size_t es = plan->dtype == PSW_F64 ? 8 : 4;
-    // ~32 MiB per chunk, at least 4 chunks when there is enough work
-    int64_t c = std::max<int64_t>(1, int64_t((32u << 20) / (size_t(n) * es)));
-    c = std::min<int64_t>(c, std::max<int64_t>(1, (nrhs + 3) / 4));
+    int64_t c = std::max<int64_t>(1, int64_t(chunk_bytes() / (size_t(n) * es)));
+    c = std::min<int64_t>(c, std::max<int64_t>(1, (nrhs + 7) / 8));
     if (layout == PSW_LAYOUT_R && c >= 32) c = c / 32 * 32;
     c = std::min(c, nrhs);
     const int64_t nchunks = (nrhs + c - 1) / c;
-    const size_t slot_bytes = size_t(c) * size_t(n) * es;
+    const size_t slot_bytes = (size_t(c) * size_t(n) * es + 255) & ~size_t(255);
 
-    Streams st;
-    PSW_CUDA_TRY(cudaStreamCreateWithFlags(&st.h2d, cudaStreamNonBlocking));
-    PSW_CUDA_TRY(cudaStreamCreateWithFlags(&st.comp, cudaStreamNonBlocking));
-    PSW_CUDA_TRY(cudaStreamCreateWithFlags(&st.d2h, cudaStreamNonBlocking));
-    for (int i = 0; i < 2; ++i) {
-        PSW_CUDA_TRY(cudaEventCreateWithFlags(&st.up[i], cudaEventDisableTiming));
-        PSW_CUDA_TRY(cudaEventCreateWithFlags(&st.done[i], cudaEventDisableTiming));
-        PSW_CUDA_TRY(cudaEventCreateWithFlags(&st.freed[i], cudaEventDisableTiming));
-    }
-    void* buf = nullptr;
-    PSW_CUDA_TRY(cudaMallocAsync(&buf, 2 * slot_bytes, st.comp));
-    PSW_CUDA_TRY(cudaStreamSynchronize(st.comp));
+    HostPipe& st = pipe_for(plan->device);
+    std::lock_guard<std::mutex> lk(st.mu);
+    if (int rc = st.init()) return rc;
+    if (int rc = st.reserve(kSlots * slot_bytes)) return rc;
+    // the pipeline starts after any earlier work of this thread's device
     int64_t launches = 0;
     int rc = PSW_OK;
     for (int64_t ci = 0; ci < nchunks && rc == PSW_OK; ++ci) {
-        const int slot = int(ci & 1);
+        const int slot = int(ci % kSlots);
         const int64_t k0 = ci * c, kc = std::min(c, nrhs - k0);
-        char* dbuf = static_cast<char*>(buf) + slot * slot_bytes;
+        char* dbuf = static_cast<char*>(st.buf) + slot * slot_bytes;
         const int64_t dld = layout == PSW_LAYOUT_R ? kc : n;
-        if (ci >= 2) PSW_CUDA_TRY(cudaStreamWaitEvent(st.h2d, st.freed[slot], 0));
+        if (ci >= kSlots) PSW_CUDA_TRY(cudaStreamWaitEvent(st.h2d, st.freed[slot], 0));
         if (layout == PSW_LAYOUT_R)
             PSW_CUDA_TRY(cudaMemcpy2DAsync(dbuf, size_t(kc) * es,
                                            static_cast<const char*>(F) + size_t(k0) * es,
@@ -100,12 +136,13 @@ extern "C" int psw_solve_host(const psw_plan* plan, const void* F, int64_t ldf, 
                                            size_t(kc), cudaMemcpyDeviceToHost, st.d2h));
         PSW_CUDA_TRY(cudaEventRecord(st.freed[slot], st.d2h));
     }
-    cudaStreamSynchronize(st.d2h);
-    cudaStreamSynchronize(st.comp);
-    cudaFreeAsync(buf, st.comp);
-    cudaStreamSynchronize(st.comp);
+    cudaError_t e1 = cudaStreamSynchronize(st.d2h);
+    cudaError_t e2 = cudaStreamSynchronize(st.comp);
+    cudaStreamSynchronize(st.h2d);
     cudaSetDevice(prev);
     psw::reset_launches();
     psw::note_launches(launches);
+    if (rc == PSW_OK && e1 != cudaSuccess) return psw::cuda_fail(e1, "psw_solve_host d2h");
+    if (rc == PSW_OK && e2 != cudaSuccess) return psw::cuda_fail(e2, "psw_solve_host solve");
     return rc;
 }
