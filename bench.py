@@ -45,7 +45,7 @@ def _args():
     ap.add_argument("--config", default="C1")
     ap.add_argument("--P", type=int, default=None, help="override the partition count")
     ap.add_argument("--layout", default=None, choices=[None, "R", "S"])
-    ap.add_argument("--path", default="auto", choices=["auto", "staged", "fused", "pipe", "tile", "chunked", "resweep"])
+    ap.add_argument("--path", default="auto", choices=["auto", "staged", "fused", "pipe", "tile", "chunked", "resweep", "cluster"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="cpu_baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -294,7 +294,7 @@ def main():
     flush = torch.empty(2 * l2 // 4 + 1, dtype=torch.float32, device=dev)
     path = {"auto": psw.PATH_AUTO, "staged": psw.PATH_STAGED, "fused": psw.PATH_FUSED,
             "pipe": psw.PATH_PIPE, "tile": psw.PATH_TILE, "chunked": psw.PATH_CHUNKED,
-            "resweep": psw.PATH_RESWEEP}[args.path]
+            "resweep": psw.PATH_RESWEEP, "cluster": psw.PATH_CLUSTER}[args.path]
 
     # discover the kernel count of the chosen path
     plan.solve(F, X, layout=layout, path=path)
@@ -347,6 +347,7 @@ def main():
            "pipe": units * 2 * es + coef,       # read F, write X (d round trip in L2)
            "tile": units * 2 * es + coef,       # read F, write X (second read from L2)
            "chunked": units * 2 * es + coef,    # read F, write X (d~ round trip in L2)
+           "cluster": units * 2 * es + coef,    # read F, write X
            "fwd": units * 2 * es + coef,        # read F, write d0
            "bwd": units * 2 * es + coef,        # read d0, write X
            "part": units * es + coef,           # read F (segment checkpoints: small)

@@ -60,8 +60,9 @@ typedef enum psw_dtype { PSW_F64 = 0, PSW_F32 = 1 } psw_dtype;
 typedef enum psw_layout { PSW_LAYOUT_R = 0, PSW_LAYOUT_S = 1 } psw_layout;
 
 /* Solve-path selection (psw_solve_ex). AUTO picks the fastest path that
- * supports the plan/shape: FUSED keeps every RHS tile resident on chip and
- * reads F once (layout R, uniform partitions whose blocks fit a cluster);
+ * supports the plan/shape: CLUSTER and FUSED keep every RHS tile resident on
+ * chip and read F once (layout R, uniform partitions whose blocks fit a
+ * cluster; CLUSTER: one CTA per SM holding G blocks, FUSED: 16-CTA clusters);
  * RESWEEP reads F twice and writes X once with per-segment checkpoints
  * (fp64 layout R, P <= 64, e.g. the 2^20-row config); STAGED is the general
  * three-kernel path (and the only one returning betas/boundary values). */
@@ -72,7 +73,8 @@ typedef enum psw_path {
     PSW_PATH_PIPE = 3,
     PSW_PATH_TILE = 4,
     PSW_PATH_CHUNKED = 5,
-    PSW_PATH_RESWEEP = 6
+    PSW_PATH_RESWEEP = 6,
+    PSW_PATH_CLUSTER = 7
 } psw_path;
 
 typedef struct psw_plan psw_plan;

@@ -32,7 +32,7 @@ import numpy as np
 __all__ = [
     "TridiagMatrix", "Partition", "Decomposition", "decompose", "compute_preliminary", "Plan",
     "solve_batch", "SolverError", "PivotBreakdown", "TooManyPEs", "NotSupported", "NotSymmetrizable", "OracleFallbackRequired", "CudaError",
-    "F64", "F32", "LAYOUT_R", "LAYOUT_S", "PATH_AUTO", "PATH_STAGED", "PATH_FUSED", "PATH_PIPE", "PATH_TILE", "PATH_CHUNKED", "PATH_RESWEEP", "last_path", "lib",
+    "F64", "F32", "LAYOUT_R", "LAYOUT_S", "PATH_AUTO", "PATH_STAGED", "PATH_FUSED", "PATH_PIPE", "PATH_TILE", "PATH_CHUNKED", "PATH_RESWEEP", "PATH_CLUSTER", "last_path", "lib",
     "library_path",
 ]
 
@@ -41,7 +41,7 @@ LIB_PATH = os.path.join(HERE, "_lib", "libparsweep_b200.so")
 
 F64, F32 = 0, 1
 LAYOUT_R, LAYOUT_S = 0, 1
-PATH_AUTO, PATH_STAGED, PATH_FUSED, PATH_PIPE, PATH_TILE, PATH_CHUNKED, PATH_RESWEEP = 0, 1, 2, 3, 4, 5, 6
+PATH_AUTO, PATH_STAGED, PATH_FUSED, PATH_PIPE, PATH_TILE, PATH_CHUNKED, PATH_RESWEEP, PATH_CLUSTER = 0, 1, 2, 3, 4, 5, 6, 7
 OK, INVALID_ARGUMENT, PIVOT_BREAKDOWN, TOO_MANY_PES, NOT_SUPPORTED, CUDA_ERROR, NCCL_ERROR, OOM = range(8)
 NOT_SYMMETRIZABLE, ORACLE_FALLBACK_REQUIRED = 8, 9
 # GRowStrategy (dichotomy/preliminary.hpp:18-24)
@@ -167,7 +167,8 @@ def last_launch_count() -> int:
 
 
 PATH_NAMES = {PATH_STAGED: "staged", PATH_FUSED: "fused", PATH_PIPE: "pipe", PATH_TILE: "tile",
-              PATH_CHUNKED: "chunked", PATH_RESWEEP: "resweep"}
+              PATH_CHUNKED: "chunked", PATH_RESWEEP: "resweep",
+              PATH_CLUSTER: "cluster"}
 
 
 def last_path() -> str:

@@ -1,0 +1,555 @@
+// CLUSTER solve path: one persistent kernel, F read once and X written once
+// (the minimum traffic of SURVEY §8(d)), one CTA per SM holding a whole
+// 128-byte-wide RHS strip of G blocks in shared memory.
+//
+// Layout R, uniform partition (n = P m), P = C G:
+//   * an RHS tile = W right-hand sides (128 contiguous bytes of every row:
+//     the write granularity that keeps HBM writes at full speed);
+//   * a thread-block cluster of C CTAs owns a tile; CTA c owns blocks
+//     [cG, cG + G) = G m rows (+1 for the last block) and keeps them in a
+//     shared-memory slab filled by TMA (W x 32-row boxes, one mbarrier per
+//     box). Clusters are persistent and walk the tiles;
+//   * one thread per (block, 32-row segment, rhs): forward sweep of the
+//     segment from a zero carry with d~ in registers, beta dot products
+//     (betas.hpp:42-57 split by segment) and Lam~ (psw_internal.h); the slab
+//     is handed to TMA for the next tile as soon as every thread swept it;
+//   * a block scan folds the segment partials into exact carries and block
+//     betas, which are pushed to every CTA of the cluster with st.async
+//     (DSMEM stores completing on the receiver's mbarrier);
+//   * each CTA evaluates the G + 1 boundary values it needs from the
+//     combination matrix (psw_plan.cpp combine_matrix: the reference
+//     dichotomy, boundary_solve.hpp:96-121, is linear in the betas);
+//   * a backward block fold gives every segment its exact x_b, and the back
+//     substitution streams X out of registers.
+// Compared with the FUSED path (psw_fused.cu: 16-CTA clusters of one block
+// each, three CTAs per SM), a CTA here holds four blocks (C1: 128 KB of F in
+// flight per SM, four CTAs per exchange) and the sweep coefficients live in
+// bank-padded structure-of-arrays tables next to the slab.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <array>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+#include <vector>
+
+#include "psw_device.cuh"
+#include "psw_internal.h"
+#include "psw_tma.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace psw {
+namespace {
+
+constexpr int kMaxThreads = 512;
+constexpr int kMaxC = 8;                    // portable cluster size
+constexpr size_t kSmemMax = 232448;         // 227 KB per CTA (sm_100)
+constexpr int kSegMax = kSegLen + 1;
+constexpr int kMaxBox = 256;                // TMA box height limit
+
+__device__ __forceinline__ void bar_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+
+__device__ __forceinline__ void st_async_2(uint32_t raddr, double a, double b, uint32_t rbar) {
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(
+            raddr),
+        "d"(a), "d"(b), "r"(rbar)
+        : "memory");
+}
+
+// optional phase trace (PSW_CLUSTER_TRACE=1): clock64 at 8 points of tile 2
+// for every CTA, dumped by the host after the launch
+constexpr int kTraceSlots = 8;
+__device__ unsigned long long g_ctrace[1024 * kTraceSlots];
+
+struct CGeom {
+    int n, P, p, m, G, C, S, H, trace, stagger;  // H: TMA box height (divides m)
+    int64_t N, ldx, ntiles;
+};
+
+// Coefficients of slab row q: two 4-vectors {rp, ma, gr, gl}, {lam, mu, w, al}
+// (64 B for fp64), 16 bytes of padding every 32 rows so that rows q and
+// q + 32 (two segments read by one warp) land in different banks.
+template <typename T>
+struct alignas(4 * sizeof(T)) Quad {
+    T x, y, z, w;
+};
+template <typename T>
+__host__ __device__ __forceinline__ size_t coff(int q) {
+    return size_t(q) * 8 * sizeof(T) + size_t(q >> 5) * 16;
+}
+
+// Shared-memory carve-up (bytes), identical on host and device.
+template <typename T, int W, int NSLAB>
+struct CLayout {
+    int ra;
+    size_t slab_b, coef, seg, allx, vals, cm, segc, bars, total;
+    __host__ __device__ CLayout(int G, int m, int S, int P, int nth) {
+        auto up = [](size_t x) { return (x + 127) & ~size_t(127); };
+        ra = G * m + 1;               // slab rows of the last CTA
+        slab_b = up(size_t(ra) * W * sizeof(T));
+        coef = NSLAB * slab_b;
+        seg = up(coef + coff<T>(ra) + 16);
+        allx = up(seg + size_t(4) * nth * sizeof(double));
+        vals = up(allx + size_t(2) * P * W * 2 * sizeof(double));
+        cm = up(vals + size_t(G + 1) * W * sizeof(double));
+        segc = up(cm + size_t(G + 1) * 2 * P * sizeof(double));
+        bars = up(segc + size_t(G) * S * sizeof(SegCoef));
+        total = bars + size_t(NSLAB * G + 2) * sizeof(uint64_t);
+    }
+};
+
+// forward rows of one segment from a zero carry: d~ into dr, partials to
+// the thread's slots (betas.hpp:42-57 split by segment; Lam~, psw_internal.h)
+template <typename T, int W, int NMAX>
+__device__ __forceinline__ void fwd(const T* slab, const unsigned char* co, int a, int lane,
+                                    int len, T (&dr)[kSegMax], double* sd, double* sx, double* sr,
+                                    double* sl, int tid) {
+    const T* col = slab + size_t(a) * W + lane;
+    T d = T(0), lx = T(0);
+    double br = 0.0, bl = 0.0;
+#pragma unroll
+    for (int r = 0; r < NMAX; ++r) {
+        if (NMAX == kSegLen || r < len) {
+            const Quad<T>* c = reinterpret_cast<const Quad<T>*>(co + coff<T>(a + r));
+            const Quad<T> c0 = c[0];
+            const T lam = c[1].x;
+            const T f = col[r * W];
+            d = fma(c0.y, d, f * c0.x);
+            br = fma(double(f), double(c0.z), br);
+            bl = fma(double(f), double(c0.w), bl);
+            lx = fma(lam, d, lx);
+            dr[r] = d;
+        }
+    }
+    sd[tid] = double(d);
+    sx[tid] = double(lx);
+    sr[tid] = br;
+    sl[tid] = bl;
+}
+
+// back substitution of one segment from the exact carries, last row first
+template <typename T, int NMAX>
+__device__ __forceinline__ void bwd(const unsigned char* co, int a, int len,
+                                    const T (&dr)[kSegMax], T D, T xl, T xn, T* xp, int64_t ldx) {
+#pragma unroll
+    for (int r = NMAX - 1; r >= 0; --r) {
+        if (NMAX == kSegLen || r < len) {
+            const Quad<T> c1 = reinterpret_cast<const Quad<T>*>(co + coff<T>(a + r))[1];
+            xn = fma(c1.w, xn, fma(xl, c1.z, fma(c1.y, D, dr[r])));
+            __stcs(xp + int64_t(r) * ldx, xn);
+        }
+    }
+}
+
+template <typename T, int W, int NSLAB>
+__global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
+    const __grid_constant__ CUtensorMap tmF, const __grid_constant__ CUtensorMap tmF1, T* X,
+    CGeom g, const FusedFwd<T>* __restrict__ gff, const FusedBwd<T>* __restrict__ gfb,
+    const SegCoef* __restrict__ gsegc, const SegDesc* __restrict__ gdesc,
+    const double* __restrict__ gcmat) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int C = g.C, G = g.G, S = g.S, P = g.P, p = g.p, m = g.m;
+    const int crank = int(cluster.block_rank());
+    const int64_t cid = blockIdx.x / C, ncl = gridDim.x / C;
+    // units of W right-hand sides; with two slabs a cluster takes them in
+    // adjacent pairs (2q, 2q + 1), so the two 64-byte halves of every 128-byte
+    // X line are written back to back and merge in L2
+    const int64_t ngroups = (g.ntiles + NSLAB - 1) / NSLAB;
+    const int64_t ntl = ngroups > cid ? NSLAB * ((ngroups - cid + ncl - 1) / ncl) : 0;
+    auto unit = [&](int64_t k) { return (cid + (k / NSLAB) * ncl) * NSLAB + (k % NSLAB); };
+    const int nth = G * S * W;
+    const int tid = threadIdx.x;
+    const CLayout<T, W, NSLAB> L(G, m, S, P, nth);
+    // slab row 0 is global row crank*G*m - 1 (row -1 of CTA 0 is outside F:
+    // TMA zero-fills it)
+    const int base = crank * G * m - 1;
+    const int nrows = crank == C - 1 ? G * m + 1 : G * m;
+    const bool last_cta = crank == C - 1;
+    unsigned char* co = smem + L.coef;  // coefficient rows (coff)
+    double* sd = reinterpret_cast<double*>(smem + L.seg);  // d~ end -> carry D
+    double* sx = sd + nth;                                 // Lam~ -> Lam~ + D K1
+    double* sr = sx + nth;                                 // right partial -> x_b
+    double* sl = sr + nth;                                 // left partial
+    double* allx = reinterpret_cast<double*>(smem + L.allx);  // [2][P][W][R, L]
+    double* vals = reinterpret_cast<double*>(smem + L.vals);  // [G + 1][W]
+    double* cm = reinterpret_cast<double*>(smem + L.cm);      // [G + 1][2P]
+    SegCoef* segc = reinterpret_cast<SegCoef*>(smem + L.segc);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
+    uint64_t* xbar = bars + NSLAB * G;
+
+    const int lane = tid % W, h = tid / W, j = h / S;
+    const int t = crank * G + j;
+    const SegDesc sgd = gdesc[t * S + h % S];
+    const int a = sgd.a - base, len = sgd.b - sgd.a;  // slab rows [a, a + len)
+    const bool first_seg = (h % S) == 0;
+
+    if (tid == 0) {
+        for (int i = 0; i < NSLAB * G; ++i) mbar_init(&bars[i], 1);
+        mbar_init(&xbar[0], 1);
+        mbar_init(&xbar[1], 1);
+        fence_mbar_init();
+    }
+    for (int i = tid; i < nrows; i += nth) {
+        const int q = base + i;
+        if (q < 0) continue;
+        const FusedFwd<T> f = gff[q];
+        const FusedBwd<T> b = gfb[q];
+        Quad<T>* o = reinterpret_cast<Quad<T>*>(co + coff<T>(i));
+        o[0] = {f.rp, f.ma, f.gr, f.gl};
+        o[1] = {f.lam, b.mu, b.w, b.al};
+    }
+    for (int i = tid; i < G * S; i += nth) segc[i] = gsegc[crank * G * S + i];
+    for (int i = tid; i < (G + 1) * 2 * P; i += nth) {  // rows of boundaries crank*G - 1 + r
+        const int bi = crank * G - 1 + i / (2 * P);
+        cm[i] = (bi >= 0 && bi < p) ? gcmat[int64_t(bi) * 2 * P + i % (2 * P)] : 0.0;
+    }
+    __syncthreads();
+    cluster.sync();  // every CTA's exchange barrier is initialised before any push
+
+    auto slab_of = [&](int64_t k) {
+        return reinterpret_cast<T*>(smem + size_t(k % NSLAB) * L.slab_b);
+    };
+    auto bars_of = [&](int64_t k) { return bars + (k % NSLAB) * G; };
+    // rows of block jb of unit k into the slab: m / H boxes (+ the n-th row
+    // for the last block of the last CTA); one mbarrier per block
+    auto issue_block = [&](int64_t k, int jb) {
+        const int k0 = int(unit(k) * W);
+        T* slab = slab_of(k);
+        uint64_t* bar = &bars_of(k)[jb];
+        const bool extra = last_cta && jb == G - 1;
+        mbar_expect_tx(bar, uint32_t((m + (extra ? 1 : 0)) * W * sizeof(T)));
+        for (int r = jb * m; r < (jb + 1) * m; r += g.H)
+            tma_load_2d(slab + size_t(r) * W, &tmF, k0, base + r, bar);
+        if (extra) tma_load_2d(slab + size_t(G * m) * W, &tmF1, k0, base + G * m, bar);
+    };
+    if (tid == 0) {
+        // clusters start spread over `stagger` ns so that their read phases
+        // (slab loads) and write phases (back substitution) interleave
+        if (g.stagger > 0) {
+            uint64_t t0, t1;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+            const uint64_t wait = uint64_t(g.stagger) * uint64_t(cid) / uint64_t(ncl);
+            do {
+                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
+            } while (t1 - t0 < wait);
+        }
+        for (int64_t k = 0; k < NSLAB && k < ntl; ++k)
+            for (int jb = 0; jb < G; ++jb) issue_block(k, jb);
+    }
+    // each block's last thread (not a scan thread when S > 1) streams the
+    // block's rows of the next unit in as soon as the block has swept them
+    const bool block_issuer = (h % S) == S - 1 && lane == W - 1;
+    T dr[kSegMax];
+    auto stamp = [&](int64_t k, int slot) {
+        if (g.trace && k == 2 && tid == 0 && blockIdx.x < 1024)
+            g_ctrace[blockIdx.x * kTraceSlots + slot] = clock64();
+    };
+    for (int64_t k = 0; k < ntl; ++k) {
+        const int buf = int(k & 1);
+        stamp(k, 0);
+        if (tid == 0) mbar_expect_tx(&xbar[buf], uint32_t(P * W * 2 * sizeof(double)));
+        T* slab = slab_of(k);
+        mbar_wait(&bars_of(k)[j], uint32_t((k / NSLAB) & 1));
+        stamp(k, 1);
+        // ---- forward sweep of the segment, d~ in registers
+        if (len == kSegLen)
+            fwd<T, W, kSegLen>(slab, co, a, lane, kSegLen, dr, sd, sx, sr, sl, tid);
+        else
+            fwd<T, W, kSegMax>(slab, co, a, lane, len, dr, sd, sx, sr, sl, tid);
+        bar_sync(2 + j, S * W);  // the block's rows swept, its partials visible
+        stamp(k, 2);
+        if (block_issuer && k + NSLAB < ntl) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue_block(k + NSLAB, j);
+        }
+        // ---- block scan: exact carries, block betas, pushed to every CTA
+        if (first_seg) {
+            double D = 0.0, R = 0.0, Lb = 0.0;
+            for (int q = 0; q < S; ++q) {
+                const int id = (j * S + q) * W + lane;
+                const SegCoef sc = segc[j * S + q];
+                const double dend = sd[id];
+                sd[id] = D;
+                sx[id] = fma(D, sc.k1, sx[id]);
+                R += sr[id];
+                Lb += sl[id];
+                D = fma(sc.mu_end, D, dend);
+            }
+            stamp(k, 7);
+            if (t >= p) R = 0.0;   // right_t exists for t < p (betas.hpp:46-49)
+            if (t == 0) Lb = 0.0;  // left_t for t > 0 (betas.hpp:51-55)
+            double* dst = allx + (size_t(buf) * P + t) * W * 2 + lane * 2;
+            const uint32_t src = smem_u32(dst), bar = smem_u32(&xbar[buf]);
+            for (int c = 0; c < C; ++c) st_async_2(mapa_u32(src, c), R, Lb, mapa_u32(bar, c));
+        }
+        stamp(k, 3);
+        // only the warps evaluating boundary values wait on the exchange (the
+        // others would spin on the barrier and starve the scan's shared loads)
+        const bool comb = tid < (G + 1) * W;
+        if (tid < ((G + 1) * W + 31) / 32 * 32) mbar_wait(&xbar[buf], uint32_t((k >> 1) & 1));
+        stamp(k, 4);
+        // ---- the G + 1 boundary values of this CTA's blocks
+        if (comb) {
+            const int r = tid / W, ln = tid % W;
+            const int bi = crank * G - 1 + r;
+            double v = 0.0;
+            if (bi >= 0 && bi < p) {
+                const double* mr = cm + r * 2 * P;
+                const double* ax = allx + size_t(buf) * P * W * 2 + ln * 2;
+                double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+                int u = 0;
+                for (; u + 2 <= P; u += 2) {
+                    v0 = fma(mr[u], ax[u * W * 2], v0);
+                    v1 = fma(mr[P + u], ax[u * W * 2 + 1], v1);
+                    v2 = fma(mr[u + 1], ax[(u + 1) * W * 2], v2);
+                    v3 = fma(mr[P + u + 1], ax[(u + 1) * W * 2 + 1], v3);
+                }
+                for (; u < P; ++u) {
+                    v0 = fma(mr[u], ax[u * W * 2], v0);
+                    v1 = fma(mr[P + u], ax[u * W * 2 + 1], v1);
+                }
+                v = (v0 + v2) + (v1 + v3);
+            }
+            vals[tid] = v;
+        }
+        bar_sync(1, nth);
+        // ---- backward block fold: x_b of every segment
+        const double xl = vals[j * W + lane];  // boundary t - 1 (0 for t = 0)
+        if (first_seg) {
+            double xb = vals[(j + 1) * W + lane];  // boundary t (0 for t = p)
+            for (int q = S - 1; q >= 0; --q) {
+                const int id = (j * S + q) * W + lane;
+                const SegCoef sc = segc[j * S + q];
+                const double A = sx[id];
+                sr[id] = xb;
+                xb = fma(sc.nu, xb, fma(xl, sc.k2, A));
+            }
+        }
+        bar_sync(1, nth);
+        stamp(k, 5);
+        // ---- back substitution from the exact carries, X streamed out
+        const int64_t kk = unit(k) * W + lane;
+        const T D = T(sd[tid]), xlt = T(xl);
+        T xn = T(sr[tid]);
+        if (kk < g.N) {
+            T* xp = X + int64_t(sgd.a) * g.ldx + kk;
+            if (len == kSegLen)
+                bwd<T, kSegLen>(co, a, kSegLen, dr, D, xlt, xn, xp, g.ldx);
+            else
+                bwd<T, kSegMax>(co, a, len, dr, D, xlt, xn, xp, g.ldx);
+        }
+        stamp(k, 6);
+    }
+    cluster.sync();  // no CTA leaves while a peer may still push into it
+}
+
+// ---------------------------------------------------------------- host side
+struct CChoice {
+    int W = 0, G = 0, C = 0, nslab = 1;
+    size_t smem = 0;
+};
+
+template <typename T, int W, int NSLAB>
+CChoice choose_t(const psw_plan* pl) {
+    CChoice ch;
+    if (!pl->uniform || pl->world != 1 || !pl->d_ffwd || !pl->d_cmat || pl->nseg <= 0) return ch;
+    const int P = int(pl->P), m = int(pl->m), S = pl->nseg;
+    if (S * kSegLen < m - 1 || S * kSegLen > m + kSegLen || m % 32) return ch;
+    static const int force_g = [] {
+        const char* e = std::getenv("PSW_CLUSTER_G");  // tuning override
+        return e ? std::atoi(e) : 0;
+    }();
+    for (int G = P; G >= 1; --G) {  // fewest CTAs per tile first
+        if (P % G) continue;
+        const int C = P / G;
+        if (C > kMaxC) break;
+        if (force_g > 0 && G != force_g) continue;
+        const int nth = G * S * W;
+        if (nth > kMaxThreads / NSLAB || nth % 32) continue;
+        const size_t smem = CLayout<T, W, NSLAB>(G, m, S, P, nth).total;
+        if (smem > kSmemMax) continue;
+        ch.nslab = NSLAB;
+        ch.W = W;
+        ch.G = G;
+        ch.C = C;
+        ch.smem = smem;
+        return ch;
+    }
+    return ch;
+}
+
+// One 128-byte slab by default. PSW_CLUSTER_SLABS=2: two 64-byte slabs
+// (the next unit streams in during the whole current one; measured slower
+// on C1, 129 vs 89 us: the per-unit time is set by the scan / exchange /
+// back-substitution latency chain, not by the slab's arrival).
+CChoice choose(const psw_plan* pl) {
+    static const int nslab = [] {
+        const char* e = std::getenv("PSW_CLUSTER_SLABS");
+        return e && std::atoi(e) == 2 ? 2 : 1;
+    }();
+    if (nslab == 2) {
+        CChoice ch = pl->dtype == PSW_F64 ? choose_t<double, 8, 2>(pl) : choose_t<float, 16, 2>(pl);
+        if (ch.G) return ch;
+    }
+    return pl->dtype == PSW_F64 ? choose_t<double, 16, 1>(pl) : choose_t<float, 32, 1>(pl);
+}
+
+int box_height(int m) {
+    for (int h = kMaxBox; h >= 32; h /= 2)
+        if (m % h == 0) return h;
+    return 32;
+}
+
+bool encode(CUtensorMap* tm, CUtensorMap* tm1, const void* F, int64_t N, int64_t n, int64_t ldf,
+            int es, int W, int H) {
+    auto enc = tensor_map_encoder();
+    if (!enc) {
+        set_error(PSW_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+        return false;
+    }
+    const cuuint64_t dims[2] = {cuuint64_t(N), cuuint64_t(n)};
+    const cuuint64_t strides[1] = {cuuint64_t(ldf) * cuuint64_t(es)};
+    const cuuint32_t box[2] = {cuuint32_t(W), cuuint32_t(H)};
+    const cuuint32_t box1[2] = {cuuint32_t(W), 1};
+    const cuuint32_t estr[2] = {1, 1};
+    const auto dt = es == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    CUresult r = enc(tm, dt, 2, const_cast<void*>(F), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS)
+        r = enc(tm1, dt, 2, const_cast<void*>(F), dims, strides, box1, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error(PSW_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+        return false;
+    }
+    return true;
+}
+
+template <typename T, int W, int NSLAB>
+int launch(const psw_plan* pl, const CChoice& ch, const void* F, int64_t ldf, void* X, int64_t ldx,
+           int64_t N, cudaStream_t s, void** ev, int nev) {
+    CUtensorMap tm, tm1;
+    const int H = box_height(int(pl->m));
+    if (!encode(&tm, &tm1, F, N, pl->n, ldf, int(sizeof(T)), W, H)) return PSW_CUDA_ERROR;
+    CGeom g;
+    g.n = int(pl->n);
+    g.P = int(pl->P);
+    g.p = int(pl->p);
+    g.m = int(pl->m);
+    g.G = ch.G;
+    g.C = ch.C;
+    g.S = pl->nseg;
+    g.H = H;
+    g.trace = std::getenv("PSW_CLUSTER_TRACE") ? 1 : 0;
+    g.stagger = [] {
+        const char* e = std::getenv("PSW_CLUSTER_STAGGER");  // ns
+        return e ? std::atoi(e) : 0;
+    }();
+    g.N = N;
+    g.ldx = ldx;
+    g.ntiles = (N + W - 1) / W;
+    auto kern = cluster_kernel<T, W, NSLAB>;
+    PSW_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ch.smem)));
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(unsigned(ch.G * g.S * W), 1, 1);
+    cfg.dynamicSmemBytes = ch.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(ch.C);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    static std::mutex mu;
+    static std::vector<std::pair<std::array<int64_t, 5>, int>> cache;
+    const std::array<int64_t, 5> key = {int64_t(sizeof(T)) + 16 * NSLAB, ch.G, ch.C, int64_t(ch.smem), pl->device};
+    int maxc = 0;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (auto& kv : cache)
+            if (kv.first == key) maxc = kv.second;
+        if (maxc == 0) {
+            cfg.gridDim = dim3(unsigned(ch.C), 1, 1);
+            PSW_CUDA_TRY(cudaOccupancyMaxActiveClusters(&maxc, kern, &cfg));
+            if (maxc < 1) maxc = 1;
+            cache.push_back({key, maxc});
+        }
+    }
+    int64_t ncl = std::min<int64_t>((g.ntiles + NSLAB - 1) / NSLAB, maxc);
+    if (const char* e = std::getenv("PSW_CLUSTER_CLUSTERS"))  // tuning override
+        ncl = std::max<int64_t>(1, std::min<int64_t>(ncl, std::atoll(e)));
+    cfg.gridDim = dim3(unsigned(ncl * ch.C), 1, 1);
+    if (std::getenv("PSW_CLUSTER_VERBOSE"))
+        std::fprintf(stderr, "cluster: W=%d slabs=%d G=%d C=%d S=%d threads=%d smem=%zu max_clusters=%d clusters=%lld\n",
+                     W, NSLAB, ch.G, ch.C, g.S, ch.G * g.S * W, ch.smem, maxc, (long long)ncl);
+    mark(ev, nev, 0, s);
+    PSW_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tm, tm1, static_cast<T*>(X), g,
+                                    static_cast<const FusedFwd<T>*>(pl->d_ffwd),
+                                    static_cast<const FusedBwd<T>*>(pl->d_fbwd), pl->d_seg,
+                                    pl->d_segdesc, pl->d_cmat));
+    mark(ev, nev, 1, s);
+    note_launches(1);
+    if (g.trace) {
+        std::vector<unsigned long long> tr(1024 * kTraceSlots);
+        cudaStreamSynchronize(s);
+        cudaMemcpyFromSymbol(tr.data(), g_ctrace, sizeof(unsigned long long) * tr.size());
+        const char* names[] = {"slab wait", "forward+B1", "scan+push", "exchange wait",
+                               "combine+B2+fold+B3", "backward", "  (scan)", "  (push)"};
+        const int nb = int(std::min<int64_t>(1024, ncl * ch.C));
+        for (int ph = 0; ph < 8; ++ph) {
+            // phases: slots 0-1-2-(7)-3-4-5-6; ph 6 = scan (2 -> 7), ph 7 = push (7 -> 3)
+            const int a0 = ph == 6 ? 2 : ph == 7 ? 7 : ph, a1 = ph == 6 ? 7 : ph == 7 ? 3 : ph + 1;
+            std::vector<long long> v;
+            for (int b = 0; b < nb; ++b)
+                v.push_back((long long)(tr[b * kTraceSlots + a1] - tr[b * kTraceSlots + a0]));
+            std::sort(v.begin(), v.end());
+            std::fprintf(stderr, "cluster trace %-22s median %7lld  p90 %7lld cycles\n", names[ph],
+                         v[v.size() / 2], v[v.size() * 9 / 10]);
+        }
+    }
+    return PSW_OK;
+}
+
+}  // namespace
+
+bool cluster_supported(const psw_plan* pl, int layout, int64_t N, const void* F, int64_t ldf) {
+    if (layout != PSW_LAYOUT_R || N < 1 || N > (int64_t{1} << 31)) return false;
+    const int es = pl->dtype == PSW_F64 ? 8 : 4;
+    if ((reinterpret_cast<uintptr_t>(F) & 15) || ((size_t(ldf) * es) & 15)) return false;
+    return choose(pl).G > 0;
+}
+
+int solve_cluster(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_t ldx, int64_t N,
+                  int layout, cudaStream_t s, void** ev, int nev) {
+    if (!cluster_supported(pl, layout, N, F, ldf)) {
+        set_error(PSW_NOT_SUPPORTED,
+                  "cluster path needs layout R, a uniform partition whose blocks fit a "
+                  "cluster, and 16-byte aligned F / row pitch");
+        return PSW_NOT_SUPPORTED;
+    }
+    const CChoice ch = choose(pl);
+    if (ch.nslab == 2)
+        return pl->dtype == PSW_F64 ? launch<double, 8, 2>(pl, ch, F, ldf, X, ldx, N, s, ev, nev)
+                                    : launch<float, 16, 2>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
+    return pl->dtype == PSW_F64 ? launch<double, 16, 1>(pl, ch, F, ldf, X, ldx, N, s, ev, nev)
+                                : launch<float, 32, 1>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
+}
+
+}  // namespace psw

@@ -157,6 +157,9 @@ bool tile_supported(const psw_plan* plan, int layout, int64_t N);
 bool chunked_supported(const psw_plan* plan, int layout, int64_t N);
 int solve_chunked(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
                   int64_t N, int layout, cudaStream_t s, void** events, int nevents);
+bool cluster_supported(const psw_plan* plan, int layout, int64_t N, const void* F, int64_t ldf);
+int solve_cluster(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
+                  int64_t N, int layout, cudaStream_t s, void** events, int nevents);
 bool resweep_supported(const psw_plan* plan, int layout, int64_t N);
 int solve_resweep(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
                   int64_t N, int layout, cudaStream_t s, void** events, int nevents);
