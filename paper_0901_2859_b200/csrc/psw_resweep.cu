@@ -1,6 +1,6 @@
 // RESWEEP solve path: F is read twice and X written once (3 s bytes per
 // unknown instead of the STAGED path's 4 s); nothing of size n x N besides F
-// and X touches HBM. Any partition; layout R.
+// and X touches HBM. Any partition; both layouts.
 //
 // Every block is cut into segments of kSegLen rows (the last one of a block
 // takes the rest, build_fused_tables). In the affine form of the unit-row
@@ -289,9 +289,132 @@ __global__ void __launch_bounds__(kThreads, 4) rs_solve_kernel(
     }
 }
 
+// ------------------------------------------------------------ layout S
+// F[k * ldf + i]: every RHS is contiguous. One warp per (32 RHS, segment):
+// the segment's rows of its 32 RHS are loaded coalesced (cp.async, 256
+// contiguous bytes per instruction) into a [rhs][row] shared tile with an
+// odd row pitch (conflict-free per-lane sweeps), lane r sweeps RHS r. Four
+// warps of a CTA share one segment (its coefficient rows are staged once).
+constexpr int kSWarps = 4;
+constexpr int kSPitch = kSegMax;  // 33: odd pitch, conflict-free column access
+
+template <typename T>
+__device__ __forceinline__ void s_tile_load(T (*tile)[kSPitch], const T* src, int64_t ld, int len,
+                                            int nk, int lane) {
+    // rows 0..31 by lane, row 32 (a 33-row segment) by lane = rhs
+#pragma unroll 4
+    for (int j = 0; j < 32; ++j)
+        if (j < nk && lane < len) {
+            const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&tile[j][lane]));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst),
+                         "l"(src + int64_t(j) * ld + lane), "n"(sizeof(T))
+                         : "memory");
+        }
+    if (len > 32 && lane < nk) {
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&tile[lane][32]));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst),
+                     "l"(src + int64_t(lane) * ld + 32), "n"(sizeof(T))
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kSWarps * 32) rs_part_s_kernel(
+    const T* __restrict__ F, int64_t ldf, int64_t N, const SegDesc* __restrict__ desc,
+    const FusedFwd<T>* __restrict__ ff, Scratch<T> sc) {
+    __shared__ T tiles[kSWarps][32][kSPitch];
+    __shared__ FusedFwd<T> cs[kSegMax];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s = blockIdx.y;
+    const int64_t k0 = (int64_t(blockIdx.x) * kSWarps + warp) * 32;
+    const int nk = k0 < N ? int(N - k0 < 32 ? N - k0 : 32) : 0;
+    const SegDesc sd = desc[s];
+    const int a = sd.a, len = sd.b - sd.a;
+    if (nk > 0) s_tile_load(tiles[warp], F + k0 * ldf + a, ldf, len, nk, lane);
+    for (int i = threadIdx.x; i < len; i += kSWarps * 32) cs[i] = ff[a + i];
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    if (lane >= nk) return;
+    const T* col = tiles[warp][lane];
+    T d = T(0), lx = T(0);
+    double br = 0.0, bl = 0.0;
+#pragma unroll
+    for (int r = 0; r < kSegMax; ++r) {
+        if (r < len) {
+            const FusedFwd<T> c = cs[r];
+            const T f = col[r];
+            d = fma(c.ma, d, f * c.rp);
+            br = fma(double(f), double(c.gr), br);
+            bl = fma(double(f), double(c.gl), bl);
+            lx = fma(c.lam, d, lx);
+        }
+    }
+    const int64_t o = int64_t(s) * sc.ld + k0 + lane;
+    sc.pd[o] = d;
+    sc.px[o] = lx;
+    sc.pr[o] = br;
+    sc.pl[o] = bl;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kSWarps * 32) rs_solve_s_kernel(
+    const T* F, int64_t ldf, T* X, int64_t ldx, int64_t N, const SegDesc* __restrict__ desc,
+    const FwdCoef<T>* __restrict__ cf, const BwdCoef<T>* __restrict__ cb, Scratch<T> sc,
+    const double* __restrict__ V, int NS) {
+    __shared__ T tiles[kSWarps][32][kSPitch];
+    __shared__ FwdCoef<T> csf[kSegMax];
+    __shared__ BwdCoef<T> csb[kSegMax];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s = NS - 1 - int(blockIdx.y);  // reverse of K1's order (L2 reuse)
+    const int64_t k0 = (int64_t(blockIdx.x) * kSWarps + warp) * 32;
+    const int nk = k0 < N ? int(N - k0 < 32 ? N - k0 : 32) : 0;
+    const SegDesc sd = desc[s];
+    const int a = sd.a, len = sd.b - sd.a, t = sd.t;
+    if (nk > 0) s_tile_load(tiles[warp], F + k0 * ldf + a, ldf, len, nk, lane);
+    for (int i = threadIdx.x; i < len; i += kSWarps * 32) {
+        csf[i] = cf[a + i];
+        csb[i] = cb[a + i];
+    }
+    T d = T(0), xn = T(0), xl = T(0);
+    if (lane < nk) {  // the carries' loads overlap the tile's
+        const int64_t o = int64_t(s) * sc.ld + k0 + lane;
+        d = sc.pd[o];
+        xn = T(sc.pr[o]);
+        if (t > 0) xl = T(V[int64_t(t - 1) * sc.ld + k0 + lane]);
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    if (nk == 0) return;
+    T* col = tiles[warp][lane];
+    if (lane < nk) {
+#pragma unroll
+        for (int r = 0; r < kSegMax; ++r) {
+            if (r < len) {
+                d = fma(csf[r].ma, d, col[r] * csf[r].rp);
+                col[r] = d;
+            }
+        }
+#pragma unroll
+        for (int r = kSegMax - 1; r >= 0; --r) {
+            if (r < len) {
+                xn = fma(csb[r].al, xn, fma(xl, csb[r].w, col[r]));
+                col[r] = xn;
+            }
+        }
+    }
+    __syncwarp();
+    // coalesced write-back: RHS j's rows by lane (row 32 by lane = rhs)
+    T* dst = X + k0 * ldx + a;
+#pragma unroll 4
+    for (int j = 0; j < 32; ++j)
+        if (j < nk && lane < len) __stcs(dst + int64_t(j) * ldx + lane, tiles[warp][j][lane]);
+    if (len > 32 && lane < nk) __stcs(dst + int64_t(lane) * ldx + 32, tiles[warp][lane][32]);
+}
+
 template <typename T>
 int launch_resweep(const psw_plan* pl, const void* Fv, int64_t ldf, void* Xv, int64_t ldx,
-                   int64_t N, cudaStream_t s, void** ev, int nev) {
+                   int64_t N, int layout, cudaStream_t s, void** ev, int nev) {
     const T* F = static_cast<const T*>(Fv);
     T* X = static_cast<T*>(Xv);
     const int P = int(pl->P), p = int(pl->p);
@@ -314,9 +437,14 @@ int launch_resweep(const psw_plan* pl, const void* Fv, int64_t ldf, void* Xv, in
     sc.px = sc.pd + sn;
     const unsigned gx = unsigned((N + kThreads - 1) / kThreads);
     const auto* desc = pl->d_segdesc;
+    const unsigned gs = unsigned((N + kSWarps * 32 - 1) / (kSWarps * 32));
     mark(ev, nev, 0, s);
-    rs_part_kernel<T><<<dim3(gx, unsigned(NS)), kThreads, 0, s>>>(
-        F, ldf, N, desc, static_cast<const FusedFwd<T>*>(pl->d_ffwd), sc);
+    if (layout == PSW_LAYOUT_S)
+        rs_part_s_kernel<T><<<dim3(gs, unsigned(NS)), kSWarps * 32, 0, s>>>(
+            F, ldf, N, desc, static_cast<const FusedFwd<T>*>(pl->d_ffwd), sc);
+    else
+        rs_part_kernel<T><<<dim3(gx, unsigned(NS)), kThreads, 0, s>>>(
+            F, ldf, N, desc, static_cast<const FusedFwd<T>*>(pl->d_ffwd), sc);
     mark(ev, nev, 1, s);
     int64_t launches = 1;
     // fused fold + combination + carries when there are enough 32-RHS CTAs
@@ -353,9 +481,14 @@ int launch_resweep(const psw_plan* pl, const void* Fv, int64_t ldf, void* Xv, in
         ++launches;
     }
     mark(ev, nev, 2, s);
-    rs_solve_kernel<T><<<dim3(gx, unsigned(NS)), kThreads, 0, s>>>(
-        F, ldf, X, ldx, N, desc, static_cast<const FwdCoef<T>*>(pl->d_fwd),
-        static_cast<const BwdCoef<T>*>(pl->d_bwd), sc, V, NS);
+    if (layout == PSW_LAYOUT_S)
+        rs_solve_s_kernel<T><<<dim3(gs, unsigned(NS)), kSWarps * 32, 0, s>>>(
+            F, ldf, X, ldx, N, desc, static_cast<const FwdCoef<T>*>(pl->d_fwd),
+            static_cast<const BwdCoef<T>*>(pl->d_bwd), sc, V, NS);
+    else
+        rs_solve_kernel<T><<<dim3(gx, unsigned(NS)), kThreads, 0, s>>>(
+            F, ldf, X, ldx, N, desc, static_cast<const FwdCoef<T>*>(pl->d_fwd),
+            static_cast<const BwdCoef<T>*>(pl->d_bwd), sc, V, NS);
     ++launches;
     mark(ev, nev, 3, s);
     cudaError_t e = cudaGetLastError();
@@ -368,16 +501,15 @@ int launch_resweep(const psw_plan* pl, const void* Fv, int64_t ldf, void* Xv, in
 }  // namespace
 
 bool resweep_supported(const psw_plan* pl, int layout, int64_t N) {
-    if (pl->world != 1 || layout != PSW_LAYOUT_R || N < 1) return false;
+    if (pl->world != 1 || (layout != PSW_LAYOUT_R && layout != PSW_LAYOUT_S) || N < 1) return false;
     if (!pl->d_segdesc || !pl->d_ffwd || pl->seg_off.empty()) return false;
     return pl->seg_off.back() < 65536 && pl->P < 65536;  // grid.y
 }
 
 int solve_resweep(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_t ldx, int64_t N,
                   int layout, cudaStream_t s, void** ev, int nev) {
-    (void)layout;
-    return pl->dtype == PSW_F64 ? launch_resweep<double>(pl, F, ldf, X, ldx, N, s, ev, nev)
-                                : launch_resweep<float>(pl, F, ldf, X, ldx, N, s, ev, nev);
+    return pl->dtype == PSW_F64 ? launch_resweep<double>(pl, F, ldf, X, ldx, N, layout, s, ev, nev)
+                                : launch_resweep<float>(pl, F, ldf, X, ldx, N, layout, s, ev, nev);
 }
 
 }  // namespace psw

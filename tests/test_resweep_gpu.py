@@ -12,41 +12,37 @@ from test_parity_gpu import FP32_TOL, FP64_TOL, gpu_solve, plan_for
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("layout", [0, 1])
 @pytest.mark.parametrize("name", golden_cases())
-def test_resweep_golden(psw, cuda, name):
+def test_resweep_golden(psw, cuda, name, layout):
     g = load_golden(name)
     plan = plan_for(psw, g)
-    ref = gpu_solve(psw, cuda, plan, g["F"], 0, path=psw.PATH_STAGED)
-    X = gpu_solve(psw, cuda, plan, g["F"], 0, path=psw.PATH_RESWEEP)
+    ref = gpu_solve(psw, cuda, plan, g["F"], layout, path=psw.PATH_STAGED)
+    X = gpu_solve(psw, cuda, plan, g["F"], layout, path=psw.PATH_RESWEEP)
     assert rel_l2(X, ref) <= 1e-12, (name, rel_l2(X, ref))
     assert rel_l2(X, g["X"]) <= FP64_TOL, (name, rel_l2(X, g["X"]))
 
 
+@pytest.mark.parametrize("layout", [0, 1])
 @pytest.mark.parametrize("N", [1, 5, 127, 129, 1000])
-def test_resweep_ragged(psw, cuda, N):
+def test_resweep_ragged(psw, cuda, N, layout):
     g = load_golden("c1_n4096_P16")
     plan = plan_for(psw, g)
     F = np.random.default_rng(N).standard_normal((N, 4096))
-    ref = gpu_solve(psw, cuda, plan, F, 0, path=psw.PATH_STAGED)
-    X = gpu_solve(psw, cuda, plan, F, 0, path=psw.PATH_RESWEEP)
-    X2 = gpu_solve(psw, cuda, plan, F, 0, path=psw.PATH_RESWEEP, inplace=False, pad=3)
+    ref = gpu_solve(psw, cuda, plan, F, layout, path=psw.PATH_STAGED)
+    X = gpu_solve(psw, cuda, plan, F, layout, path=psw.PATH_RESWEEP)
+    X2 = gpu_solve(psw, cuda, plan, F, layout, path=psw.PATH_RESWEEP, inplace=False, pad=3)
     assert rel_l2(X, ref) <= 1e-13
     assert np.array_equal(X, X2)
 
 
+@pytest.mark.parametrize("layout", [0, 1])
 @pytest.mark.parametrize("name", ["c2_n8192_P8", "c2_n8192_P64", "c2_n8192_P512"])
-def test_resweep_fp32(psw, cuda, name):
+def test_resweep_fp32(psw, cuda, name, layout):
     g = load_golden(name)
     plan = plan_for(psw, g, dtype=psw.F32)
-    X = gpu_solve(psw, cuda, plan, g["F"], 0, path=psw.PATH_RESWEEP)
+    X = gpu_solve(psw, cuda, plan, g["F"], layout, path=psw.PATH_RESWEEP)
     assert rel_l2(X, g["X"]) <= FP32_TOL
-
-
-def test_resweep_not_layout_s(psw, cuda):
-    g = load_golden("c0_n1024_P4")
-    plan = plan_for(psw, g)
-    with pytest.raises(psw.NotSupported):
-        gpu_solve(psw, cuda, plan, g["F"], 1, path=psw.PATH_RESWEEP)
 
 
 def test_resweep_config_C1(psw, cuda):
