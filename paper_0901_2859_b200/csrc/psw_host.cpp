@@ -89,9 +89,19 @@ extern "C" int psw_solve_host(const psw_plan* plan, const void* F, int64_t ldf, 
     PSW_CUDA_TRY(cudaSetDevice(plan->device));
     const int64_t n = plan->n;
     const size_t es = plan->dtype == PSW_F64 ? 8 : 4;
-    int64_t c = std::max<int64_t>(1, int64_t(chunk_bytes() / (size_t(n) * es)));
+    // >= 16 MB chunks, up to 1/16 of the batch (<= 1 GB) for large batches so
+    // that every chunk's solve is itself a full-GPU launch
+    const size_t total = size_t(nrhs) * size_t(n) * es;
+    const size_t target = std::max(chunk_bytes(), std::min(size_t(1) << 30, total / 16));
+    int64_t c = std::max<int64_t>(1, int64_t(target / (size_t(n) * es)));
     c = std::min<int64_t>(c, std::max<int64_t>(1, (nrhs + 7) / 8));
-    if (layout == PSW_LAYOUT_R && c >= 32) c = c / 32 * 32;
+    if (layout == PSW_LAYOUT_R) {
+        // a layout-R chunk is a pitched copy of c * es bytes per row: keep
+        // rows >= 2 KB (narrower DMA rows crawl: 16-256 B rows ran at 2-16
+        // GB/s on the 2^20-row and fp32 configs), even if chunks get large
+        c = std::max<int64_t>(c, int64_t(2048 / es));
+        if (c >= 32) c = c / 32 * 32;
+    }
     c = std::min(c, nrhs);
     const int64_t nchunks = (nrhs + c - 1) / c;
     const size_t slot_bytes = (size_t(c) * size_t(n) * es + 255) & ~size_t(255);

@@ -844,8 +844,10 @@ int psw_solve_ex(const psw_plan* plan, const void* F, int64_t ldf, void* X, int6
         psw::set_error(PSW_NOT_SUPPORTED, "fused path does not support this plan/shape");
         rc = PSW_NOT_SUPPORTED;
     } else if (path == PSW_PATH_AUTO && !want_intermediates &&
+               nrhs * (plan->dtype == PSW_F64 ? 8 : 4) >= 128 * 128 &&
                psw::cluster_supported(plan, layout, nrhs, F, ldf)) {
-        // measured C1: CLUSTER 88.7 us, FUSED 93.2 us (profiles/r01_*)
+        // >= 128 RHS tiles of 128 B: measured C1 (256 tiles) CLUSTER 88.8 us vs
+        // FUSED 93.2 us; C0 (16 tiles) CLUSTER 22.9 us vs FUSED 14.2 us
         t_last_path = PSW_PATH_CLUSTER;
         rc = psw::solve_cluster(plan, F, ldf, X, ldx, nrhs, layout, s,
                                 opts ? opts->events : nullptr, opts ? opts->nevents : 0);
