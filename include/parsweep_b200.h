@@ -135,6 +135,16 @@ int psw_plan_create_ex(psw_plan** out, int64_t n, const double* sub, const doubl
 int psw_plan_destroy(psw_plan* plan);
 int psw_plan_info(const psw_plan* plan, psw_plan_info_t* info);
 
+/* ---- multi-matrix batched solve ---------------------------------------- */
+/* Replaces the per-harmonic loop of fourier_solve (poisson/fourier.hpp:157-164)
+ * over FourierWorkspace::solve_harmonic (:75-86): column k of the layout-R
+ * series F (device, k < nplans, row pitch ldf) is solved with plans[k] into
+ * column k of X, all columns in one pass (the STAGED kernels with per-column
+ * plan tables; betas and boundary values bitwise the reference's). The plans
+ * must share the order, the partition, the dtype and the device. */
+int psw_solve_multi(const psw_plan* const* plans, int64_t nplans, const void* F, int64_t ldf,
+                    void* X, int64_t ldx, void* stream);
+
 /* ---- batched solve ---------------------------------------------------- */
 /* Replaces the per-RHS loop of solve_batch (dichotomy/batch.hpp:67-73) over
  * solve_with_preliminary_into (batch.hpp:20-51): solves all `nrhs` systems

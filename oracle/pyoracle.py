@@ -252,6 +252,8 @@ class Reference(_Base):
         L.ref_adi_solve.argtypes = [C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int64,
                                     C.c_int64, C.c_double, _d, _d, _d, _d, _i64]
         L.ref_model_problem.argtypes = [C.c_int64, C.c_int64, _d, _d]
+        L.ref_fourier_solve.argtypes = [C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int64,
+                                        _d, _d, _i64, _i64]
 
     # ---- poisson/adi.hpp (the ADI consumer) -------------
     def adi_iteration_bound(self, n: int, eps: float) -> int:
@@ -276,6 +278,15 @@ class Reference(_Base):
                                     _dp(ex) if ex is not None else None, _dp(u), _ip(its))
         self._check(rc)
         return u, int(its[0])
+
+    # ---- poisson/fourier.hpp (the Fourier consumer) -----
+    def fourier_solve(self, n1, n2, h1, h2, pes, f):
+        f = _f64(f)
+        u = np.empty_like(f)
+        bnd = np.zeros(max(n1, 1), np.int64)
+        p = np.zeros(1, np.int64)
+        self._check(self.lib.ref_fourier_solve(n1, n2, h1, h2, pes, _dp(f), _dp(u), _ip(bnd), _ip(p)))
+        return u, bnd[: int(p[0])]
 
     def model_problem(self, n1, n2):
         f = np.zeros((n1 + 1, n2 + 1))

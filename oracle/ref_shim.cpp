@@ -26,6 +26,7 @@
 #include "parsweep/runtime/decompose.hpp"
 #include "parsweep/runtime/run.hpp"
 #include "parsweep/poisson/adi.hpp"
+#include "parsweep/poisson/fourier.hpp"
 #include "parsweep/poisson/model_problem.hpp"
 
 namespace {
@@ -311,6 +312,24 @@ void ref_model_problem(int64_t n1, int64_t n2, double* f, double* exact) {
                                                      static_cast<std::size_t>(n2));
     std::memcpy(f, fg.values.data(), sizeof(double) * fg.values.size());
     std::memcpy(exact, eg.values.data(), sizeof(double) * eg.values.size());
+}
+
+// ---- Fourier consumer (poisson/fourier.hpp), §8(f) rank 3 ---------------
+// fourier_solve(f, FourierWorkspace(n1, n2, h1, h2, pes)) -> u; also the
+// workspace's partition boundaries (p of them, *p_out)
+int ref_fourier_solve(int64_t n1, int64_t n2, double h1, double h2, int64_t pes, const double* f,
+                      double* u, int64_t* bnd_out, int64_t* p_out) {
+    return guarded([&] {
+        parsweep::poisson::FourierWorkspace ws(static_cast<std::size_t>(n1),
+                                               static_cast<std::size_t>(n2), h1, h2,
+                                               static_cast<std::size_t>(pes));
+        auto fg = make_grid(n1, n2, h1, h2, f);
+        auto ug = parsweep::poisson::fourier_solve(fg, ws);
+        std::memcpy(u, ug.values.data(), sizeof(double) * ug.values.size());
+        const auto& b = ws.partition().boundaries;
+        *p_out = static_cast<int64_t>(b.size());
+        for (std::size_t i = 0; i < b.size(); ++i) bnd_out[i] = static_cast<int64_t>(b[i]);
+    }, nullptr);
 }
 
 int ref_hardware_concurrency(void) { return static_cast<int>(std::thread::hardware_concurrency()); }

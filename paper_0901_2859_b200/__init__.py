@@ -31,7 +31,7 @@ import numpy as np
 
 __all__ = [
     "TridiagMatrix", "Partition", "Decomposition", "decompose", "compute_preliminary", "Plan",
-    "solve_batch", "SolverError", "PivotBreakdown", "TooManyPEs", "NotSupported", "NotSymmetrizable", "OracleFallbackRequired", "CudaError",
+    "solve_batch", "solve_multi", "SolverError", "PivotBreakdown", "TooManyPEs", "NotSupported", "NotSymmetrizable", "OracleFallbackRequired", "CudaError",
     "F64", "F32", "LAYOUT_R", "LAYOUT_S", "PATH_AUTO", "PATH_STAGED", "PATH_FUSED", "PATH_PIPE", "PATH_TILE", "PATH_CHUNKED", "PATH_RESWEEP", "PATH_CLUSTER", "last_path", "lib",
     "library_path",
 ]
@@ -120,6 +120,7 @@ def lib() -> C.CDLL:
         L.psw_solve.argtypes = [vp, vp, C.c_int64, vp, C.c_int64, C.c_int64, C.c_int, vp]
         L.psw_solve_ex.argtypes = [vp, vp, C.c_int64, vp, C.c_int64, C.c_int64, C.c_int, vp, vp]
         L.psw_solve_host.argtypes = [vp, vp, C.c_int64, vp, C.c_int64, C.c_int64, C.c_int]
+        L.psw_solve_multi.argtypes = [C.POINTER(vp), C.c_int64, vp, C.c_int64, vp, C.c_int64, vp]
         L.psw_shard_partials_count.argtypes = [vp]
         L.psw_shard_partials_count.restype = C.c_int64
         L.psw_shard_row_offset.argtypes = [vp]
@@ -454,6 +455,15 @@ def solve_batch(A: TridiagMatrix, part: Partition, rhs_series: Sequence[Sequence
     F = np.ascontiguousarray(np.asarray(rhs_series, dtype=dt).reshape(len(rhs_series), A.n()))
     X = plan.solve_host(F, layout=LAYOUT_S)
     return [X[k] for k in range(X.shape[0])]
+
+
+def solve_multi(plans: Sequence["Plan"], F, X, stream=None):
+    """psw_solve_multi: column k of the layout-R CUDA tensor F (n x ld) is
+    solved with plans[k] into column k of X (the per-harmonic loop of
+    poisson/fourier.hpp:157-164 as one pass)."""
+    arr = (C.c_void_p * len(plans))(*[pl._h for pl in plans])
+    _check(lib().psw_solve_multi(arr, len(plans), _ptr(F), F.stride(0), _ptr(X), X.stride(0),
+                                 _stream_ptr(stream)))
 
 
 def fill_uniform(t, seed: int, lo: float, hi: float, offset: int = 0, stream=None):

@@ -1,0 +1,151 @@
+// Multi-matrix batched solve (psw_solve_multi): right-hand side k (column k
+// of a layout-R series) is solved with its own plan, plans[k]. This is the
+// per-harmonic loop of the reference Fourier solver (poisson/fourier.hpp:
+// 157-164 over FourierWorkspace::solve_harmonic, :75-86: one matrix
+// B_l = tri(1, -(2 + d_l), 1) and one right-hand side per harmonic) as one
+// three-kernel pass over all harmonics instead of one solve per harmonic.
+//
+// The kernels are the STAGED path's (psw_staged.cu) with per-RHS plan
+// tables: one thread per (rhs k, block t) for the forward sweep with both
+// beta dot products and the backward sweep, one thread per rhs for the
+// level-order dichotomy with that rhs' Z samples. Every right-hand side
+// therefore gets bitwise the betas, boundary values and solution of a
+// single-plan STAGED solve, i.e. the reference's betas and boundary values.
+// All plans share the partition (the workspace's, fourier.hpp:47-51).
+#include <vector>
+
+#include "psw_device.cuh"
+#include "psw_internal.h"
+
+namespace psw {
+namespace {
+
+constexpr int kThreads = 128;
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) multi_fwd_kernel(
+    const T* F, int64_t ldf, T* X, int64_t ldx, int64_t N, const int32_t* __restrict__ blk,
+    const FwdCoef<T>* const* __restrict__ cfs, double* __restrict__ bl_out,
+    double* __restrict__ br_out, int p) {
+    const int t = blockIdx.y;
+    const int64_t k = int64_t(blockIdx.x) * kThreads + threadIdx.x;
+    if (k >= N) return;
+    const FwdCoef<T>* cf = cfs[k];
+    const int s = blk[2 * t], e = blk[2 * t + 1];
+    T d = T(0);
+    double br = 0.0, bl = 0.0;
+    for (int q = s; q < e; ++q) {
+        const FwdCoef<T> c = cf[q];
+        const T fv = F[int64_t(q) * ldf + k];
+        d = fma(c.ma, d, fv * c.rp);
+        br = madd_rn(br, double(fv), double(c.gr));
+        bl = madd_rn(bl, double(fv), double(c.gl));
+        X[int64_t(q) * ldx + k] = d;
+    }
+    if (t < p) br_out[int64_t(t) * N + k] = br;
+    if (t > 0) bl_out[int64_t(t) * N + k] = bl;
+}
+
+__global__ void __launch_bounds__(kThreads) multi_combine_kernel(
+    const double* __restrict__ bl, const double* __restrict__ br, int64_t N, int p,
+    const CombineItem* __restrict__ items, const double* const* __restrict__ zrs,
+    const double* const* __restrict__ zls, double* __restrict__ V) {
+    const int64_t k = int64_t(blockIdx.x) * kThreads + threadIdx.x;
+    if (k >= N) return;
+    combine_rhs(items, p, bl + k, br + k, N, zrs[k], zls[k], V + k, N);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) multi_bwd_kernel(
+    T* X, int64_t ldx, int64_t N, const int32_t* __restrict__ blk,
+    const BwdCoef<T>* const* __restrict__ cbs, const double* __restrict__ V, int p) {
+    const int t = blockIdx.y;
+    const int64_t k = int64_t(blockIdx.x) * kThreads + threadIdx.x;
+    if (k >= N) return;
+    const BwdCoef<T>* cb = cbs[k];
+    const int s = blk[2 * t], e = blk[2 * t + 1];
+    const T xl = t > 0 ? T(V[int64_t(t - 1) * N + k]) : T(0);
+    T xn = t < p ? T(V[int64_t(t) * N + k]) : T(0);
+    for (int q = e - 1; q >= s; --q) {
+        const BwdCoef<T> c = cb[q];
+        xn = fma(c.al, xn, fma(xl, c.w, X[int64_t(q) * ldx + k]));
+        X[int64_t(q) * ldx + k] = xn;
+    }
+}
+
+template <typename T>
+int launch_multi(const psw_plan* const* plans, int64_t N, const void* Fv, int64_t ldf, void* Xv,
+                 int64_t ldx, cudaStream_t s) {
+    const psw_plan* p0 = plans[0];
+    const int P = int(p0->P), p = int(p0->p);
+    // per-RHS table pointers (device), then betas and boundary values
+    std::vector<const void*> tab(size_t(4) * N);
+    for (int64_t k = 0; k < N; ++k) {
+        tab[k] = plans[k]->d_fwd;
+        tab[N + k] = plans[k]->d_bwd;
+        tab[2 * N + k] = plans[k]->d_zr;
+        tab[3 * N + k] = plans[k]->d_zl;
+    }
+    const size_t tab_b = sizeof(void*) * tab.size();
+    const size_t need = tab_b + sizeof(double) * size_t(N) * (2 * size_t(P) + size_t(p > 0 ? p : 1));
+    void* scratch = nullptr;
+    PSW_CUDA_TRY(cudaMallocAsync(&scratch, need, s));
+    PSW_CUDA_TRY(cudaMemcpyAsync(scratch, tab.data(), tab_b, cudaMemcpyHostToDevice, s));
+    PSW_CUDA_TRY(cudaStreamSynchronize(s));  // the host table goes out of scope
+    auto** dtab = static_cast<const void**>(scratch);
+    double* bl = reinterpret_cast<double*>(static_cast<char*>(scratch) + tab_b);
+    double* br = bl + size_t(P) * N;
+    double* V = br + size_t(P) * N;
+    const dim3 grid(unsigned((N + kThreads - 1) / kThreads), unsigned(P));
+    multi_fwd_kernel<T><<<grid, kThreads, 0, s>>>(
+        static_cast<const T*>(Fv), ldf, static_cast<T*>(Xv), ldx, N, p0->d_blk,
+        reinterpret_cast<const FwdCoef<T>* const*>(dtab), bl, br, p);
+    int64_t launches = 1;
+    if (p > 0) {
+        multi_combine_kernel<<<grid.x, kThreads, 0, s>>>(
+            bl, br, N, p, p0->d_items, reinterpret_cast<const double* const*>(dtab + 2 * N),
+            reinterpret_cast<const double* const*>(dtab + 3 * N), V);
+        ++launches;
+    }
+    multi_bwd_kernel<T><<<grid, kThreads, 0, s>>>(
+        static_cast<T*>(Xv), ldx, N, p0->d_blk, reinterpret_cast<const BwdCoef<T>* const*>(dtab + N),
+        V, p);
+    ++launches;
+    cudaError_t e = cudaGetLastError();
+    cudaFreeAsync(scratch, s);
+    if (e != cudaSuccess) return cuda_fail(e, "multi-plan kernels");
+    note_launches(launches);
+    return PSW_OK;
+}
+
+}  // namespace
+}  // namespace psw
+
+extern "C" int psw_solve_multi(const psw_plan* const* plans, int64_t nplans, const void* F,
+                               int64_t ldf, void* X, int64_t ldx, void* stream) {
+    psw::clear_error();
+    psw::reset_launches();
+    if (nplans < 0 || (nplans > 0 && (!plans || !F || !X)) || ldf < nplans || ldx < nplans) {
+        psw::set_error(PSW_INVALID_ARGUMENT, "invalid arguments to psw_solve_multi");
+        return PSW_INVALID_ARGUMENT;
+    }
+    if (nplans == 0) return PSW_OK;
+    const psw_plan* p0 = plans[0];
+    for (int64_t k = 0; k < nplans; ++k) {
+        const psw_plan* q = plans[k];
+        if (!q || q->world != 1 || q->n != p0->n || q->P != p0->P || q->dtype != p0->dtype ||
+            q->device != p0->device || q->bnd != p0->bnd) {
+            psw::set_error(PSW_INVALID_ARGUMENT,
+                           "psw_solve_multi: plans must share order, partition, dtype and device");
+            return PSW_INVALID_ARGUMENT;
+        }
+    }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != p0->device) PSW_CUDA_TRY(cudaSetDevice(p0->device));
+    auto s = static_cast<cudaStream_t>(stream);
+    const int rc = p0->dtype == PSW_F64 ? psw::launch_multi<double>(plans, nplans, F, ldf, X, ldx, s)
+                                        : psw::launch_multi<float>(plans, nplans, F, ldf, X, ldx, s);
+    if (prev != p0->device) cudaSetDevice(prev);
+    return rc;
+}

@@ -1,0 +1,107 @@
+"""Fourier (variable-separation) Poisson solver on the GPU: the second
+consumer of the batched dichotomy solve (reference
+poisson/fourier.hpp, poisson/dst.hpp).
+
+Mirrors the reference API: ``harmonic_system``, ``FourierWorkspace`` (the
+once-per-mesh phase: the direction-1 partition and, per direction-2 harmonic
+l, the matrix B_l = tri(1, -(2 + d_l), 1) with its device-resident plan) and
+``fourier_solve``. Fields are CUDA fp64 tensors in the reference's Grid2D
+layout ((n1+1) x (n2+1) nodes, row-major, j contiguous, zero Dirichlet
+boundary), as in the ADI driver (adi.py).
+
+Per Poisson right-hand side:
+  1. the DST-I of every interior row along direction 2 (dst.hpp:13-20:
+     out_l = sum_j in_j sin(pi j l / N)), scaled by 2/N2 (fourier.hpp:130) —
+     one batched fp64 FFT of the odd extension, the reference's own
+     construction for power-of-two N (dst.hpp:107-118) and used for every N
+     here;
+  2. rhs = -h1^2 coeff (fourier.hpp:159) and ONE multi-matrix solve of all
+     harmonics (psw_solve_multi: column l of the coefficient grid with the
+     plan of B_l; the reference's per-harmonic solve_harmonic loop,
+     fourier.hpp:157-164);
+  3. the inverse DST-I of every row (fourier.hpp:167-186).
+The transforms round differently from the reference's radix-2 FFT (a few ulp
+of the field); the solves are the dichotomy path of the reference.
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import F64, Plan, TridiagMatrix, solve_multi
+from .adi import _make_partition
+
+
+class HarmonicSystem:
+    """fourier.hpp:16-33"""
+
+    def __init__(self, l: int, d_l: float, matrix: TridiagMatrix):
+        self.l, self.d_l, self.matrix = l, d_l, matrix
+
+
+def harmonic_system(n1: int, n2: int, h1: float, h2: float, l: int) -> HarmonicSystem:
+    """fourier.hpp:25-33: B_l = T - d_l I, d_l = 4 (h1/h2)^2 sin^2(pi l / (2 N2))."""
+    s = math.sin(math.pi * float(l) / (2.0 * n2))
+    d_l = 4.0 * (h1 * h1) / (h2 * h2) * s * s
+    return HarmonicSystem(l, d_l, TridiagMatrix.constant(n1 - 1, 1.0, -(2.0 + d_l), 1.0))
+
+
+def dst_raw(x: torch.Tensor) -> torch.Tensor:
+    """out[..., l-1] = sum_{j=1}^{N-1} x[..., j-1] sin(pi j l / N) for rows of
+    length N-1 (dst.hpp:93-118): FFT of the odd extension of length 2N."""
+    m = x.shape[-1]
+    n = m + 1
+    v = torch.zeros(*x.shape[:-1], 2 * n, dtype=torch.float64, device=x.device)
+    v[..., 1:n] = x
+    v[..., n + 1:] = -torch.flip(x, dims=[-1])
+    V = torch.fft.fft(v, dim=-1)
+    return -0.5 * V[..., 1:n].imag
+
+
+class FourierWorkspace:
+    """fourier.hpp:35-105: the direction-1 partition (dichotomy_pes ranges,
+    reduced while order < 2 pes) and one device plan per harmonic
+    l = 1..n2-1 (the reference's cached HarmonicPlan list)."""
+
+    def __init__(self, n1: int, n2: int, h1: float, h2: float, dichotomy_pes: int = 1,
+                 device: int = 0):
+        if n1 < 3 or n2 < 2:
+            raise ValueError("FourierWorkspace: needs n1 >= 3 and n2 >= 2 cells")
+        self.n1, self.n2, self.h1, self.h2 = n1, n2, h1, h2
+        self.device = device
+        order = n1 - 1
+        self.part = _make_partition(order, dichotomy_pes)
+        self.harmonics = [harmonic_system(n1, n2, h1, h2, l) for l in range(1, n2)]
+        self.plans = [Plan(hs.matrix, self.part, dtype=F64, device=device) for hs in self.harmonics]
+
+    def partition(self):
+        return self.part
+
+    def solve_harmonics(self, coeff: torch.Tensor, out: torch.Tensor | None = None, stream=None):
+        """All harmonic systems at once: column l-1 of `coeff` ((n1-1) x (n2-1),
+        row i-1 = direction-1 node i) is the right-hand side of B_l."""
+        if out is None:
+            out = torch.empty_like(coeff)
+        solve_multi(self.plans, coeff, out, stream=stream)
+        return out
+
+
+def fourier_solve(f: torch.Tensor, ws: FourierWorkspace | None = None, h1: float | None = None,
+                  h2: float | None = None) -> torch.Tensor:
+    """fourier.hpp:111-186: Dirichlet Poisson laplace(u) = -f on the mesh of
+    f ((n1+1) x (n2+1) CUDA fp64 tensor). Without a workspace, a single-PE one
+    is built (fourier.hpp:189-193; h1, h2 default to the unit square)."""
+    n1, n2 = f.shape[0] - 1, f.shape[1] - 1
+    if ws is None:
+        ws = FourierWorkspace(n1, n2, h1 if h1 is not None else 1.0 / n1,
+                              h2 if h2 is not None else 1.0 / n2, 1, device=f.device.index or 0)
+    if (ws.n1, ws.n2) != (n1, n2):
+        raise ValueError("fourier_solve: workspace mesh does not match the field")
+    interior = f[1:n1, 1:n2].to(torch.float64)
+    coeff = (2.0 / float(n2)) * dst_raw(interior)          # fourier.hpp:129-149
+    rhs = (-ws.h1 * ws.h1) * coeff                          # fourier.hpp:159
+    sol = ws.solve_harmonics(rhs.contiguous())              # fourier.hpp:157-164
+    u = torch.zeros_like(f, dtype=torch.float64)
+    u[1:n1, 1:n2] = dst_raw(sol)                            # fourier.hpp:167-186
+    return u

@@ -38,9 +38,9 @@ def ref():
 
 
 def golden_cases():
-    """Batched-solve fixtures (the ADI consumer's fixtures are adi_*.npz)."""
+    """Batched-solve fixtures (the consumers' fixtures are adi_*.npz, fourier_*.npz)."""
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
-                  if not os.path.basename(p).startswith("adi_"))
+                  if not os.path.basename(p).startswith(("adi_", "fourier_")))
 
 
 def load_golden(name):

@@ -93,6 +93,25 @@ def adi(ref: Reference, seed: int = 2026):
     print(f"adi_solve_32x32: {its} iterations (cycle {cycle})")
 
 
+def fourier(ref: Reference, seed: int = 2026):
+    """The Fourier consumer (poisson/fourier.hpp): fourier_solve of the model
+    problem (1 and 4 dichotomy PEs) and of a seeded random field on a
+    rectangular mesh."""
+    for n1, n2, pes in ((32, 32, 1), (64, 64, 4), (24, 40, 3)):
+        h1, h2 = 1.0 / n1, 1.0 / n2
+        if n1 == n2:
+            f, _ = ref.model_problem(n1, n2)
+        else:
+            rng = np.random.default_rng(seed + n1 + n2)
+            f = np.zeros((n1 + 1, n2 + 1))
+            f[1:-1, 1:-1] = rng.uniform(-1, 1, (n1 - 1, n2 - 1))
+        u, bnd = ref.fourier_solve(n1, n2, h1, h2, pes, f)
+        name = f"fourier_{n1}x{n2}_pes{pes}"
+        np.savez_compressed(os.path.join(OUT, name + ".npz"), n1=n1, n2=n2, h1=h1, h2=h2, pes=pes,
+                            f=f, u=u, bnd=bnd)
+        print(name, "boundaries", list(bnd))
+
+
 def main():
     build(ref=True)
     ref = Reference()
@@ -103,6 +122,9 @@ def main():
         return
     if len(sys.argv) > 1 and sys.argv[1] == "--adi":
         adi(ref, seed)
+        return
+    if len(sys.argv) > 1 and sys.argv[1] == "--fourier":
+        fourier(ref, seed)
         return
 
     # C0 shape: n=1024, P=4, dominant (slack U[0.1,1]), F ~ U[-1,1]
@@ -165,6 +187,7 @@ def main():
     case("mixed_n96_P8", a, b, bnd, F, ref)
     nonsymmetric(ref, seed)
     adi(ref, seed)
+    fourier(ref, seed)
 
 
 if __name__ == "__main__":

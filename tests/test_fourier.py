@@ -1,0 +1,136 @@
+"""Fourier consumer (paper_0901_2859_b200/fourier.py, reference
+poisson/fourier.hpp + poisson/dst.hpp): the reference's fourier_solve
+fixtures (tests/gen_golden.py --fourier), the reference's Fourier tests
+restated (test_poisson.cpp:145-224), and the multi-matrix solve
+(psw_solve_multi) against single-plan STAGED solves."""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+
+def test_dst_raw_matches_the_sine_sum():
+    import torch
+    from paper_0901_2859_b200.fourier import dst_raw
+    for n in (8, 13, 32):  # power of two and not (dst.hpp:96-118 / :120-128)
+        x = np.random.default_rng(n).standard_normal((3, n - 1))
+        j = np.arange(1, n)
+        S = np.sin(np.pi * np.outer(j, j) / n)
+        want = x @ S.T
+        got = dst_raw(torch.from_numpy(x)).numpy()
+        assert np.max(np.abs(got - want)) <= 1e-13 * np.max(np.abs(want))
+        # (2/N) S is the inverse of S (dst.hpp:13-17)
+        back = dst_raw(torch.from_numpy(got * 2.0 / n)).numpy()
+        assert np.max(np.abs(back - x)) <= 1e-13 * np.max(np.abs(x))
+
+
+def test_harmonic_system_is_the_reference_matrix():
+    from paper_0901_2859_b200.fourier import harmonic_system
+    n1, n2, h1, h2 = 24, 40, 1 / 24, 1 / 40
+    for l in (1, 7, 39):
+        hs = harmonic_system(n1, n2, h1, h2, l)
+        s = math.sin(math.pi * l / (2.0 * n2))
+        d = 4.0 * (h1 * h1) / (h2 * h2) * s * s
+        assert hs.d_l == d and hs.matrix.n() == n1 - 1
+        assert np.all(hs.matrix.diag == -(2.0 + d)) and np.all(hs.matrix.sub == 1.0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["fourier_32x32_pes1", "fourier_64x64_pes4", "fourier_24x40_pes3"])
+def test_fourier_matches_reference(psw, cuda, name):
+    from paper_0901_2859_b200.fourier import FourierWorkspace, fourier_solve
+    g = load_golden(name)
+    n1, n2, pes = int(g["n1"]), int(g["n2"]), int(g["pes"])
+    ws = FourierWorkspace(n1, n2, float(g["h1"]), float(g["h2"]), pes)
+    assert ws.partition().boundaries == [int(b) for b in g["bnd"]]
+    u = fourier_solve(cuda.from_numpy(g["f"]).cuda(), ws).cpu().numpy()
+    want = g["u"]
+    assert np.linalg.norm(u - want) / np.linalg.norm(want) <= 1e-12
+    assert np.max(np.abs(u - want)) <= 1e-12 * np.max(np.abs(want))
+    assert np.all(u[0] == 0) and np.all(u[-1] == 0) and np.all(u[:, 0] == 0) and np.all(u[:, -1] == 0)
+
+
+@pytest.mark.gpu
+def test_fourier_zero_is_zero(psw, cuda):  # test_poisson.cpp:145-149
+    from paper_0901_2859_b200.fourier import fourier_solve
+    u = fourier_solve(cuda.zeros(17, 17, dtype=cuda.float64, device="cuda"))
+    assert bool((u == 0).all())
+
+
+@pytest.mark.gpu
+def test_fourier_inverts_discrete_eigenfunction(psw, cuda):  # test_poisson.cpp:151-165
+    from paper_0901_2859_b200.fourier import fourier_solve
+    n, k, m = 32, 3, 5
+    h = 1.0 / n
+    x = np.arange(n + 1) * h
+    f = np.outer(np.sin(np.pi * k * x), np.sin(np.pi * m * x))
+    f[0, :] = f[-1, :] = f[:, 0] = f[:, -1] = 0.0
+    lam = 4 / h**2 * math.sin(math.pi * k / (2 * n)) ** 2 + 4 / h**2 * math.sin(math.pi * m / (2 * n)) ** 2
+    u = fourier_solve(cuda.from_numpy(f).cuda()).cpu().numpy()
+    assert np.max(np.abs(u[1:-1, 1:-1] - f[1:-1, 1:-1] / lam)) <= 1e-12
+
+
+def _laplacian(u, h1, h2):
+    return ((u[2:, 1:-1] - 2 * u[1:-1, 1:-1] + u[:-2, 1:-1]) / h1**2 +
+            (u[1:-1, 2:] - 2 * u[1:-1, 1:-1] + u[1:-1, :-2]) / h2**2)
+
+
+@pytest.mark.gpu
+def test_fourier_discrete_equations_and_convergence(psw, cuda, ref):  # test_poisson.cpp:167-190
+    from paper_0901_2859_b200.fourier import fourier_solve
+    prev = 0.0
+    for n in (16, 32, 64, 128):
+        f, exact = ref.model_problem(n, n)
+        u = fourier_solve(cuda.from_numpy(f).cuda()).cpu().numpy()
+        if n == 64:
+            assert np.max(np.abs(_laplacian(u, 1 / n, 1 / n) + f[1:-1, 1:-1])) <= 1e-9 * np.max(np.abs(f))
+        err = np.max(np.abs(u - exact))
+        if prev:
+            assert 3.5 < prev / err < 4.5
+        prev = err
+
+
+@pytest.mark.gpu
+def test_fourier_rectangular_and_split(psw, cuda, ref):  # test_poisson.cpp:192-224
+    from paper_0901_2859_b200.fourier import FourierWorkspace, fourier_solve
+    n1, n2 = 24, 40
+    x, y = np.arange(n1 + 1) / n1, np.arange(n2 + 1) / n2
+    exact = np.outer(np.sin(2 * np.pi * x), np.sin(2 * np.pi * y))
+    f = 8 * np.pi**2 * exact
+    u = fourier_solve(cuda.from_numpy(f).cuda(), FourierWorkspace(n1, n2, 1 / n1, 1 / n2)).cpu().numpy()
+    assert np.max(np.abs(u - exact)) < 0.05
+    assert np.max(np.abs(_laplacian(u, 1 / n1, 1 / n2) + f[1:-1, 1:-1])) <= 1e-9 * np.max(np.abs(f))
+    f64, _ = ref.model_problem(64, 64)
+    fd = cuda.from_numpy(f64).cuda()
+    plain = fourier_solve(fd, FourierWorkspace(64, 64, 1 / 64, 1 / 64, 1)).cpu().numpy()
+    ws = FourierWorkspace(64, 64, 1 / 64, 1 / 64, 4)
+    assert ws.partition().p() == 3
+    split = fourier_solve(fd, ws).cpu().numpy()
+    assert np.max(np.abs(plain - split)) <= 1e-11
+    assert np.array_equal(split, fourier_solve(fd, ws).cpu().numpy())  # run to run
+
+
+@pytest.mark.gpu
+def test_solve_multi_equals_single_plan_staged(psw, cuda):
+    """psw_solve_multi is, column by column, the single-plan STAGED solve."""
+    rng = np.random.default_rng(5)
+    n, K = 300, 37
+    part = psw.decompose(n, 6).induced_partition()
+    plans, As = [], []
+    for k in range(K):
+        a = rng.uniform(-1, -0.5, n - 1)
+        b = np.abs(np.r_[0, a]) + np.abs(np.r_[a, 0]) + rng.uniform(0.1, 1, n)
+        As.append((a, b))
+        plans.append(psw.Plan(psw.TridiagMatrix.symmetric(a, b), part))
+    F = cuda.from_numpy(rng.uniform(-1, 1, (n, K + 3))).cuda()
+    X = cuda.zeros_like(F)
+    psw.solve_multi(plans, F, X)
+    for k in (0, 17, K - 1):
+        xs = cuda.zeros(n, 1, dtype=cuda.float64, device="cuda")
+        plans[k].solve(F[:, k:k + 1].contiguous(), xs, layout=psw.LAYOUT_R, path=psw.PATH_STAGED)
+        assert cuda.equal(X[:, k], xs[:, 0])
+    with pytest.raises(ValueError):  # plans must share the partition
+        other = psw.Plan(psw.TridiagMatrix.symmetric(*As[0]), psw.decompose(n, 5).induced_partition())
+        psw.solve_multi(plans[:2] + [other], F, X)
