@@ -73,9 +73,11 @@ __device__ __forceinline__ void st_async_2(uint32_t raddr, double a, double b, u
 // for every CTA, dumped by the host after the launch
 constexpr int kTraceSlots = 8;
 __device__ unsigned long long g_ctrace[1024 * kTraceSlots];
+__device__ unsigned long long g_gtrace[1024 * 2];  // globaltimer: push, exchange complete
+__device__ unsigned long long g_btrace[1024 * 8];  // globaltimer: push of every block (G <= 8)
 
 struct CGeom {
-    int n, P, p, m, G, C, S, H, trace, stagger;  // H: TMA box height (divides m)
+    int n, P, p, m, G, C, S, H, trace;  // H: TMA box height (divides m)
     int64_t N, ldx, ntiles;
 };
 
@@ -113,7 +115,7 @@ struct CLayout {
 
 // forward rows of one segment from a zero carry: d~ into dr, partials to
 // the thread's slots (betas.hpp:42-57 split by segment; Lam~, psw_internal.h)
-template <typename T, int W, int NMAX>
+template <typename T, int W, int NMAX, bool EXACT = (NMAX <= kSegLen)>
 __device__ __forceinline__ void fwd(const T* slab, const unsigned char* co, int a, int lane,
                                     int len, T (&dr)[kSegMax], double* sd, double* sx, double* sr,
                                     double* sl, int tid) {
@@ -122,7 +124,7 @@ __device__ __forceinline__ void fwd(const T* slab, const unsigned char* co, int 
     double br = 0.0, bl = 0.0;
 #pragma unroll
     for (int r = 0; r < NMAX; ++r) {
-        if (NMAX == kSegLen || r < len) {
+        if (EXACT || r < kSegLen - 1 || r < len) {
             const Quad<T>* c = reinterpret_cast<const Quad<T>*>(co + coff<T>(a + r));
             const Quad<T> c0 = c[0];
             const T lam = c[1].x;
@@ -141,12 +143,12 @@ __device__ __forceinline__ void fwd(const T* slab, const unsigned char* co, int 
 }
 
 // back substitution of one segment from the exact carries, last row first
-template <typename T, int NMAX>
+template <typename T, int NMAX, bool EXACT = (NMAX <= kSegLen)>
 __device__ __forceinline__ void bwd(const unsigned char* co, int a, int len,
                                     const T (&dr)[kSegMax], T D, T xl, T xn, T* xp, int64_t ldx) {
 #pragma unroll
     for (int r = NMAX - 1; r >= 0; --r) {
-        if (NMAX == kSegLen || r < len) {
+        if (EXACT || r < kSegLen - 1 || r < len) {
             const Quad<T> c1 = reinterpret_cast<const Quad<T>*>(co + coff<T>(a + r))[1];
             xn = fma(c1.w, xn, fma(xl, c1.z, fma(c1.y, D, dr[r])));
             __stcs(xp + int64_t(r) * ldx, xn);
@@ -156,8 +158,8 @@ __device__ __forceinline__ void bwd(const unsigned char* co, int a, int len,
 
 template <typename T, int W, int NSLAB>
 __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
-    const __grid_constant__ CUtensorMap tmF, const __grid_constant__ CUtensorMap tmF1, T* X,
-    CGeom g, const FusedFwd<T>* __restrict__ gff, const FusedBwd<T>* __restrict__ gfb,
+    const __grid_constant__ CUtensorMap tmF, const __grid_constant__ CUtensorMap tmF1,
+    const __grid_constant__ CUtensorMap tmF2, const T* F, int64_t ldf, T* X, CGeom g, const FusedFwd<T>* __restrict__ gff, const FusedBwd<T>* __restrict__ gfb,
     const SegCoef* __restrict__ gsegc, const SegDesc* __restrict__ gdesc,
     const double* __restrict__ gcmat) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -197,11 +199,45 @@ __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
     const int a = sgd.a - base, len = sgd.b - sgd.a;  // slab rows [a, a + len)
     const bool first_seg = (h % S) == 0;
 
+    auto slab_of = [&](int64_t k) {
+        return reinterpret_cast<T*>(smem + size_t(k % NSLAB) * L.slab_b);
+    };
+    auto bars_of = [&](int64_t k) { return bars + (k % NSLAB) * G; };
+    // rows of block jb of unit k into the slab: m / H boxes (+ the n-th row
+    // for the last block of the last CTA); one mbarrier per block
+    auto issue_block = [&](int64_t k, int jb) {
+        const int k0 = int(unit(k) * W);
+        T* slab = slab_of(k);
+        uint64_t* bar = &bars_of(k)[jb];
+        const bool extra = last_cta && jb == G - 1;
+        if (crank == 0 && jb == 0) {
+            // global rows [0, m - 1) into slab rows [1, m): no box reaches row -1
+            // (a box partly outside F is slow to complete)
+            mbar_expect_tx(bar, uint32_t((m - 1) * W * sizeof(T)));
+            for (int r = 0; r + g.H < m; r += g.H)
+                tma_load_2d(slab + size_t(r + 1) * W, &tmF, k0, r, bar);
+            tma_load_2d(slab + size_t(m - g.H + 1) * W, &tmF2, k0, m - g.H, bar);
+            return;
+        }
+        mbar_expect_tx(bar, uint32_t((m + (extra ? 1 : 0)) * W * sizeof(T)));
+        for (int r = jb * m; r < (jb + 1) * m; r += g.H)
+            tma_load_2d(slab + size_t(r) * W, &tmF, k0, base + r, bar);
+        if (extra) {  // row n - 1: one 128-byte bulk copy unless the tile is ragged
+            const int64_t row = base + G * m;
+            if (int64_t(k0) + W <= g.N)
+                bulk_load(slab + size_t(G * m) * W, F + row * ldf + k0, uint32_t(W * sizeof(T)), bar);
+            else
+                tma_load_2d(slab + size_t(G * m) * W, &tmF1, k0, int(row), bar);
+        }
+    };
     if (tid == 0) {
         for (int i = 0; i < NSLAB * G; ++i) mbar_init(&bars[i], 1);
         mbar_init(&xbar[0], 1);
         mbar_init(&xbar[1], 1);
         fence_mbar_init();
+        // the first units stream in while the coefficient tables are copied
+        for (int64_t k = 0; k < NSLAB && k < ntl; ++k)
+            for (int jb = 0; jb < G; ++jb) issue_block(k, jb);
     }
     for (int i = tid; i < nrows; i += nth) {
         const int q = base + i;
@@ -220,36 +256,6 @@ __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
     __syncthreads();
     cluster.sync();  // every CTA's exchange barrier is initialised before any push
 
-    auto slab_of = [&](int64_t k) {
-        return reinterpret_cast<T*>(smem + size_t(k % NSLAB) * L.slab_b);
-    };
-    auto bars_of = [&](int64_t k) { return bars + (k % NSLAB) * G; };
-    // rows of block jb of unit k into the slab: m / H boxes (+ the n-th row
-    // for the last block of the last CTA); one mbarrier per block
-    auto issue_block = [&](int64_t k, int jb) {
-        const int k0 = int(unit(k) * W);
-        T* slab = slab_of(k);
-        uint64_t* bar = &bars_of(k)[jb];
-        const bool extra = last_cta && jb == G - 1;
-        mbar_expect_tx(bar, uint32_t((m + (extra ? 1 : 0)) * W * sizeof(T)));
-        for (int r = jb * m; r < (jb + 1) * m; r += g.H)
-            tma_load_2d(slab + size_t(r) * W, &tmF, k0, base + r, bar);
-        if (extra) tma_load_2d(slab + size_t(G * m) * W, &tmF1, k0, base + G * m, bar);
-    };
-    if (tid == 0) {
-        // clusters start spread over `stagger` ns so that their read phases
-        // (slab loads) and write phases (back substitution) interleave
-        if (g.stagger > 0) {
-            uint64_t t0, t1;
-            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
-            const uint64_t wait = uint64_t(g.stagger) * uint64_t(cid) / uint64_t(ncl);
-            do {
-                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
-            } while (t1 - t0 < wait);
-        }
-        for (int64_t k = 0; k < NSLAB && k < ntl; ++k)
-            for (int jb = 0; jb < G; ++jb) issue_block(k, jb);
-    }
     // each block's last thread (not a scan thread when S > 1) streams the
     // block's rows of the next unit in as soon as the block has swept them
     const bool block_issuer = (h % S) == S - 1 && lane == W - 1;
@@ -266,11 +272,15 @@ __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
         mbar_wait(&bars_of(k)[j], uint32_t((k / NSLAB) & 1));
         stamp(k, 1);
         // ---- forward sweep of the segment, d~ in registers
-        if (len == kSegLen)
-            fwd<T, W, kSegLen>(slab, co, a, lane, kSegLen, dr, sd, sx, sr, sl, tid);
-        else
-            fwd<T, W, kSegMax>(slab, co, a, lane, len, dr, sd, sx, sr, sl, tid);
+        // one instruction stream for every lane: segments are 31, 32 or 33 rows
+        // (m % 32 == 0), and the two segments a warp sweeps may differ in length;
+        // rows 0..30 unpredicated, the last two under a predicate
+        fwd<T, W, kSegMax, false>(slab, co, a, lane, len, dr, sd, sx, sr, sl, tid);
         bar_sync(2 + j, S * W);  // the block's rows swept, its partials visible
+        if (g.trace > 2 && tid == 0) {  // force the deferred barrier wait before the stamp
+            volatile double* vs = sd;
+            if (vs[nth - 1] == 1.2345e300) sd[0] = 0.0;
+        }
         stamp(k, 2);
         if (block_issuer && k + NSLAB < ntl) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -294,14 +304,29 @@ __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
             if (t == 0) Lb = 0.0;  // left_t for t > 0 (betas.hpp:51-55)
             double* dst = allx + (size_t(buf) * P + t) * W * 2 + lane * 2;
             const uint32_t src = smem_u32(dst), bar = smem_u32(&xbar[buf]);
+            if (g.trace && k == 2 && lane == 0 && blockIdx.x < 1024 && j < 8) {
+                unsigned long long tt;
+                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tt));
+                g_btrace[blockIdx.x * 8 + j] = tt;
+            }
             for (int c = 0; c < C; ++c) st_async_2(mapa_u32(src, c), R, Lb, mapa_u32(bar, c));
         }
         stamp(k, 3);
+        if (g.trace && k == 2 && tid == 0 && blockIdx.x < 1024) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            g_gtrace[blockIdx.x * 2] = t;
+        }
         // only the warps evaluating boundary values wait on the exchange (the
         // others would spin on the barrier and starve the scan's shared loads)
         const bool comb = tid < (G + 1) * W;
         if (tid < ((G + 1) * W + 31) / 32 * 32) mbar_wait(&xbar[buf], uint32_t((k >> 1) & 1));
         stamp(k, 4);
+        if (g.trace && k == 2 && tid == 0 && blockIdx.x < 1024) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            g_gtrace[blockIdx.x * 2 + 1] = t;
+        }
         // ---- the G + 1 boundary values of this CTA's blocks
         if (comb) {
             const int r = tid / W, ln = tid % W;
@@ -347,10 +372,7 @@ __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
         T xn = T(sr[tid]);
         if (kk < g.N) {
             T* xp = X + int64_t(sgd.a) * g.ldx + kk;
-            if (len == kSegLen)
-                bwd<T, kSegLen>(co, a, kSegLen, dr, D, xlt, xn, xp, g.ldx);
-            else
-                bwd<T, kSegMax>(co, a, len, dr, D, xlt, xn, xp, g.ldx);
+            bwd<T, kSegMax, false>(co, a, len, dr, D, xlt, xn, xp, g.ldx);
         }
         stamp(k, 6);
     }
@@ -414,8 +436,8 @@ int box_height(int m) {
     return 32;
 }
 
-bool encode(CUtensorMap* tm, CUtensorMap* tm1, const void* F, int64_t N, int64_t n, int64_t ldf,
-            int es, int W, int H) {
+bool encode(CUtensorMap* tm, CUtensorMap* tm1, CUtensorMap* tm2, const void* F, int64_t N,
+            int64_t n, int64_t ldf, int es, int W, int H) {
     auto enc = tensor_map_encoder();
     if (!enc) {
         set_error(PSW_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
@@ -425,6 +447,7 @@ bool encode(CUtensorMap* tm, CUtensorMap* tm1, const void* F, int64_t N, int64_t
     const cuuint64_t strides[1] = {cuuint64_t(ldf) * cuuint64_t(es)};
     const cuuint32_t box[2] = {cuuint32_t(W), cuuint32_t(H)};
     const cuuint32_t box1[2] = {cuuint32_t(W), 1};
+    const cuuint32_t box2[2] = {cuuint32_t(W), cuuint32_t(H - 1)};
     const cuuint32_t estr[2] = {1, 1};
     const auto dt = es == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     CUresult r = enc(tm, dt, 2, const_cast<void*>(F), dims, strides, box, estr,
@@ -432,6 +455,10 @@ bool encode(CUtensorMap* tm, CUtensorMap* tm1, const void* F, int64_t N, int64_t
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r == CUDA_SUCCESS)
         r = enc(tm1, dt, 2, const_cast<void*>(F), dims, strides, box1, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS)
+        r = enc(tm2, dt, 2, const_cast<void*>(F), dims, strides, box2, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
@@ -444,9 +471,9 @@ bool encode(CUtensorMap* tm, CUtensorMap* tm1, const void* F, int64_t N, int64_t
 template <typename T, int W, int NSLAB>
 int launch(const psw_plan* pl, const CChoice& ch, const void* F, int64_t ldf, void* X, int64_t ldx,
            int64_t N, cudaStream_t s, void** ev, int nev) {
-    CUtensorMap tm, tm1;
+    CUtensorMap tm, tm1, tm2;
     const int H = box_height(int(pl->m));
-    if (!encode(&tm, &tm1, F, N, pl->n, ldf, int(sizeof(T)), W, H)) return PSW_CUDA_ERROR;
+    if (!encode(&tm, &tm1, &tm2, F, N, pl->n, ldf, int(sizeof(T)), W, H)) return PSW_CUDA_ERROR;
     CGeom g;
     g.n = int(pl->n);
     g.P = int(pl->P);
@@ -456,11 +483,7 @@ int launch(const psw_plan* pl, const CChoice& ch, const void* F, int64_t ldf, vo
     g.C = ch.C;
     g.S = pl->nseg;
     g.H = H;
-    g.trace = std::getenv("PSW_CLUSTER_TRACE") ? 1 : 0;
-    g.stagger = [] {
-        const char* e = std::getenv("PSW_CLUSTER_STAGGER");  // ns
-        return e ? std::atoi(e) : 0;
-    }();
+    g.trace = std::getenv("PSW_CLUSTER_TRACE") ? std::atoi(std::getenv("PSW_CLUSTER_TRACE")) : 0;
     g.N = N;
     g.ldx = ldx;
     g.ntiles = (N + W - 1) / W;
@@ -500,7 +523,8 @@ int launch(const psw_plan* pl, const CChoice& ch, const void* F, int64_t ldf, vo
         std::fprintf(stderr, "cluster: W=%d slabs=%d G=%d C=%d S=%d threads=%d smem=%zu max_clusters=%d clusters=%lld\n",
                      W, NSLAB, ch.G, ch.C, g.S, ch.G * g.S * W, ch.smem, maxc, (long long)ncl);
     mark(ev, nev, 0, s);
-    PSW_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tm, tm1, static_cast<T*>(X), g,
+    PSW_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tm, tm1, tm2, static_cast<const T*>(F), ldf,
+                                    static_cast<T*>(X), g,
                                     static_cast<const FusedFwd<T>*>(pl->d_ffwd),
                                     static_cast<const FusedBwd<T>*>(pl->d_fbwd), pl->d_seg,
                                     pl->d_segdesc, pl->d_cmat));
@@ -513,6 +537,17 @@ int launch(const psw_plan* pl, const CChoice& ch, const void* F, int64_t ldf, vo
         const char* names[] = {"slab wait", "forward+B1", "scan+push", "exchange wait",
                                "combine+B2+fold+B3", "backward", "  (scan)", "  (push)"};
         const int nb = int(std::min<int64_t>(1024, ncl * ch.C));
+        for (int r = 0; r < ch.C && g.trace > 1; ++r) {  // per cluster rank, phases 0..5
+            std::fprintf(stderr, "cluster trace rank %d:", r);
+            for (int ph = 0; ph < 6; ++ph) {
+                std::vector<long long> v;
+                for (int b = r; b < nb; b += ch.C)
+                    v.push_back((long long)(tr[b * kTraceSlots + ph + 1] - tr[b * kTraceSlots + ph]));
+                std::sort(v.begin(), v.end());
+                std::fprintf(stderr, " %s %lld |", names[ph], v[v.size() / 2]);
+            }
+            std::fprintf(stderr, "\n");
+        }
         for (int ph = 0; ph < 8; ++ph) {
             // phases: slots 0-1-2-(7)-3-4-5-6; ph 6 = scan (2 -> 7), ph 7 = push (7 -> 3)
             const int a0 = ph == 6 ? 2 : ph == 7 ? 7 : ph, a1 = ph == 6 ? 7 : ph == 7 ? 3 : ph + 1;
@@ -520,9 +555,57 @@ int launch(const psw_plan* pl, const CChoice& ch, const void* F, int64_t ldf, vo
             for (int b = 0; b < nb; ++b)
                 v.push_back((long long)(tr[b * kTraceSlots + a1] - tr[b * kTraceSlots + a0]));
             std::sort(v.begin(), v.end());
-            std::fprintf(stderr, "cluster trace %-22s median %7lld  p90 %7lld cycles\n", names[ph],
-                         v[v.size() / 2], v[v.size() * 9 / 10]);
+            std::fprintf(stderr, "cluster trace %-22s min %7lld median %7lld  p90 %7lld cycles\n", names[ph],
+                         v[0], v[v.size() / 2], v[v.size() * 9 / 10]);
         }
+        std::vector<unsigned long long> gt(1024 * 2);
+        cudaMemcpyFromSymbol(gt.data(), g_gtrace, sizeof(unsigned long long) * gt.size());
+        std::vector<long long> lat, skew;
+        for (int c0 = 0; c0 + ch.C <= nb; c0 += ch.C) {
+            unsigned long long mx = 0, mn = ~0ull;
+            for (int r = 0; r < ch.C; ++r) {
+                mx = std::max(mx, gt[(c0 + r) * 2]);
+                mn = std::min(mn, gt[(c0 + r) * 2]);
+            }
+            skew.push_back((long long)(mx - mn));
+            for (int r = 0; r < ch.C; ++r) lat.push_back((long long)(gt[(c0 + r) * 2 + 1]) - (long long)mx);
+        }
+        std::vector<std::vector<long long>> byrank(ch.C);
+        for (int c0 = 0; c0 + ch.C <= nb; c0 += ch.C) {
+            unsigned long long mn = ~0ull;
+            for (int r = 0; r < ch.C; ++r) mn = std::min(mn, gt[(c0 + r) * 2]);
+            for (int r = 0; r < ch.C; ++r) byrank[r].push_back((long long)(gt[(c0 + r) * 2] - mn));
+        }
+        for (int r = 0; r < ch.C; ++r) {
+            std::sort(byrank[r].begin(), byrank[r].end());
+            std::fprintf(stderr, "cluster trace rank %d push offset (ns): median %lld\n", r,
+                         byrank[r][byrank[r].size() / 2]);
+        }
+        {
+            std::vector<unsigned long long> bt(1024 * 8);
+            cudaMemcpyFromSymbol(bt.data(), g_btrace, sizeof(unsigned long long) * bt.size());
+            std::vector<std::vector<long long>> off(ch.C * ch.G);
+            for (int c0 = 0; c0 + ch.C <= nb; c0 += ch.C) {
+                unsigned long long mn = ~0ull;
+                for (int r = 0; r < ch.C; ++r)
+                    for (int jb = 0; jb < ch.G; ++jb) mn = std::min(mn, bt[(c0 + r) * 8 + jb]);
+                for (int r = 0; r < ch.C; ++r)
+                    for (int jb = 0; jb < ch.G; ++jb)
+                        off[r * ch.G + jb].push_back((long long)(bt[(c0 + r) * 8 + jb] - mn));
+            }
+            std::fprintf(stderr, "cluster trace block push offsets (ns, median) rank x block:");
+            for (size_t i = 0; i < off.size(); ++i) {
+                std::sort(off[i].begin(), off[i].end());
+                std::fprintf(stderr, "%s%lld", i % ch.G ? " " : " | ", off[i][off[i].size() / 2]);
+            }
+            std::fprintf(stderr, "\n");
+        }
+        std::sort(lat.begin(), lat.end());
+        std::sort(skew.begin(), skew.end());
+        std::fprintf(stderr, "cluster trace push skew in cluster (ns): median %lld p90 %lld; "
+                     "exchange complete after the last push (ns): min %lld median %lld p90 %lld\n",
+                     skew[skew.size() / 2], skew[skew.size() * 9 / 10], lat[0], lat[lat.size() / 2],
+                     lat[lat.size() * 9 / 10]);
     }
     return PSW_OK;
 }
