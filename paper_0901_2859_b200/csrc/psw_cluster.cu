@@ -75,6 +75,7 @@ constexpr int kTraceSlots = 8;
 __device__ unsigned long long g_ctrace[1024 * kTraceSlots];
 __device__ unsigned long long g_gtrace[1024 * 2];  // globaltimer: push, exchange complete
 __device__ unsigned long long g_btrace[1024 * 8];  // globaltimer: push of every block (G <= 8)
+__device__ unsigned long long g_etrace[1024 * 4];  // globaltimer: entry, tables ready, first tile done, exit
 
 struct CGeom {
     int n, P, p, m, G, C, S, H, trace;  // H: TMA box height (divides m)
@@ -109,7 +110,7 @@ struct CLayout {
         cm = up(vals + size_t(G + 1) * W * sizeof(double));
         segc = up(cm + size_t(G + 1) * 2 * P * sizeof(double));
         bars = up(segc + size_t(G) * S * sizeof(SegCoef));
-        total = bars + size_t(NSLAB * G + 2) * sizeof(uint64_t);
+        total = bars + size_t(NSLAB * G + 3) * sizeof(uint64_t);
     }
 };
 
@@ -161,9 +162,17 @@ __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
     const __grid_constant__ CUtensorMap tmF, const __grid_constant__ CUtensorMap tmF1,
     const __grid_constant__ CUtensorMap tmF2, const T* F, int64_t ldf, T* X, CGeom g, const FusedFwd<T>* __restrict__ gff, const FusedBwd<T>* __restrict__ gfb,
     const SegCoef* __restrict__ gsegc, const SegDesc* __restrict__ gdesc,
-    const double* __restrict__ gcmat) {
+    const double* __restrict__ gcmat, const unsigned char* __restrict__ gtab, int64_t tab_stride) {
     extern __shared__ __align__(128) unsigned char smem[];
     cg::cluster_group cluster = cg::this_cluster();
+    auto etrace = [&](int slot) {
+        if (g.trace && threadIdx.x == 0 && blockIdx.x < 1024) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            g_etrace[blockIdx.x * 4 + slot] = t;
+        }
+    };
+    etrace(0);
     const int C = g.C, G = g.G, S = g.S, P = g.P, p = g.p, m = g.m;
     const int crank = int(cluster.block_rank());
     const int64_t cid = blockIdx.x / C, ncl = gridDim.x / C;
@@ -234,19 +243,17 @@ __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
         for (int i = 0; i < NSLAB * G; ++i) mbar_init(&bars[i], 1);
         mbar_init(&xbar[0], 1);
         mbar_init(&xbar[1], 1);
+        mbar_init(&xbar[2], 1);  // coefficient tables
         fence_mbar_init();
+        // this rank's coefficient tables (prebuilt in the shared-memory layout)
+        const uint32_t tb = uint32_t(coff<T>(nrows) + 16 + 15) & ~15u;
+        mbar_expect_tx(&xbar[2], tb);
+        for (uint32_t o = 0; o < tb; o += 32768)
+            bulk_load(co + o, gtab + size_t(crank) * size_t(tab_stride) + o,
+                      tb - o < 32768u ? tb - o : 32768u, &xbar[2]);
         // the first units stream in while the coefficient tables are copied
         for (int64_t k = 0; k < NSLAB && k < ntl; ++k)
             for (int jb = 0; jb < G; ++jb) issue_block(k, jb);
-    }
-    for (int i = tid; i < nrows; i += nth) {
-        const int q = base + i;
-        if (q < 0) continue;
-        const FusedFwd<T> f = gff[q];
-        const FusedBwd<T> b = gfb[q];
-        Quad<T>* o = reinterpret_cast<Quad<T>*>(co + coff<T>(i));
-        o[0] = {f.rp, f.ma, f.gr, f.gl};
-        o[1] = {f.lam, b.mu, b.w, b.al};
     }
     for (int i = tid; i < G * S; i += nth) segc[i] = gsegc[crank * G * S + i];
     for (int i = tid; i < (G + 1) * 2 * P; i += nth) {  // rows of boundaries crank*G - 1 + r
@@ -255,6 +262,8 @@ __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
     }
     __syncthreads();
     cluster.sync();  // every CTA's exchange barrier is initialised before any push
+    mbar_wait(&xbar[2], 0);
+    etrace(1);
 
     // each block's last thread (not a scan thread when S > 1) streams the
     // block's rows of the next unit in as soon as the block has swept them
@@ -375,8 +384,10 @@ __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
             bwd<T, kSegMax, false>(co, a, len, dr, D, xlt, xn, xp, g.ldx);
         }
         stamp(k, 6);
+        if (k == 0) etrace(2);
     }
     cluster.sync();  // no CTA leaves while a peer may still push into it
+    etrace(3);
 }
 
 // ---------------------------------------------------------------- host side
@@ -468,9 +479,49 @@ bool encode(CUtensorMap* tm, CUtensorMap* tm1, CUtensorMap* tm2, const void* F, 
     return true;
 }
 
+// Coefficient tables of every cluster rank in the kernel's shared-memory
+// layout (coff), built once per plan and choice: the kernel fetches its
+// rank's table with one bulk copy instead of scattering rows.
+template <typename T>
+int cluster_tables(const psw_plan* pl, const CChoice& ch) {
+    const int G = ch.G, C = ch.C, m = int(pl->m);
+    const int64_t key = (int64_t(G) << 32) | (int64_t(C) << 16) | int64_t(sizeof(T));
+    if (pl->d_ctab && pl->ctab_key == key) return PSW_OK;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    if (pl->d_ctab && pl->ctab_key == key) return PSW_OK;
+    const int ra = G * m + 1;
+    const size_t stride = ((coff<T>(ra) + 16 + 127) / 128) * 128;
+    std::vector<FusedFwd<T>> ff(pl->n);
+    std::vector<FusedBwd<T>> fb(pl->n);
+    PSW_CUDA_TRY(cudaMemcpy(ff.data(), pl->d_ffwd, sizeof(FusedFwd<T>) * pl->n, cudaMemcpyDeviceToHost));
+    PSW_CUDA_TRY(cudaMemcpy(fb.data(), pl->d_fbwd, sizeof(FusedBwd<T>) * pl->n, cudaMemcpyDeviceToHost));
+    std::vector<unsigned char> host(stride * C, 0);
+    for (int c = 0; c < C; ++c) {
+        const int base = c * G * m - 1;
+        const int nrows = c == C - 1 ? G * m + 1 : G * m;
+        for (int i = 0; i < nrows; ++i) {
+            const int q = base + i;
+            if (q < 0 || q >= pl->n) continue;
+            Quad<T>* o = reinterpret_cast<Quad<T>*>(host.data() + size_t(c) * stride + coff<T>(i));
+            o[0] = {ff[q].rp, ff[q].ma, ff[q].gr, ff[q].gl};
+            o[1] = {ff[q].lam, fb[q].mu, fb[q].w, fb[q].al};
+        }
+    }
+    void* d = nullptr;
+    PSW_CUDA_TRY(cudaMalloc(&d, host.size()));
+    PSW_CUDA_TRY(cudaMemcpy(d, host.data(), host.size(), cudaMemcpyHostToDevice));
+    if (pl->d_ctab) cudaFree(pl->d_ctab);
+    pl->d_ctab = d;
+    pl->ctab_key = key;
+    pl->ctab_stride = int64_t(stride);
+    return PSW_OK;
+}
+
 template <typename T, int W, int NSLAB>
 int launch(const psw_plan* pl, const CChoice& ch, const void* F, int64_t ldf, void* X, int64_t ldx,
            int64_t N, cudaStream_t s, void** ev, int nev) {
+    if (int rc = cluster_tables<T>(pl, ch)) return rc;
     CUtensorMap tm, tm1, tm2;
     const int H = box_height(int(pl->m));
     if (!encode(&tm, &tm1, &tm2, F, N, pl->n, ldf, int(sizeof(T)), W, H)) return PSW_CUDA_ERROR;
@@ -527,7 +578,8 @@ int launch(const psw_plan* pl, const CChoice& ch, const void* F, int64_t ldf, vo
                                     static_cast<T*>(X), g,
                                     static_cast<const FusedFwd<T>*>(pl->d_ffwd),
                                     static_cast<const FusedBwd<T>*>(pl->d_fbwd), pl->d_seg,
-                                    pl->d_segdesc, pl->d_cmat));
+                                    pl->d_segdesc, pl->d_cmat,
+                                    static_cast<const unsigned char*>(pl->d_ctab), pl->ctab_stride));
     mark(ev, nev, 1, s);
     note_launches(1);
     if (g.trace) {
@@ -599,6 +651,22 @@ int launch(const psw_plan* pl, const CChoice& ch, const void* F, int64_t ldf, vo
                 std::fprintf(stderr, "%s%lld", i % ch.G ? " " : " | ", off[i][off[i].size() / 2]);
             }
             std::fprintf(stderr, "\n");
+        }
+        {
+            std::vector<unsigned long long> et(1024 * 4);
+            cudaMemcpyFromSymbol(et.data(), g_etrace, sizeof(unsigned long long) * et.size());
+            unsigned long long t0 = ~0ull;
+            for (int b = 0; b < nb; ++b) t0 = std::min(t0, et[b * 4]);
+            long long mx[4] = {0, 0, 0, 0}, mnv[4] = {1LL << 60, 1LL << 60, 1LL << 60, 1LL << 60};
+            for (int b = 0; b < nb; ++b)
+                for (int q = 0; q < 4; ++q) {
+                    const long long v = (long long)(et[b * 4 + q] - t0);
+                    mx[q] = std::max(mx[q], v);
+                    mnv[q] = std::min(mnv[q], v);
+                }
+            std::fprintf(stderr, "cluster trace timeline (ns from the first CTA): entry %lld..%lld, "
+                         "tables ready %lld..%lld, first tile done %lld..%lld, exit %lld..%lld\n",
+                         mnv[0], mx[0], mnv[1], mx[1], mnv[2], mx[2], mnv[3], mx[3]);
         }
         std::sort(lat.begin(), lat.end());
         std::sort(skew.begin(), skew.end());

@@ -114,6 +114,10 @@ struct psw_plan {
     psw::SegCoef* d_seg = nullptr;     // per segment (block-major, see seg_off)
     psw::SegDesc* d_segdesc = nullptr; // per segment rows / block
     int32_t* d_segoff = nullptr;       // [P+1] first segment of every block
+    // CLUSTER path: per-cluster-rank coefficient tables in the kernel's shared
+    // memory layout, built at the first CLUSTER solve (psw_cluster.cu)
+    mutable void* d_ctab = nullptr;
+    mutable int64_t ctab_key = 0, ctab_stride = 0;
     std::vector<int32_t> seg_off;      // host copy
 
     // multi-GPU row shard (psw_shard_*); world == 1 for a full plan

@@ -323,7 +323,7 @@ void free_plan(psw_plan* pl) {
     cudaSetDevice(pl->device);
     void* ptrs[] = {pl->d_fwd, pl->d_bwd, pl->d_blk, pl->d_zr, pl->d_zl, pl->d_items,
                     pl->d_lvl_off, pl->d_ffwd, pl->d_fbwd, pl->d_seg, pl->d_cmat,
-                    pl->d_segdesc, pl->d_segoff,
+                    pl->d_segdesc, pl->d_segoff, pl->d_ctab,
                     pl->d_partial_spec, pl->d_coarse_items, pl->d_local_items, pl->d_partial_index};
     for (void* q : ptrs)
         if (q) cudaFree(q);
