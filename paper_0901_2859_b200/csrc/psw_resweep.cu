@@ -26,6 +26,7 @@
 // last are still in L2 when K3 starts (C1: F = 128 MB, L2 = 126 MB).
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "psw_device.cuh"
 #include "psw_internal.h"
@@ -62,27 +63,38 @@ __global__ void __launch_bounds__(kThreads) rs_part_kernel(
     const SegDesc sd = desc[s];
     const int a = sd.a, len = sd.b - sd.a;
     const T* fp = F + int64_t(a) * ldf + (kv ? k : 0);
-    T v[kSegMax];
-    if (kv) {
-#pragma unroll
-        for (int r = 0; r < kSegMax; ++r)
-            if (r < len) v[r] = fp[int64_t(r) * ldf];
-    }
-    for (int i = threadIdx.x; i < len; i += kThreads) cs[i] = ff[a + i];
-    __syncthreads();
-    if (!kv) return;
+    // segments of >= 31 rows (every segment of a uniform partition) run
+    // their first 31 rows unpredicated: a fully predicated 33-row sweep is
+    // several times slower
     T d = T(0), lx = T(0);
     double br = 0.0, bl = 0.0;
+    auto sweep = [&](auto full) {
+        constexpr bool FULL = decltype(full)::value;
+        T v[kSegMax];
+        if (kv) {
 #pragma unroll
-    for (int r = 0; r < kSegMax; ++r) {
-        if (r < len) {
-            const FusedFwd<T> c = cs[r];
-            d = fma(c.ma, d, v[r] * c.rp);
-            br = fma(double(v[r]), double(c.gr), br);
-            bl = fma(double(v[r]), double(c.gl), bl);
-            lx = fma(c.lam, d, lx);
+            for (int r = 0; r < kSegMax; ++r)
+                if ((FULL && r < kSegLen - 1) || r < len) v[r] = fp[int64_t(r) * ldf];
         }
-    }
+        for (int i = threadIdx.x; i < len; i += kThreads) cs[i] = ff[a + i];
+        __syncthreads();
+        if (!kv) return;
+#pragma unroll
+        for (int r = 0; r < kSegMax; ++r) {
+            if ((FULL && r < kSegLen - 1) || r < len) {
+                const FusedFwd<T> c = cs[r];
+                d = fma(c.ma, d, v[r] * c.rp);
+                br = fma(double(v[r]), double(c.gr), br);
+                bl = fma(double(v[r]), double(c.gl), bl);
+                lx = fma(c.lam, d, lx);
+            }
+        }
+    };
+    if (len >= kSegLen - 1)
+        sweep(std::true_type{});
+    else
+        sweep(std::false_type{});
+    if (!kv) return;
     const int64_t o = int64_t(s) * sc.ld + k;
     sc.pd[o] = d;
     sc.px[o] = lx;
@@ -256,37 +268,44 @@ __global__ void __launch_bounds__(kThreads, 4) rs_solve_kernel(
     const SegDesc sd = desc[s];
     const int a = sd.a, len = sd.b - sd.a, t = sd.t;
     const T* fp = F + int64_t(a) * ldf + (kv ? k : 0);
-    T v[kSegMax];
-    if (kv) {
+    auto sweep = [&](auto full) {
+        constexpr bool FULL = decltype(full)::value;
+        T v[kSegMax];
+        if (kv) {
 #pragma unroll
-        for (int r = 0; r < kSegMax; ++r)
-            if (r < len) v[r] = __ldcs(fp + int64_t(r) * ldf);
-    }
-    for (int i = threadIdx.x; i < len; i += kThreads) {
-        csf[i] = cf[a + i];
-        csb[i] = cb[a + i];
-    }
-    __syncthreads();
-    if (!kv) return;
-    const int64_t o = int64_t(s) * sc.ld + k;
-    T d = sc.pd[o];
-    T xn = T(sc.pr[o]);
-    const T xl = t > 0 ? T(V[int64_t(t - 1) * sc.ld + k]) : T(0);
-#pragma unroll
-    for (int r = 0; r < kSegMax; ++r) {
-        if (r < len) {
-            d = fma(csf[r].ma, d, v[r] * csf[r].rp);
-            v[r] = d;
+            for (int r = 0; r < kSegMax; ++r)
+                if ((FULL && r < kSegLen - 1) || r < len) v[r] = __ldcs(fp + int64_t(r) * ldf);
         }
-    }
-    T* xp = X + int64_t(a) * ldx + k;
-#pragma unroll
-    for (int r = kSegMax - 1; r >= 0; --r) {
-        if (r < len) {
-            xn = fma(csb[r].al, xn, fma(xl, csb[r].w, v[r]));
-            __stcs(xp + int64_t(r) * ldx, xn);
+        for (int i = threadIdx.x; i < len; i += kThreads) {
+            csf[i] = cf[a + i];
+            csb[i] = cb[a + i];
         }
-    }
+        __syncthreads();
+        if (!kv) return;
+        const int64_t o = int64_t(s) * sc.ld + k;
+        T d = sc.pd[o];
+        T xn = T(sc.pr[o]);
+        const T xl = t > 0 ? T(V[int64_t(t - 1) * sc.ld + k]) : T(0);
+#pragma unroll
+        for (int r = 0; r < kSegMax; ++r) {
+            if ((FULL && r < kSegLen - 1) || r < len) {
+                d = fma(csf[r].ma, d, v[r] * csf[r].rp);
+                v[r] = d;
+            }
+        }
+        T* xp = X + int64_t(a) * ldx + k;
+#pragma unroll
+        for (int r = kSegMax - 1; r >= 0; --r) {
+            if ((FULL && r < kSegLen - 1) || r < len) {
+                xn = fma(csb[r].al, xn, fma(xl, csb[r].w, v[r]));
+                __stcs(xp + int64_t(r) * ldx, xn);
+            }
+        }
+    };
+    if (len >= kSegLen - 1)
+        sweep(std::true_type{});
+    else
+        sweep(std::false_type{});
 }
 
 // ------------------------------------------------------------ layout S
@@ -339,17 +358,24 @@ __global__ void __launch_bounds__(kSWarps * 32) rs_part_s_kernel(
     const T* col = tiles[warp][lane];
     T d = T(0), lx = T(0);
     double br = 0.0, bl = 0.0;
+    auto sweep = [&](auto full) {
+        constexpr bool FULL = decltype(full)::value;
 #pragma unroll
-    for (int r = 0; r < kSegMax; ++r) {
-        if (r < len) {
-            const FusedFwd<T> c = cs[r];
-            const T f = col[r];
-            d = fma(c.ma, d, f * c.rp);
-            br = fma(double(f), double(c.gr), br);
-            bl = fma(double(f), double(c.gl), bl);
-            lx = fma(c.lam, d, lx);
+        for (int r = 0; r < kSegMax; ++r) {
+            if ((FULL && r < kSegLen - 1) || r < len) {
+                const FusedFwd<T> c = cs[r];
+                const T f = col[r];
+                d = fma(c.ma, d, f * c.rp);
+                br = fma(double(f), double(c.gr), br);
+                bl = fma(double(f), double(c.gl), bl);
+                lx = fma(c.lam, d, lx);
+            }
         }
-    }
+    };
+    if (len >= kSegLen - 1)
+        sweep(std::true_type{});
+    else
+        sweep(std::false_type{});
     const int64_t o = int64_t(s) * sc.ld + k0 + lane;
     sc.pd[o] = d;
     sc.px[o] = lx;
@@ -387,21 +413,28 @@ __global__ void __launch_bounds__(kSWarps * 32) rs_solve_s_kernel(
     __syncthreads();
     if (nk == 0) return;
     T* col = tiles[warp][lane];
-    if (lane < nk) {
+    auto sweep = [&](auto full) {
+        constexpr bool FULL = decltype(full)::value;
 #pragma unroll
         for (int r = 0; r < kSegMax; ++r) {
-            if (r < len) {
+            if ((FULL && r < kSegLen - 1) || r < len) {
                 d = fma(csf[r].ma, d, col[r] * csf[r].rp);
                 col[r] = d;
             }
         }
 #pragma unroll
         for (int r = kSegMax - 1; r >= 0; --r) {
-            if (r < len) {
+            if ((FULL && r < kSegLen - 1) || r < len) {
                 xn = fma(csb[r].al, xn, fma(xl, csb[r].w, col[r]));
                 col[r] = xn;
             }
         }
+    };
+    if (lane < nk) {
+        if (len >= kSegLen - 1)
+            sweep(std::true_type{});
+        else
+            sweep(std::false_type{});
     }
     __syncwarp();
     // coalesced write-back: RHS j's rows by lane (row 32 by lane = rhs)
