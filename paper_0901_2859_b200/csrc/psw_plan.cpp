@@ -856,10 +856,11 @@ int psw_solve_ex(const psw_plan* plan, const void* F, int64_t ldf, void* X, int6
         t_last_path = PSW_PATH_FUSED;
         rc = psw::solve_fused(plan, F, ldf, X, ldx, nrhs, layout, s, opts ? opts->events : nullptr,
                               opts ? opts->nevents : 0);
-    } else if (path == PSW_PATH_AUTO && !want_intermediates && plan->dtype == PSW_F64 &&
-               plan->P <= 64 && psw::resweep_supported(plan, layout, nrhs)) {
-        // fp64 layout R beyond the FUSED path's reach (large blocks, e.g. C3):
-        // 3 s bytes per unknown instead of STAGED's 4 s (measured C3 5.3 vs 6.3 ms)
+    } else if (path == PSW_PATH_AUTO && !want_intermediates && plan->P <= 64 &&
+               psw::resweep_supported(plan, layout, nrhs)) {
+        // beyond the CLUSTER/FUSED paths' reach (large blocks, layout S): 3 s
+        // bytes per unknown instead of STAGED's 4 s (measured C3 4.6 vs 6.3 ms,
+        // C4 rows 136 vs 195 us, C2 fp32 11.9 vs 13.3 ms)
         t_last_path = PSW_PATH_RESWEEP;
         rc = psw::solve_resweep(plan, F, ldf, X, ldx, nrhs, layout, s,
                                 opts ? opts->events : nullptr, opts ? opts->nevents : 0);

@@ -46,8 +46,8 @@ template <typename T>
 struct Scratch {
     T* pd;
     T* px;
-    double* pr;
-    double* pl;
+    T* pr;  // partial sums accumulated in double, stored in the solve precision
+    T* pl;
     int64_t ld;  // row pitch (>= N, a multiple of 32)
 };
 
@@ -98,8 +98,8 @@ __global__ void __launch_bounds__(kThreads) rs_part_kernel(
     const int64_t o = int64_t(s) * sc.ld + k;
     sc.pd[o] = d;
     sc.px[o] = lx;
-    sc.pr[o] = br;
-    sc.pl[o] = bl;
+    sc.pr[o] = T(br);
+    sc.pl[o] = T(bl);
 }
 
 // ------------------------------------------------------------------ K2
@@ -121,8 +121,8 @@ __device__ __forceinline__ void fold_fwd(const Scratch<T>& sc, const SegCoef* __
                 const int64_t o = int64_t(lo + u) * sc.ld + k;
                 dv[u] = sc.pd[o];
                 xv[u] = sc.px[o];
-                rv[u] = sc.pr[o];
-                lv[u] = sc.pl[o];
+                rv[u] = double(sc.pr[o]);
+                lv[u] = double(sc.pl[o]);
             }
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -154,7 +154,7 @@ __device__ __forceinline__ void fold_bwd(const Scratch<T>& sc, const SegCoef* __
             const int sg = hi - 1 - u;
             if (sg >= s0) {
                 const SegCoef c = segc[sg];
-                sc.pr[int64_t(sg) * sc.ld + k] = xb;
+                sc.pr[int64_t(sg) * sc.ld + k] = T(xb);
                 xb = fma(c.nu, xb, fma(xl, c.k2, double(av[u])));
             }
         }
@@ -379,8 +379,8 @@ __global__ void __launch_bounds__(kSWarps * 32) rs_part_s_kernel(
     const int64_t o = int64_t(s) * sc.ld + k0 + lane;
     sc.pd[o] = d;
     sc.px[o] = lx;
-    sc.pr[o] = br;
-    sc.pl[o] = bl;
+    sc.pr[o] = T(br);
+    sc.pl[o] = T(bl);
 }
 
 template <typename T>
@@ -454,19 +454,19 @@ int launch_resweep(const psw_plan* pl, const void* Fv, int64_t ldf, void* Xv, in
     const int NS = pl->seg_off.back();
     const int64_t ld = (N + 31) / 32 * 32;  // scratch row pitch
     const size_t sn = size_t(NS) * size_t(ld);
-    const size_t need = sn * (2 * sizeof(T) + 2 * sizeof(double)) +
-                        sizeof(double) * size_t(ld) * (2 * size_t(P) + size_t(std::max(p, 1)));
+    const size_t need = sn * 4 * sizeof(T) +
+                        sizeof(double) * size_t(ld) * (2 * size_t(P) + size_t(std::max(p, 1))) + 256;
     void* scratch = nullptr;
     PSW_CUDA_TRY(cudaMallocAsync(&scratch, need, s));
     char* c = static_cast<char*>(scratch);
     Scratch<T> sc;
     sc.ld = ld;
-    sc.pr = reinterpret_cast<double*>(c);
-    sc.pl = sc.pr + sn;
-    double* bl = sc.pl + sn;
+    double* bl = reinterpret_cast<double*>(c);
     double* br = bl + size_t(P) * ld;
     double* V = br + size_t(P) * ld;
-    sc.pd = reinterpret_cast<T*>(V + size_t(std::max(p, 1)) * ld);
+    sc.pr = reinterpret_cast<T*>(V + size_t(std::max(p, 1)) * ld);
+    sc.pl = sc.pr + sn;
+    sc.pd = sc.pl + sn;
     sc.px = sc.pd + sn;
     const unsigned gx = unsigned((N + kThreads - 1) / kThreads);
     const auto* desc = pl->d_segdesc;
@@ -485,7 +485,11 @@ int launch_resweep(const psw_plan* pl, const void* Fv, int64_t ldf, void* Xv, in
     int nsm = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, pl->device);
     const bool cm = pl->d_cmat && P <= kCombMaxP;
-    if (cm && (N + 31) / 32 >= nsm) {
+    static const int fused_comb = [] {  // PSW_RESWEEP_COMB=0: always the split kernels
+        const char* e = std::getenv("PSW_RESWEEP_COMB");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (cm && fused_comb && (N + 31) / 32 >= nsm && int64_t(NS) * 4 <= 512) {
         const size_t cmb = sizeof(double) * size_t(p) * 2 * P;
         PSW_CUDA_TRY(cudaFuncSetAttribute(rs_comb_kernel<T>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(cmb)));
