@@ -80,3 +80,19 @@ def test_cluster_config_C1(psw, cuda):
     Xs = X[:, cuda.from_numpy(ks).cuda()].T.cpu().numpy()
     want = Oracle().solve_batch_threads(a, b, a, np.array(part.boundaries), Fs, 8)[0]
     assert rel_l2(Xs, want) <= FP64_TOL
+
+
+@pytest.mark.parametrize("n,P,dtype", [(4096, 16, 0), (8192, 8, 0), (2048, 4, 0), (4096, 32, 0),
+                                       (1024, 4, 0), (2048, 8, 1), (4096, 8, 1)])
+def test_cluster_shapes(psw, cuda, n, P, dtype):
+    """Cluster sizes 1..8, blocks of 128..1024 rows, both dtypes, against STAGED."""
+    rng = np.random.default_rng(n + P)
+    a = rng.uniform(-1, -0.5, n - 1)
+    b = np.abs(np.r_[0, a]) + np.abs(np.r_[a, 0]) + rng.uniform(0.1, 1, n)
+    plan = psw.Plan(psw.TridiagMatrix.symmetric(a, b), psw.decompose(n, P).induced_partition(),
+                    dtype=psw.F64 if dtype == 0 else psw.F32)
+    F = rng.uniform(-1, 1, (300, n))
+    ref = gpu_solve(psw, cuda, plan, F, 0, path=psw.PATH_STAGED)
+    X = gpu_solve(psw, cuda, plan, F, 0, path=psw.PATH_CLUSTER)
+    tol = 1e-12 if dtype == 0 else 1e-5
+    assert rel_l2(X, ref) <= tol, rel_l2(X, ref)
