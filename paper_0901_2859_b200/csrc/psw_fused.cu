@@ -129,13 +129,13 @@ constexpr int kSegMax = kSegLen + 1;  // the last block owns m + 1 rows
 
 // Forward rows of one segment, d~ kept in registers. NMAX is a compile-time
 // bound (fully unrolled); rows q >= len are skipped (only when NMAX > len).
-template <typename T, int W, int NMAX>
+template <typename T, int W, int NMAX, bool UNI = false>
 __device__ __forceinline__ void fwd_rows(const FusedFwd<T>* __restrict__ cf,
                                          const T* __restrict__ col, T (&dr)[kSegMax], T& d,
                                          T& sr, T& sl, T& sx, int len) {
 #pragma unroll
     for (int q = 0; q < NMAX; ++q) {
-        if (NMAX == kSegLen || q < len) {
+        if (NMAX == kSegLen || (UNI && q < kSegLen - 1) || q < len) {
             const FusedFwd<T> c = cf[q];
             const T f = col[q * W];
             d = fma(c.ma, d, f * c.rp);
@@ -148,12 +148,12 @@ __device__ __forceinline__ void fwd_rows(const FusedFwd<T>* __restrict__ cf,
 }
 
 // Forward rows of one segment, d~ written back over f in the slab.
-template <typename T, int W, int NMAX>
+template <typename T, int W, int NMAX, bool UNI = false>
 __device__ __forceinline__ void fwd_rows_smem(const FusedFwd<T>* __restrict__ cf, T* col, T& d,
                                               T& sr, T& sl, T& sx, int len) {
 #pragma unroll
     for (int q = 0; q < NMAX; ++q) {
-        if (NMAX == kSegLen || q < len) {
+        if (NMAX == kSegLen || (UNI && q < kSegLen - 1) || q < len) {
             const FusedFwd<T> c = cf[q];
             const T f = col[q * W];
             d = fma(c.ma, d, f * c.rp);
@@ -166,12 +166,12 @@ __device__ __forceinline__ void fwd_rows_smem(const FusedFwd<T>* __restrict__ cf
 }
 
 // Backward rows reading d~ from the slab (see bwd_rows).
-template <typename T, int W, int NMAX>
+template <typename T, int W, int NMAX, bool UNI = false>
 __device__ __forceinline__ void bwd_rows_smem(const FusedBwd<T>* __restrict__ cb, const T* col,
                                               T D, T xl, T xn, T* xp, int64_t ldx, int len) {
 #pragma unroll
     for (int q = NMAX - 1; q >= 0; --q) {
-        if (NMAX == kSegLen || q < len) {
+        if (NMAX == kSegLen || (UNI && q < kSegLen - 1) || q < len) {
             const FusedBwd<T> c = cb[q];
             const T cq = fma(xl, c.w, fma(c.mu, D, col[q * W]));
             xn = fma(c.al, xn, cq);
@@ -183,13 +183,13 @@ __device__ __forceinline__ void bwd_rows_smem(const FusedBwd<T>* __restrict__ cb
 
 // Backward rows of one segment from the exact carry xn, last row first;
 // xp points at the segment's last row of X and walks up by ldx.
-template <typename T, int NMAX>
+template <typename T, int NMAX, bool UNI = false>
 __device__ __forceinline__ void bwd_rows(const FusedBwd<T>* __restrict__ cb,
                                          const T (&dr)[kSegMax], T D, T xl, T xn, T* xp,
                                          int64_t ldx, int len) {
 #pragma unroll
     for (int q = NMAX - 1; q >= 0; --q) {
-        if (NMAX == kSegLen || q < len) {
+        if (NMAX == kSegLen || (UNI && q < kSegLen - 1) || q < len) {
             const FusedBwd<T> c = cb[q];
             const T cq = fma(xl, c.w, fma(c.mu, D, dr[q]));
             xn = fma(c.al, xn, cq);
@@ -286,13 +286,14 @@ struct FusedTile {
         T* col = slab(k) + x.lane + (x.a - x.row0) * W;
         T d = T(0), sr = T(0), sl = T(0), sx = T(0);
         if constexpr (LAG) {  // d~ parked in place in the slab
-            if (x.len == kSegLen)
-                fwd_rows_smem<T, W, kSegLen>(cf, col, d, sr, sl, sx, kSegLen);
+            // segments of 31..33 rows (m % 32 == 0) share one instruction stream
+            if (x.len >= kSegLen - 1)
+                fwd_rows_smem<T, W, kSegMax, true>(cf, col, d, sr, sl, sx, x.len);
             else
                 fwd_rows_smem<T, W, kSegMax>(cf, col, d, sr, sl, sx, x.len);
         } else {
-            if (x.len == kSegLen)
-                fwd_rows<T, W, kSegLen>(cf, col, dr, d, sr, sl, sx, kSegLen);
+            if (x.len >= kSegLen - 1)
+                fwd_rows<T, W, kSegMax, true>(cf, col, dr, d, sr, sl, sx, x.len);
             else
                 fwd_rows<T, W, kSegMax>(cf, col, dr, d, sr, sl, sx, x.len);
         }
@@ -379,8 +380,8 @@ struct FusedTile {
         const T xn = T(sk[2 * GSW + x.tid]);
         if (k0 + x.lane < g.N && x.len > 0) {
             T* xp = X + k0 + x.lane + int64_t(x.b - 1) * g.ldx;  // last row first
-            if (x.len == kSegLen)
-                bwd_rows<T, kSegLen>(cb, dr, D, xlt, xn, xp, g.ldx, kSegLen);
+            if (x.len >= kSegLen - 1)
+                bwd_rows<T, kSegMax, true>(cb, dr, D, xlt, xn, xp, g.ldx, x.len);
             else
                 bwd_rows<T, kSegMax>(cb, dr, D, xlt, xn, xp, g.ldx, x.len);
         }
