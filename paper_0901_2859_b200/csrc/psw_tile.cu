@@ -23,6 +23,8 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <type_traits>
+
 #include "psw_device.cuh"
 #include "psw_internal.h"
 
@@ -80,14 +82,15 @@ __device__ __forceinline__ void prefetch_l2(const void* q) {
 }
 
 // a segment's rows of this thread's RHS into registers
-template <typename T, int LAYOUT>
+// (FULL: the segment has >= kSegLen - 1 rows, only the last two are predicated)
+template <typename T, int LAYOUT, bool FULL = false>
 __device__ __forceinline__ void load_seg(const T* F, int64_t ldf, int64_t k, int a, int len,
                                          bool kv, uint64_t pol, T (&v)[kSegMax]) {
     const T* src = LAYOUT == PSW_LAYOUT_R ? F + int64_t(a) * ldf + k : F + k * ldf + a;
     const int64_t step = LAYOUT == PSW_LAYOUT_R ? ldf : 1;
 #pragma unroll
     for (int r = 0; r < kSegMax; ++r)
-        v[r] = (kv && r < len) ? ld_hint(src + r * step, pol) : T(0);
+        v[r] = (kv && ((FULL && r < kSegLen - 1) || r < len)) ? ld_hint(src + r * step, pol) : T(0);
 }
 
 // A segment's coefficient rows into the worker's shared staging area, the
@@ -136,33 +139,42 @@ __global__ void __launch_bounds__(kMaxThreads) tile_kernel(const T* F, T* X, con
         for (int s = worker; s < NS; s += NW) {
             const SegDesc sd = tb.desc[s];
             const int len = sd.b - sd.a;
-            T v[kSegMax];
-            load_seg<T, LAYOUT>(F, g.ldf, k, sd.a, len, kv, keep, v);
-            if (g.prefetch && s + NW < NS) {
-                // the worker's next segment into L2 while this one is in flight
-                const SegDesc sn = tb.desc[s + NW];
-                if (LAYOUT == PSW_LAYOUT_R) {
-                    if (lane == 0)
-                        for (int r = 0; r < sn.b - sn.a; ++r)
-                            prefetch_l2(F + int64_t(sn.a + r) * g.ldf + tile * W);
-                } else if (kv) {
-                    for (int r = 0; r < sn.b - sn.a; r += 16) prefetch_l2(F + k * g.ldf + sn.a + r);
-                }
-            }
-            const FusedFwd<T>* cf = stage(ffw + sd.a, len, lane, W, sff);
-            __syncwarp(wmask);
             T d = T(0);
             double sR = 0.0, sL = 0.0, sX = 0.0;
-#pragma unroll
-            for (int r = 0; r < kSegMax; ++r) {
-                if (r < len) {
-                    const FusedFwd<T> c = cf[r];
-                    d = fma(c.ma, d, v[r] * c.rp);
-                    sR = fma(double(v[r]), double(c.gr), sR);
-                    sL = fma(double(v[r]), double(c.gl), sL);
-                    sX = fma(double(c.lam), double(d), sX);
+            // one instruction stream for segments of >= 31 rows (both workers
+            // of a warp), rows 0..30 unpredicated
+            auto pass1 = [&](auto full) {
+                constexpr bool FULL = decltype(full)::value;
+                T v[kSegMax];
+                load_seg<T, LAYOUT, FULL>(F, g.ldf, k, sd.a, len, kv, keep, v);
+                if (g.prefetch && s + NW < NS) {
+                    // the worker's next segment into L2 while this one is in flight
+                    const SegDesc sn = tb.desc[s + NW];
+                    if (LAYOUT == PSW_LAYOUT_R) {
+                        if (lane == 0)
+                            for (int r = 0; r < sn.b - sn.a; ++r)
+                                prefetch_l2(F + int64_t(sn.a + r) * g.ldf + tile * W);
+                    } else if (kv) {
+                        for (int r = 0; r < sn.b - sn.a; r += 16) prefetch_l2(F + k * g.ldf + sn.a + r);
+                    }
                 }
-            }
+                const FusedFwd<T>* cf = stage(ffw + sd.a, len, lane, W, sff);
+                __syncwarp(wmask);
+#pragma unroll
+                for (int r = 0; r < kSegMax; ++r) {
+                    if ((FULL && r < kSegLen - 1) || r < len) {
+                        const FusedFwd<T> c = cf[r];
+                        d = fma(c.ma, d, v[r] * c.rp);
+                        sR = fma(double(v[r]), double(c.gr), sR);
+                        sL = fma(double(v[r]), double(c.gl), sL);
+                        sX = fma(double(c.lam), double(d), sX);
+                    }
+                }
+            };
+            if (len >= kSegLen - 1)
+                pass1(std::true_type{});
+            else
+                pass1(std::false_type{});
             double* ps = part + (size_t(s) * W + lane) * 4;
             ps[0] = double(d);
             ps[1] = sX;
@@ -219,39 +231,46 @@ __global__ void __launch_bounds__(kMaxThreads) tile_kernel(const T* F, T* X, con
         for (int s = worker; s < NS; s += NW) {
             const SegDesc sd = tb.desc[s];
             const int len = sd.b - sd.a, t = sd.t;
-            T v[kSegMax];
-            load_seg<T, LAYOUT>(F, g.ldf, k, sd.a, len, kv, drop, v);
-            const FusedFwd<T>* cf = stage(ffw + sd.a, len, lane, W, sff);
-            const FusedBwd<T>* cb = stage(fbw + sd.a, len, lane, W, sfb);
-            const double* ps = part + (size_t(s) * W + lane) * 4;
-            const T D = T(ps[0]);
-            T x = T(ps[1]);
-            const T xl = t > 0 ? T(vals[(t - 1) * W + lane]) : T(0);
-            __syncwarp(wmask);
-            T d = D;
+            auto pass2 = [&](auto full) {
+                constexpr bool FULL = decltype(full)::value;
+                T v[kSegMax];
+                load_seg<T, LAYOUT, FULL>(F, g.ldf, k, sd.a, len, kv, drop, v);
+                const FusedFwd<T>* cf = stage(ffw + sd.a, len, lane, W, sff);
+                const FusedBwd<T>* cb = stage(fbw + sd.a, len, lane, W, sfb);
+                const double* ps = part + (size_t(s) * W + lane) * 4;
+                const T D = T(ps[0]);
+                T x = T(ps[1]);
+                const T xl = t > 0 ? T(vals[(t - 1) * W + lane]) : T(0);
+                __syncwarp(wmask);
+                T d = D;
 #pragma unroll
-            for (int r = 0; r < kSegMax; ++r) {
-                if (r < len) {
-                    const FusedFwd<T> c = cf[r];
-                    d = fma(c.ma, d, v[r] * c.rp);
-                    v[r] = d;
+                for (int r = 0; r < kSegMax; ++r) {
+                    if ((FULL && r < kSegLen - 1) || r < len) {
+                        const FusedFwd<T> c = cf[r];
+                        d = fma(c.ma, d, v[r] * c.rp);
+                        v[r] = d;
+                    }
                 }
-            }
 #pragma unroll
-            for (int r = kSegMax - 1; r >= 0; --r) {
-                if (r < len) {
-                    const FusedBwd<T> c = cb[r];
-                    x = fma(c.al, x, fma(xl, c.w, v[r]));
-                    v[r] = x;
+                for (int r = kSegMax - 1; r >= 0; --r) {
+                    if ((FULL && r < kSegLen - 1) || r < len) {
+                        const FusedBwd<T> c = cb[r];
+                        x = fma(c.al, x, fma(xl, c.w, v[r]));
+                        v[r] = x;
+                    }
                 }
-            }
-            if (kv) {
-                T* dst = LAYOUT == PSW_LAYOUT_R ? X + int64_t(sd.a) * g.ldx + k : X + k * g.ldx + sd.a;
-                const int64_t step = LAYOUT == PSW_LAYOUT_R ? g.ldx : 1;
+                if (kv) {
+                    T* dst = LAYOUT == PSW_LAYOUT_R ? X + int64_t(sd.a) * g.ldx + k : X + k * g.ldx + sd.a;
+                    const int64_t step = LAYOUT == PSW_LAYOUT_R ? g.ldx : 1;
 #pragma unroll
-                for (int r = 0; r < kSegMax; ++r)
-                    if (r < len) __stcs(dst + r * step, v[r]);
-            }
+                    for (int r = 0; r < kSegMax; ++r)
+                        if ((FULL && r < kSegLen - 1) || r < len) __stcs(dst + r * step, v[r]);
+                }
+            };
+            if (len >= kSegLen - 1)
+                pass2(std::true_type{});
+            else
+                pass2(std::false_type{});
             __syncwarp(wmask);
         }
         __syncthreads();
