@@ -489,7 +489,7 @@ int launch_resweep(const psw_plan* pl, const void* Fv, int64_t ldf, void* Xv, in
         const char* e = std::getenv("PSW_RESWEEP_COMB");
         return e ? std::atoi(e) : 1;
     }();
-    if (cm && fused_comb && (N + 31) / 32 >= nsm && int64_t(NS) * 4 <= 512) {
+    if (cm && fused_comb && (N + 31) / 32 >= nsm / 2 && int64_t(NS) * 4 <= 512) {
         const size_t cmb = sizeof(double) * size_t(p) * 2 * P;
         PSW_CUDA_TRY(cudaFuncSetAttribute(rs_comb_kernel<T>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(cmb)));
