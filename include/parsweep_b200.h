@@ -93,7 +93,7 @@ typedef struct psw_plan_info_t {
     double setup_seconds;   /* host time of the preliminary phase */
     double max_z_norm;      /* PreliminaryData::max_z_norm (preliminary.hpp:75-83) */
     int32_t strategy_used;  /* psw_grow_strategy: PreliminaryData::strategy_used (:65) */
-    int32_t reserved;
+    int32_t device_setup;   /* 1 if the preliminary's boundary sweeps ran on the GPU (psw_prelim.cu) */
 } psw_plan_info_t;
 
 /* ---- errors ------------------------------------------------------------ */

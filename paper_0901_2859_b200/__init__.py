@@ -297,7 +297,7 @@ class _Info(C.Structure):
                 ("uniform", C.c_int32), ("fused_ok", C.c_int32), ("device_bytes", C.c_int64),
                 ("combine_terms", C.c_int64), ("comm_rounds", C.c_int64),
                 ("setup_seconds", C.c_double), ("max_z_norm", C.c_double),
-                ("strategy_used", C.c_int32), ("reserved", C.c_int32)]
+                ("strategy_used", C.c_int32), ("device_setup", C.c_int32)]
 
 
 class _Opts(C.Structure):

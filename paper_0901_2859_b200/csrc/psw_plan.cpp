@@ -370,6 +370,20 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
                int strategy = PSW_GROW_AUTO);
 
 int build_shard_tables(psw_plan* pl, const std::vector<double>& cmat);  // psw_shard.cu
+int device_preliminary(int64_t n, const double* sub, const double* diag, const double* sup,
+                       int64_t p, const int64_t* bnd, const std::vector<int32_t>& blk,
+                       std::vector<double>& gr, std::vector<double>& gl, std::vector<double>& zr,
+                       std::vector<double>& zl, double& max_z, int64_t& bad_row);  // psw_prelim.cu
+
+// Where the DirectSymmetric preliminary runs: PSW_DEVICE_SETUP=1 moves the
+// 3p boundary sweeps to the GPU (psw_prelim.cu, bitwise the host setup). The
+// default is the host: the sweeps are single-thread recurrences through an
+// IEEE division per row, and on B200 they run slower than the host's worker
+// threads (C3: 3.3 s vs 0.3 s; tests/test_prelim_gpu.py).
+static bool want_device_setup(int64_t n, int64_t p) {
+    const char* e = std::getenv("PSW_DEVICE_SETUP");
+    return p > 0 && n > 0 && e && std::atoi(e) != 0;
+}
 
 int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
                const double* sup, int64_t p, const int64_t* bnd, int dtype, int device,
@@ -443,6 +457,33 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
             delete pl;
             return PSW_PIVOT_BREAKDOWN;
         }
+    } else if (grow.strategy == PSW_GROW_DIRECT_SYMMETRIC && want_device_setup(n, p)) {
+        // the 3p sweeps on the GPU, bitwise the host restatement (psw_prelim.cu)
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0 || device < 0 || device >= ndev) {
+            set_error(PSW_CUDA_ERROR, "no CUDA device for the device preliminary (no CPU fallback)");
+            delete pl;
+            return PSW_CUDA_ERROR;
+        }
+        int prev_dev = 0;
+        cudaGetDevice(&prev_dev);
+        cudaSetDevice(device);
+        int64_t bad = -1;
+        const int rc = device_preliminary(n, sub, diag, sup, p, bnd, pl->blk, gr, gl, zr, zl, max_z,
+                                          bad);
+        cudaSetDevice(prev_dev);
+        if (rc == PSW_PIVOT_BREAKDOWN) {
+            set_error(PSW_PIVOT_BREAKDOWN,
+                      "pivot breakdown during forward elimination at row " + std::to_string(bad),
+                      bad);
+            delete pl;
+            return PSW_PIVOT_BREAKDOWN;
+        }
+        if (rc != PSW_OK) {
+            delete pl;
+            return rc;
+        }
+        pl->info.device_setup = 1;
     } else {
         // boundaries are independent items (preliminary.hpp:182-195); errors
         // are reported in the serial executor's order (boundary, then g,

@@ -409,6 +409,16 @@ size_t combine_smem(int64_t P) {
     return b;
 }
 
+// beyond 48 KB of dynamic shared memory (P in 37..40 with staged tables)
+// the kernel must opt in
+int combine_prepare(int64_t P) {
+    const size_t b = combine_smem(P);
+    if (b > 48 * 1024)
+        PSW_CUDA_TRY(cudaFuncSetAttribute(combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(b)));
+    return PSW_OK;
+}
+
 template <typename T>
 int launch_staged(const psw_plan* pl, const void* Fv, int64_t ldf, void* Xv, int64_t ldx,
                   int64_t N, int layout, cudaStream_t s, double* bl, double* br, double* V,
@@ -426,6 +436,7 @@ int launch_staged(const psw_plan* pl, const void* Fv, int64_t ldf, void* Xv, int
         ++launches;
         mark(ev, nev, 1, s);
         if (p > 0) {
+            if (int rc = combine_prepare(pl->P)) return rc;
             combine_kernel<<<unsigned((N + kCombineThreads - 1) / kCombineThreads), kCombineThreads,
                              combine_smem(pl->P), s>>>(bl, br, N, p, pl->d_items, pl->d_zr, pl->d_zl, V);
             ++launches;
@@ -446,6 +457,7 @@ int launch_staged(const psw_plan* pl, const void* Fv, int64_t ldf, void* Xv, int
         ++launches;
         mark(ev, nev, 1, s);
         if (p > 0) {
+            if (int rc = combine_prepare(pl->P)) return rc;
             combine_kernel<<<unsigned((N + kCombineThreads - 1) / kCombineThreads), kCombineThreads,
                              combine_smem(pl->P), s>>>(
                 bl, br, N, p, pl->d_items, pl->d_zr, pl->d_zl, V);
@@ -467,6 +479,7 @@ int launch_combine(const psw_plan* pl, const double* bl, const double* br, int64
                    cudaStream_t s) {
     const int p = int(pl->p);
     if (p <= 0) return PSW_OK;
+    if (int rc = combine_prepare(pl->P)) return rc;
     combine_kernel<<<unsigned((N + kCombineThreads - 1) / kCombineThreads), kCombineThreads,
                      combine_smem(pl->P), s>>>(bl, br, N, p, pl->d_items, pl->d_zr, pl->d_zl, V);
     PSW_CUDA_TRY(cudaGetLastError());
