@@ -64,7 +64,7 @@ typedef enum psw_layout { PSW_LAYOUT_R = 0, PSW_LAYOUT_S = 1 } psw_layout;
  * chip and read F once (layout R, uniform partitions whose blocks fit a
  * cluster; CLUSTER: one CTA per SM holding G blocks, FUSED: 16-CTA clusters);
  * RESWEEP reads F twice and writes X once with per-segment checkpoints
- * (fp64 layout R, P <= 64, e.g. the 2^20-row config); STAGED is the general
+ * (either layout, e.g. the 2^20-row and fp32 configs); STAGED is the general
  * three-kernel path (and the only one returning betas/boundary values). */
 typedef enum psw_path {
     PSW_PATH_AUTO = 0,

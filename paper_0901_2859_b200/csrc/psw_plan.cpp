@@ -897,11 +897,12 @@ int psw_solve_ex(const psw_plan* plan, const void* F, int64_t ldf, void* X, int6
         t_last_path = PSW_PATH_FUSED;
         rc = psw::solve_fused(plan, F, ldf, X, ldx, nrhs, layout, s, opts ? opts->events : nullptr,
                               opts ? opts->nevents : 0);
-    } else if (path == PSW_PATH_AUTO && !want_intermediates && plan->P <= 64 &&
+    } else if (path == PSW_PATH_AUTO && !want_intermediates &&
                psw::resweep_supported(plan, layout, nrhs)) {
         // beyond the CLUSTER/FUSED paths' reach (large blocks, layout S): 3 s
         // bytes per unknown instead of STAGED's 4 s (measured C3 4.6 vs 6.3 ms,
-        // C4 rows 136 vs 195 us, C2 fp32 11.9 vs 13.3 ms)
+        // C4 rows 126 vs 195 us, C2 fp32 at P = 8..512: 11.1-13.1 vs 12.8-13.9 ms,
+        // profiles/r01_c2_partition_sweep.txt)
         t_last_path = PSW_PATH_RESWEEP;
         rc = psw::solve_resweep(plan, F, ldf, X, ldx, nrhs, layout, s,
                                 opts ? opts->events : nullptr, opts ? opts->nevents : 0);
