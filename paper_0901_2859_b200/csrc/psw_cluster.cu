@@ -425,19 +425,10 @@ CChoice choose_t(const psw_plan* pl) {
     return ch;
 }
 
-// One 128-byte slab by default. PSW_CLUSTER_SLABS=2: two 64-byte slabs
-// (the next unit streams in during the whole current one; measured slower
-// on C1, 129 vs 89 us: the per-unit time is set by the scan / exchange /
-// back-substitution latency chain, not by the slab's arrival).
+// One 128-byte slab per CTA. (A two-slab variant with 64-byte rows, so the
+// next unit streams in during the whole current one, measured slower on C1 —
+// 129 vs 89 us before the segment fix — and was removed.)
 CChoice choose(const psw_plan* pl) {
-    static const int nslab = [] {
-        const char* e = std::getenv("PSW_CLUSTER_SLABS");
-        return e && std::atoi(e) == 2 ? 2 : 1;
-    }();
-    if (nslab == 2) {
-        CChoice ch = pl->dtype == PSW_F64 ? choose_t<double, 8, 2>(pl) : choose_t<float, 16, 2>(pl);
-        if (ch.G) return ch;
-    }
     return pl->dtype == PSW_F64 ? choose_t<double, 16, 1>(pl) : choose_t<float, 32, 1>(pl);
 }
 
@@ -696,9 +687,6 @@ int solve_cluster(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64
         return PSW_NOT_SUPPORTED;
     }
     const CChoice ch = choose(pl);
-    if (ch.nslab == 2)
-        return pl->dtype == PSW_F64 ? launch<double, 8, 2>(pl, ch, F, ldf, X, ldx, N, s, ev, nev)
-                                    : launch<float, 16, 2>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
     return pl->dtype == PSW_F64 ? launch<double, 16, 1>(pl, ch, F, ldf, X, ldx, N, s, ev, nev)
                                 : launch<float, 32, 1>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
 }
