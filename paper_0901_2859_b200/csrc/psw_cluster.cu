@@ -46,7 +46,8 @@ namespace psw {
 namespace {
 
 constexpr int kMaxThreads = 512;
-constexpr int kMaxC = 8;                    // portable cluster size
+constexpr int kMaxC = 16;                   // cluster size (> 8 needs the non-portable opt-in)
+constexpr size_t kSmemTwoPerSm = 115712 - 512;  // two CTAs per SM (228 KB, 1 KB reserved each)
 constexpr size_t kSmemMax = 232448;         // 227 KB per CTA (sm_100)
 constexpr int kSegMax = kSegLen + 1;
 constexpr int kMaxBox = 256;                // TMA box height limit
@@ -105,7 +106,9 @@ struct CLayout {
         slab_b = up(size_t(ra) * W * sizeof(T));
         coef = NSLAB * slab_b;
         seg = up(coef + coff<T>(ra) + 16);
-        allx = up(seg + size_t(4) * nth * sizeof(double));
+        // sd, sx per thread; the beta partials per pair of segments when a warp
+        // holds two segments of one block (W = 16), else per thread
+        allx = up(seg + size_t(W == 16 ? 3 : 4) * nth * sizeof(double));
         vals = up(allx + size_t(2) * P * W * 2 * sizeof(double));
         cm = up(vals + size_t(G + 1) * W * sizeof(double));
         segc = up(cm + size_t(G + 1) * 2 * P * sizeof(double));
@@ -139,8 +142,17 @@ __device__ __forceinline__ void fwd(const T* slab, const unsigned char* co, int 
     }
     sd[tid] = double(d);
     sx[tid] = double(lx);
-    sr[tid] = br;
-    sl[tid] = bl;
+    if constexpr (W == 16) {  // lanes 16..31 sweep the next segment of the same block
+        br += __shfl_down_sync(0xffffffffu, br, 16);
+        bl += __shfl_down_sync(0xffffffffu, bl, 16);
+        if ((tid & 31) < 16) {
+            sr[(tid >> 5) * 16 + (tid & 15)] = br;
+            sl[(tid >> 5) * 16 + (tid & 15)] = bl;
+        }
+    } else {
+        sr[tid] = br;
+        sl[tid] = bl;
+    }
 }
 
 // back substitution of one segment from the exact carries, last row first
@@ -193,8 +205,8 @@ __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
     unsigned char* co = smem + L.coef;  // coefficient rows (coff)
     double* sd = reinterpret_cast<double*>(smem + L.seg);  // d~ end -> carry D
     double* sx = sd + nth;                                 // Lam~ -> Lam~ + D K1
-    double* sr = sx + nth;                                 // right partial -> x_b
-    double* sl = sr + nth;                                 // left partial
+    double* sr = sx + nth;                                 // right partials
+    double* sl = sr + (W == 16 ? nth / 2 : nth);           // left partials
     double* allx = reinterpret_cast<double*>(smem + L.allx);  // [2][P][W][R, L]
     double* vals = reinterpret_cast<double*>(smem + L.vals);  // [G + 1][W]
     double* cm = reinterpret_cast<double*>(smem + L.cm);      // [G + 1][2P]
@@ -304,8 +316,12 @@ __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
                 const double dend = sd[id];
                 sd[id] = D;
                 sx[id] = fma(D, sc.k1, sx[id]);
-                R += sr[id];
-                Lb += sl[id];
+                // the beta partials of segment pairs (W = 16) or segments
+                if (W != 16 || (q & 1) == 0) {
+                    const int bid = W == 16 ? ((j * S + q) >> 1) * 16 + lane : id;
+                    R += sr[bid];
+                    Lb += sl[bid];
+                }
                 D = fma(sc.mu_end, D, dend);
             }
             stamp(k, 7);
@@ -369,7 +385,7 @@ __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
                 const int id = (j * S + q) * W + lane;
                 const SegCoef sc = segc[j * S + q];
                 const double A = sx[id];
-                sr[id] = xb;
+                sx[id] = xb;  // sx: Lam~ + D K1 -> x_b
                 xb = fma(sc.nu, xb, fma(xl, sc.k2, A));
             }
         }
@@ -378,7 +394,7 @@ __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
         // ---- back substitution from the exact carries, X streamed out
         const int64_t kk = unit(k) * W + lane;
         const T D = T(sd[tid]), xlt = T(xl);
-        T xn = T(sr[tid]);
+        T xn = T(sx[tid]);
         if (kk < g.N) {
             T* xp = X + int64_t(sgd.a) * g.ldx + kk;
             bwd<T, kSegMax, false>(co, a, len, dr, D, xlt, xn, xp, g.ldx);
@@ -402,25 +418,31 @@ CChoice choose_t(const psw_plan* pl) {
     if (!pl->uniform || pl->world != 1 || !pl->d_ffwd || !pl->d_cmat || pl->nseg <= 0) return ch;
     const int P = int(pl->P), m = int(pl->m), S = pl->nseg;
     if (S * kSegLen < m - 1 || S * kSegLen > m + kSegLen || m % 32) return ch;
+    if (W == 16 && S % 2) return ch;  // a warp's two segments must share a block
     static const int force_g = [] {
         const char* e = std::getenv("PSW_CLUSTER_G");  // tuning override
         return e ? std::atoi(e) : 0;
     }();
-    for (int G = P; G >= 1; --G) {  // fewest CTAs per tile first
-        if (P % G) continue;
-        const int C = P / G;
-        if (C > kMaxC) break;
-        if (force_g > 0 && G != force_g) continue;
-        const int nth = G * S * W;
-        if (nth > kMaxThreads / NSLAB || nth % 32) continue;
-        const size_t smem = CLayout<T, W, NSLAB>(G, m, S, P, nth).total;
-        if (smem > kSmemMax) continue;
-        ch.nslab = NSLAB;
-        ch.W = W;
-        ch.G = G;
-        ch.C = C;
-        ch.smem = smem;
-        return ch;
+    // Two CTAs per SM when a CTA fits half the shared memory (two independent
+    // tile chains per SM; C1: G = 2, C = 8 -> 63.9 us vs G = 4, C = 4 -> 68.1
+    // us), else one; within each, the fewest CTAs per tile first.
+    for (int pass = 0; pass < 2 && ch.G == 0; ++pass) {
+        for (int G = P; G >= 1; --G) {
+            if (P % G) continue;
+            const int C = P / G;
+            if (C > kMaxC) break;
+            if (force_g > 0 && G != force_g) continue;
+            const int nth = G * S * W;
+            if (nth > kMaxThreads / NSLAB || nth % 32) continue;
+            const size_t smem = CLayout<T, W, NSLAB>(G, m, S, P, nth).total;
+            if (smem > (pass == 0 && force_g == 0 ? kSmemTwoPerSm : kSmemMax)) continue;
+            ch.nslab = NSLAB;
+            ch.W = W;
+            ch.G = G;
+            ch.C = C;
+            ch.smem = smem;
+            break;
+        }
     }
     return ch;
 }
@@ -542,6 +564,8 @@ int launch(const psw_plan* pl, const CChoice& ch, const void* F, int64_t ldf, vo
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (ch.C > 8)
+        PSW_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     static std::mutex mu;
     static std::vector<std::pair<std::array<int64_t, 5>, int>> cache;
     const std::array<int64_t, 5> key = {int64_t(sizeof(T)) + 16 * NSLAB, ch.G, ch.C, int64_t(ch.smem), pl->device};
