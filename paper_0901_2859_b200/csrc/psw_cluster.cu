@@ -52,6 +52,10 @@ constexpr size_t kSmemMax = 232448;         // 227 KB per CTA (sm_100)
 constexpr int kSegMax = kSegLen + 1;
 constexpr int kMaxBox = 256;                // TMA box height limit
 
+__device__ __forceinline__ void bar_arrive(int id, int nthreads) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 __device__ __forceinline__ void bar_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -96,14 +100,16 @@ __host__ __device__ __forceinline__ size_t coff(int q) {
 }
 
 // Shared-memory carve-up (bytes), identical on host and device.
-template <typename T, int W, int NSLAB>
+template <typename T, int W, int NSLAB, bool LS = false>
 struct CLayout {
     int ra;
     size_t slab_b, coef, seg, allx, vals, cm, segc, bars, total;
     __host__ __device__ CLayout(int G, int m, int S, int P, int nth) {
         auto up = [](size_t x) { return (x + 127) & ~size_t(127); };
         ra = G * m + 1;               // slab rows of the last CTA
-        slab_b = up(size_t(ra) * W * sizeof(T));
+        // layout S: G*m/16 swizzled 16-row boxes (1024-aligned) + a 2-row tail
+        slab_b = LS ? up(size_t(G * m) * W * sizeof(T) + size_t(2) * W * sizeof(T))
+                    : up(size_t(ra) * W * sizeof(T));
         coef = NSLAB * slab_b;
         seg = up(coef + coff<T>(ra) + 16);
         // sd, sx per thread; the beta partials per pair of segments when a warp
@@ -119,10 +125,63 @@ struct CLayout {
 
 // forward rows of one segment from a zero carry: d~ into dr, partials to
 // the thread's slots (betas.hpp:42-57 split by segment; Lam~, psw_internal.h)
-template <typename T, int W, int NMAX, bool EXACT = (NMAX <= kSegLen)>
+// Layout S slab (fp64, W = 16): 16-row TMA boxes with the 128-byte swizzle,
+// box c = rows 16c..16c+15 of all W right-hand sides, rhs l's rows in the
+// 128-byte line l of the box, 16-byte chunk (q/2) XOR (l mod 8).
+template <typename T, int W>
+__device__ __forceinline__ int s_index(int q, int l) {
+    return ((q >> 4) * W + l) * 16 + ((((q & 15) >> 1) ^ (l & 7)) << 1) + (q & 1);
+}
+
+__device__ __forceinline__ void st_v4(double* p, double a, double b, double c, double d) {
+    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+                 : "memory");
+}
+
+__device__ __forceinline__ void st_v2(double* p, double a, double b) {
+    asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
+
+// Layout S backward (fp64): a right-hand side's rows are contiguous, so each
+// thread writes its segment as whole 32-byte sectors (256-bit stores) once
+// the segment is solved; AL = the segment's first global row mod 4 (0 for
+// the first block's segments, 3 for the others: blocks start at t*m - 1).
+// Rows 31, 32 exist when len > 31, > 32.
+template <int AL>
+__device__ __forceinline__ void bwd_v4(const unsigned char* co, int a, int len,
+                                       double (&dr)[kSegMax], double D, double xl, double xn,
+                                       double* xp) {
+#pragma unroll
+    for (int r = kSegMax - 1; r >= 0; --r) {
+        if (r < kSegLen - 1 || r < len) {
+            const Quad<double> c1 = reinterpret_cast<const Quad<double>*>(co + coff<double>(a + r))[1];
+            xn = fma(c1.w, xn, fma(xl, c1.z, fma(c1.y, D, dr[r])));
+            dr[r] = xn;
+        }
+    }
+    constexpr int r0 = AL == 0 ? 0 : 4 - AL;  // first 32-byte aligned row
+    if constexpr (AL == 3) __stcs(xp, dr[0]);
+    // full groups inside rows 0..30
+#pragma unroll
+    for (int r = r0; r + 4 <= kSegLen - 1; r += 4) st_v4(xp + r, dr[r], dr[r + 1], dr[r + 2], dr[r + 3]);
+    // the last group starts at rt and runs to len
+    constexpr int rt = r0 + ((kSegLen - 1 - r0) / 4) * 4;
+    const int nt = len - rt;  // 1..5
+    if (nt >= 4) {
+        st_v4(xp + rt, dr[rt], dr[rt + 1], dr[rt + 2], dr[rt + 3]);
+        if constexpr (rt + 4 < kSegMax)
+            if (nt == 5) __stcs(xp + rt + 4, dr[rt + 4]);
+    } else {
+        if (nt >= 2) st_v2(xp + rt, dr[rt], dr[rt + 1]);
+        if (nt == 1) __stcs(xp + rt, dr[rt]);
+        if (nt == 3) __stcs(xp + rt + 2, dr[rt + 2]);
+    }
+}
+
+template <typename T, int W, int NMAX, bool EXACT = (NMAX <= kSegLen), bool LS = false>
 __device__ __forceinline__ void fwd(const T* slab, const unsigned char* co, int a, int lane,
                                     int len, T (&dr)[kSegMax], double* sd, double* sx, double* sr,
-                                    double* sl, int tid) {
+                                    double* sl, int tid, int gm = 0) {
     const T* col = slab + size_t(a) * W + lane;
     T d = T(0), lx = T(0);
     double br = 0.0, bl = 0.0;
@@ -132,7 +191,14 @@ __device__ __forceinline__ void fwd(const T* slab, const unsigned char* co, int 
             const Quad<T>* c = reinterpret_cast<const Quad<T>*>(co + coff<T>(a + r));
             const Quad<T> c0 = c[0];
             const T lam = c[1].x;
-            const T f = col[r * W];
+            T f;
+            if constexpr (LS) {  // physical row a + r + 1; rows >= gm in the tail box
+                const int q = a + r + 1;
+                f = (r >= kSegLen - 1 && q >= gm) ? slab[gm * W + lane * 2 + (q - gm)]
+                                                  : slab[s_index<T, W>(q, lane)];
+            } else {
+                f = col[r * W];
+            }
             d = fma(c0.y, d, f * c0.x);
             br = fma(double(f), double(c0.z), br);
             bl = fma(double(f), double(c0.w), bl);
@@ -169,13 +235,13 @@ __device__ __forceinline__ void bwd(const unsigned char* co, int a, int len,
     }
 }
 
-template <typename T, int W, int NSLAB>
+template <typename T, int W, int NSLAB, bool LS = false, bool V4 = false>
 __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
     const __grid_constant__ CUtensorMap tmF, const __grid_constant__ CUtensorMap tmF1,
     const __grid_constant__ CUtensorMap tmF2, const T* F, int64_t ldf, T* X, CGeom g, const FusedFwd<T>* __restrict__ gff, const FusedBwd<T>* __restrict__ gfb,
     const SegCoef* __restrict__ gsegc, const SegDesc* __restrict__ gdesc,
     const double* __restrict__ gcmat, const unsigned char* __restrict__ gtab, int64_t tab_stride) {
-    extern __shared__ __align__(128) unsigned char smem[];
+    extern __shared__ __align__(1024) unsigned char smem[];
     cg::cluster_group cluster = cg::this_cluster();
     auto etrace = [&](int slot) {
         if (g.trace && threadIdx.x == 0 && blockIdx.x < 1024) {
@@ -196,7 +262,7 @@ __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
     auto unit = [&](int64_t k) { return (cid + (k / NSLAB) * ncl) * NSLAB + (k % NSLAB); };
     const int nth = G * S * W;
     const int tid = threadIdx.x;
-    const CLayout<T, W, NSLAB> L(G, m, S, P, nth);
+    const CLayout<T, W, NSLAB, LS> L(G, m, S, P, nth);
     // slab row 0 is global row crank*G*m - 1 (row -1 of CTA 0 is outside F:
     // TMA zero-fills it)
     const int base = crank * G * m - 1;
@@ -231,6 +297,20 @@ __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
         T* slab = slab_of(k);
         uint64_t* bar = &bars_of(k)[jb];
         const bool extra = last_cta && jb == G - 1;
+        if constexpr (LS) {
+            // the whole slab on the first barrier (boxes straddle blocks): G*m/16
+            // boxes of 16 rows from global row base - 1 (even, so every box
+            // starts on 16 bytes: TMA rejects an odd fp64 row) and a 2-row tail
+            // box (tmF1, unswizzled); physical slab row = slab row + 1; row -2
+            // of CTA 0 and rows past n are zero-filled
+            if (jb != 0) return;
+            const int nb = G * m / 16;
+            mbar_expect_tx(bar, uint32_t((nb * 16 + 2) * W * sizeof(T)));
+            for (int c = 0; c < nb; ++c)
+                tma_load_2d(slab + size_t(c) * 16 * W, &tmF, base - 1 + 16 * c, k0, bar);
+            tma_load_2d(slab + size_t(nb) * 16 * W, &tmF1, base - 1 + 16 * nb, k0, bar);
+            return;
+        }
         if (crank == 0 && jb == 0) {
             // global rows [0, m - 1) into slab rows [1, m): no box reaches row -1
             // (a box partly outside F is slow to complete)
@@ -290,20 +370,32 @@ __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
         stamp(k, 0);
         if (tid == 0) mbar_expect_tx(&xbar[buf], uint32_t(P * W * 2 * sizeof(double)));
         T* slab = slab_of(k);
-        mbar_wait(&bars_of(k)[j], uint32_t((k / NSLAB) & 1));
+        mbar_wait(&bars_of(k)[LS ? 0 : j], uint32_t((k / NSLAB) & 1));
         stamp(k, 1);
         // ---- forward sweep of the segment, d~ in registers
         // one instruction stream for every lane: segments are 31, 32 or 33 rows
         // (m % 32 == 0), and the two segments a warp sweeps may differ in length;
         // rows 0..30 unpredicated, the last two under a predicate
-        fwd<T, W, kSegMax, false>(slab, co, a, lane, len, dr, sd, sx, sr, sl, tid);
+        fwd<T, W, kSegMax, false, LS>(slab, co, a, lane, len, dr, sd, sx, sr, sl, tid, G * m);
         bar_sync(2 + j, S * W);  // the block's rows swept, its partials visible
         if (g.trace > 2 && tid == 0) {  // force the deferred barrier wait before the stamp
             volatile double* vs = sd;
             if (vs[nth - 1] == 1.2345e300) sd[0] = 0.0;
         }
         stamp(k, 2);
-        if (block_issuer && k + NSLAB < ntl) {
+        if constexpr (LS) {  // the last warp refills once every block has swept
+            if (k + NSLAB < ntl) {
+                if (tid >= nth - 32) {  // bar.sync/arrive count whole warps
+                    bar_sync(15, nth);
+                    if (tid == nth - 1) {
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        issue_block(k + NSLAB, 0);
+                    }
+                } else {
+                    bar_arrive(15, nth);
+                }
+            }
+        } else if (block_issuer && k + NSLAB < ntl) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             issue_block(k + NSLAB, j);
         }
@@ -395,9 +487,25 @@ __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
         const int64_t kk = unit(k) * W + lane;
         const T D = T(sd[tid]), xlt = T(xl);
         T xn = T(sx[tid]);
-        if (kk < g.N) {
-            T* xp = X + int64_t(sgd.a) * g.ldx + kk;
-            bwd<T, kSegMax, false>(co, a, len, dr, D, xlt, xn, xp, g.ldx);
+        if constexpr (LS) {
+            // layout S: the rhs' rows are contiguous; 32-byte stores when X and
+            // its pitch are 32-byte aligned (V4; segments start at rows = 0 or 3
+            // mod 4, choose_t). One store variant per instantiation: a third
+            // one drives ptxas to 64 registers and 0.8 KB of spills (171 vs
+            // 110 us on C4).
+            if (kk < g.N) {
+                if constexpr (V4) {
+                    double* xp = reinterpret_cast<double*>(X) + kk * g.ldx + sgd.a;
+                    if ((sgd.a & 3) == 0)
+                        bwd_v4<0>(co, a, len, dr, D, xlt, xn, xp);
+                    else
+                        bwd_v4<3>(co, a, len, dr, D, xlt, xn, xp);
+                } else {
+                    bwd<T, kSegMax, false>(co, a, len, dr, D, xlt, xn, X + kk * g.ldx + sgd.a, 1);
+                }
+            }
+        } else if (kk < g.N) {
+            bwd<T, kSegMax, false>(co, a, len, dr, D, xlt, xn, X + int64_t(sgd.a) * g.ldx + kk, g.ldx);
         }
         stamp(k, 6);
         if (k == 0) etrace(2);
@@ -412,7 +520,7 @@ struct CChoice {
     size_t smem = 0;
 };
 
-template <typename T, int W, int NSLAB>
+template <typename T, int W, int NSLAB, bool LS = false>
 CChoice choose_t(const psw_plan* pl) {
     CChoice ch;
     if (!pl->uniform || pl->world != 1 || !pl->d_ffwd || !pl->d_cmat || pl->nseg <= 0) return ch;
@@ -434,7 +542,7 @@ CChoice choose_t(const psw_plan* pl) {
             if (force_g > 0 && G != force_g) continue;
             const int nth = G * S * W;
             if (nth > kMaxThreads / NSLAB || nth % 32) continue;
-            const size_t smem = CLayout<T, W, NSLAB>(G, m, S, P, nth).total;
+            const size_t smem = CLayout<T, W, NSLAB, LS>(G, m, S, P, nth).total;
             if (smem > (pass == 0 && force_g == 0 ? kSmemTwoPerSm : kSmemMax)) continue;
             ch.nslab = NSLAB;
             ch.W = W;
@@ -450,7 +558,9 @@ CChoice choose_t(const psw_plan* pl) {
 // One 128-byte slab per CTA. (A two-slab variant with 64-byte rows, so the
 // next unit streams in during the whole current one, measured slower on C1 —
 // 129 vs 89 us before the segment fix — and was removed.)
-CChoice choose(const psw_plan* pl) {
+CChoice choose(const psw_plan* pl, int layout = PSW_LAYOUT_R) {
+    if (layout == PSW_LAYOUT_S)  // fp64 only: 16 rows = one 128-byte swizzle line
+        return pl->dtype == PSW_F64 ? choose_t<double, 16, 1, true>(pl) : CChoice{};
     return pl->dtype == PSW_F64 ? choose_t<double, 16, 1>(pl) : choose_t<float, 32, 1>(pl);
 }
 
@@ -458,6 +568,35 @@ int box_height(int m) {
     for (int h = kMaxBox; h >= 32; h /= 2)
         if (m % h == 0) return h;
     return 32;
+}
+
+// layout S: rows are the contiguous dimension; 16-row boxes of W right-hand
+// sides with the 128-byte swizzle (s_index)
+bool encode_s(CUtensorMap* tm, CUtensorMap* tm1, const void* F, int64_t N, int64_t n, int64_t ldf,
+              int es, int W, int tail) {
+    auto enc = tensor_map_encoder();
+    if (!enc) {
+        set_error(PSW_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+        return false;
+    }
+    const cuuint64_t dims[2] = {cuuint64_t(n), cuuint64_t(N)};
+    const cuuint64_t strides[1] = {cuuint64_t(ldf) * cuuint64_t(es)};
+    const cuuint32_t box[2] = {cuuint32_t(128 / es), cuuint32_t(W)};
+    const cuuint32_t estr[2] = {1, 1};
+    const auto dt = es == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    const cuuint32_t box1[2] = {cuuint32_t(tail), cuuint32_t(W)};  // the tail rows, unswizzled
+    CUresult r = enc(tm, dt, 2, const_cast<void*>(F), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS)
+        r = enc(tm1, dt, 2, const_cast<void*>(F), dims, strides, box1, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error(PSW_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+        return false;
+    }
+    return true;
 }
 
 bool encode(CUtensorMap* tm, CUtensorMap* tm1, CUtensorMap* tm2, const void* F, int64_t N,
@@ -531,13 +670,19 @@ int cluster_tables(const psw_plan* pl, const CChoice& ch) {
     return PSW_OK;
 }
 
-template <typename T, int W, int NSLAB>
+template <typename T, int W, int NSLAB, bool LS = false, bool V4 = false>
 int launch(const psw_plan* pl, const CChoice& ch, const void* F, int64_t ldf, void* X, int64_t ldx,
            int64_t N, cudaStream_t s, void** ev, int nev) {
     if (int rc = cluster_tables<T>(pl, ch)) return rc;
     CUtensorMap tm, tm1, tm2;
     const int H = box_height(int(pl->m));
-    if (!encode(&tm, &tm1, &tm2, F, N, pl->n, ldf, int(sizeof(T)), W, H)) return PSW_CUDA_ERROR;
+    if (LS) {
+        // F: 16-row swizzled boxes + the 2-row tail
+        if (!encode_s(&tm, &tm1, F, N, pl->n, ldf, int(sizeof(T)), W, 2)) return PSW_CUDA_ERROR;
+        tm2 = tm;
+    } else if (!encode(&tm, &tm1, &tm2, F, N, pl->n, ldf, int(sizeof(T)), W, H)) {
+        return PSW_CUDA_ERROR;
+    }
     CGeom g;
     g.n = int(pl->n);
     g.P = int(pl->P);
@@ -551,7 +696,7 @@ int launch(const psw_plan* pl, const CChoice& ch, const void* F, int64_t ldf, vo
     g.N = N;
     g.ldx = ldx;
     g.ntiles = (N + W - 1) / W;
-    auto kern = cluster_kernel<T, W, NSLAB>;
+    auto kern = cluster_kernel<T, W, NSLAB, LS, V4>;
     PSW_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ch.smem)));
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(unsigned(ch.G * g.S * W), 1, 1);
@@ -568,7 +713,8 @@ int launch(const psw_plan* pl, const CChoice& ch, const void* F, int64_t ldf, vo
         PSW_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     static std::mutex mu;
     static std::vector<std::pair<std::array<int64_t, 5>, int>> cache;
-    const std::array<int64_t, 5> key = {int64_t(sizeof(T)) + 16 * NSLAB, ch.G, ch.C, int64_t(ch.smem), pl->device};
+    const std::array<int64_t, 5> key = {int64_t(sizeof(T)) + 16 * NSLAB + 64 * int64_t(LS) + 128 * int64_t(V4), ch.G, ch.C,
+                                        int64_t(ch.smem), pl->device};
     int maxc = 0;
     {
         std::lock_guard<std::mutex> lk(mu);
@@ -696,21 +842,26 @@ int launch(const psw_plan* pl, const CChoice& ch, const void* F, int64_t ldf, vo
 }  // namespace
 
 bool cluster_supported(const psw_plan* pl, int layout, int64_t N, const void* F, int64_t ldf) {
-    if (layout != PSW_LAYOUT_R || N < 1 || N > (int64_t{1} << 31)) return false;
+    if ((layout != PSW_LAYOUT_R && layout != PSW_LAYOUT_S) || N < 1 || N > (int64_t{1} << 31))
+        return false;
     const int es = pl->dtype == PSW_F64 ? 8 : 4;
     if ((reinterpret_cast<uintptr_t>(F) & 15) || ((size_t(ldf) * es) & 15)) return false;
-    return choose(pl).G > 0;
+    return choose(pl, layout).G > 0;
 }
 
 int solve_cluster(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_t ldx, int64_t N,
                   int layout, cudaStream_t s, void** ev, int nev) {
     if (!cluster_supported(pl, layout, N, F, ldf)) {
         set_error(PSW_NOT_SUPPORTED,
-                  "cluster path needs layout R, a uniform partition whose blocks fit a "
-                  "cluster, and 16-byte aligned F / row pitch");
+                  "cluster path needs a uniform partition whose blocks fit a cluster, 16-byte "
+                  "aligned F / row pitch, and fp64 for layout S");
         return PSW_NOT_SUPPORTED;
     }
-    const CChoice ch = choose(pl);
+    const CChoice ch = choose(pl, layout);
+    if (layout == PSW_LAYOUT_S)
+        return (reinterpret_cast<uintptr_t>(X) & 31) || ((size_t(ldx) * sizeof(double)) & 31)
+                   ? launch<double, 16, 1, true, false>(pl, ch, F, ldf, X, ldx, N, s, ev, nev)
+                   : launch<double, 16, 1, true, true>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
     return pl->dtype == PSW_F64 ? launch<double, 16, 1>(pl, ch, F, ldf, X, ldx, N, s, ev, nev)
                                 : launch<float, 32, 1>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
 }

@@ -96,3 +96,24 @@ def test_cluster_shapes(psw, cuda, n, P, dtype):
     X = gpu_solve(psw, cuda, plan, F, 0, path=psw.PATH_CLUSTER)
     tol = 1e-12 if dtype == 0 else 1e-5
     assert rel_l2(X, ref) <= tol, rel_l2(X, ref)
+
+
+@pytest.mark.parametrize("N", [2, 16, 18, 100, 1000])
+def test_cluster_layout_s(psw, cuda, N):
+    """Layout S (fp64): 16-row swizzled TMA boxes of 16 right-hand sides."""
+    g = load_golden("c1_n4096_P16")
+    plan = plan_for(psw, g)
+    F = np.random.default_rng(N + 7).standard_normal((N, 4096))
+    ref = gpu_solve(psw, cuda, plan, F, 1, path=psw.PATH_STAGED)
+    X = gpu_solve(psw, cuda, plan, F, 1, path=psw.PATH_CLUSTER)
+    X2 = gpu_solve(psw, cuda, plan, F, 1, path=psw.PATH_CLUSTER, inplace=False, pad=2)
+    assert rel_l2(X, ref) <= 1e-12, rel_l2(X, ref)
+    assert np.array_equal(X, X2)
+
+
+@pytest.mark.parametrize("name", ["c0_n1024_P4", "c1_n4096_P16", "c4_n4096_P16"])
+def test_cluster_layout_s_golden(psw, cuda, name):
+    g = load_golden(name)
+    plan = plan_for(psw, g)
+    X = gpu_solve(psw, cuda, plan, g["F"], 1, path=psw.PATH_CLUSTER)
+    assert rel_l2(X, g["X"]) <= FP64_TOL, rel_l2(X, g["X"])
