@@ -540,6 +540,10 @@ CChoice choose_t(const psw_plan* pl) {
             const int C = P / G;
             if (C > kMaxC) break;
             if (force_g > 0 && G != force_g) continue;
+            // layout S with one block per CTA (G = 1, C = 16) gives wrong rows from
+            // the second segment on (C1 matrix, a single unit; G = 2 is exact on
+            // every test): excluded until understood
+            if (LS && G == 1) continue;
             const int nth = G * S * W;
             if (nth > kMaxThreads / NSLAB || nth % 32) continue;
             const size_t smem = CLayout<T, W, NSLAB, LS>(G, m, S, P, nth).total;
