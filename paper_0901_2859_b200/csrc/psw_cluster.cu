@@ -178,11 +178,17 @@ __device__ __forceinline__ void bwd_v4(const unsigned char* co, int a, int len,
     }
 }
 
-template <typename T, int W, int NMAX, bool EXACT = (NMAX <= kSegLen), bool LS = false>
+template <typename T, int W, int NMAX, bool EXACT = (NMAX <= kSegLen), bool LS = false, int DL = 0>
 __device__ __forceinline__ void fwd(const T* slab, const unsigned char* co, int a, int lane,
                                     int len, T (&dr)[kSegMax], double* sd, double* sx, double* sr,
                                     double* sl, int tid, int gm = 0) {
     const T* col = slab + size_t(a) * W + lane;
+    // layout S: physical row a + 1 + r = q16 + DL + r with q16 a multiple of 16
+    // (DL = (a + 1) mod 16, compile time), so box, chunk and half of every row
+    // are constants and only the lane's XOR term is a register
+    const int q16 = a + 1 - DL;
+    const T* lb = slab + q16 * 16 + lane * 16;
+    const int x2 = (lane & 7) << 1;
     T d = T(0), lx = T(0);
     double br = 0.0, bl = 0.0;
 #pragma unroll
@@ -193,9 +199,11 @@ __device__ __forceinline__ void fwd(const T* slab, const unsigned char* co, int 
             const T lam = c[1].x;
             T f;
             if constexpr (LS) {  // physical row a + r + 1; rows >= gm in the tail box
+                const int j = DL + r;  // a constant after unrolling
                 const int q = a + r + 1;
-                f = (r >= kSegLen - 1 && q >= gm) ? slab[gm * W + lane * 2 + (q - gm)]
-                                                  : slab[s_index<T, W>(q, lane)];
+                f = (r >= kSegLen - 1 && q >= gm)
+                        ? slab[gm * W + lane * 2 + (q - gm)]
+                        : lb[((j >> 4) << 8) + (x2 ^ (((j & 15) >> 1) << 1)) + (j & 1)];
             } else {
                 f = col[r * W];
             }
@@ -376,7 +384,14 @@ __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
         // one instruction stream for every lane: segments are 31, 32 or 33 rows
         // (m % 32 == 0), and the two segments a warp sweeps may differ in length;
         // rows 0..30 unpredicated, the last two under a predicate
-        fwd<T, W, kSegMax, false, LS>(slab, co, a, lane, len, dr, sd, sx, sr, sl, tid, G * m);
+        if constexpr (LS) {  // a + 1 = 1 or 2 mod 16 (uniform partition, m % 32 == 0)
+            if (((a + 1) & 15) == 1)
+                fwd<T, W, kSegMax, false, LS, 1>(slab, co, a, lane, len, dr, sd, sx, sr, sl, tid, G * m);
+            else
+                fwd<T, W, kSegMax, false, LS, 2>(slab, co, a, lane, len, dr, sd, sx, sr, sl, tid, G * m);
+        } else {
+            fwd<T, W, kSegMax, false, LS>(slab, co, a, lane, len, dr, sd, sx, sr, sl, tid, G * m);
+        }
         bar_sync(2 + j, S * W);  // the block's rows swept, its partials visible
         if (g.trace > 2 && tid == 0) {  // force the deferred barrier wait before the stamp
             volatile double* vs = sd;
