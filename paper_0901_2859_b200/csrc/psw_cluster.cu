@@ -189,6 +189,7 @@ __device__ __forceinline__ void fwd(const T* slab, const unsigned char* co, int 
     const int q16 = a + 1 - DL;
     const T* lb = slab + q16 * 16 + lane * 16;
     const int x2 = (lane & 7) << 1;
+    T fn = T(0);  // the second row of a 16-byte chunk (layout S)
     T d = T(0), lx = T(0);
     double br = 0.0, bl = 0.0;
 #pragma unroll
@@ -199,11 +200,22 @@ __device__ __forceinline__ void fwd(const T* slab, const unsigned char* co, int 
             const T lam = c[1].x;
             T f;
             if constexpr (LS) {  // physical row a + r + 1; rows >= gm in the tail box
+                // rows 0..30 two at a time (one 16-byte chunk: conflict-free for
+                // 16 lanes), rows 31, 32 one at a time (they may be in the tail box)
                 const int j = DL + r;  // a constant after unrolling
-                const int q = a + r + 1;
-                f = (r >= kSegLen - 1 && q >= gm)
-                        ? slab[gm * W + lane * 2 + (q - gm)]
-                        : lb[((j >> 4) << 8) + (x2 ^ (((j & 15) >> 1) << 1)) + (j & 1)];
+                const int o = ((j >> 4) << 8) + (x2 ^ (((j & 15) >> 1) << 1));
+                if (r >= kSegLen - 1) {
+                    const int q = a + r + 1;
+                    f = q >= gm ? slab[gm * W + lane * 2 + (q - gm)] : lb[o + (j & 1)];
+                } else if ((j & 1) == 0 && r + 1 <= kSegLen - 2) {
+                    const double2 v = *reinterpret_cast<const double2*>(lb + o);
+                    f = v.x;
+                    fn = v.y;
+                } else if ((j & 1) == 1 && r >= 1) {
+                    f = fn;
+                } else {
+                    f = lb[o + (j & 1)];
+                }
             } else {
                 f = col[r * W];
             }
