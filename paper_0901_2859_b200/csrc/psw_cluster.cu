@@ -99,6 +99,19 @@ __host__ __device__ __forceinline__ size_t coff(int q) {
     return size_t(q) * 8 * sizeof(T) + size_t(q >> 5) * 16;
 }
 
+// Coefficient row a + r from the segment's first row a: segments start at
+// slab rows a = 0 or 1 mod 32 (uniform partitions, m % 32 == 0), so with
+// AC = a mod 32 known at compile time every row is a constant offset from
+// coff(a) (AC < 0: computed).
+template <typename T, int AC>
+__device__ __forceinline__ const unsigned char* crow(const unsigned char* co, const unsigned char* cb,
+                                                     int a, int r) {
+    if constexpr (AC < 0)
+        return co + coff<T>(a + r);
+    else
+        return cb + size_t(r) * 8 * sizeof(T) + size_t((AC + r) >> 5) * 16;
+}
+
 // Shared-memory carve-up (bytes), identical on host and device.
 template <typename T, int W, int NSLAB, bool LS = false>
 struct CLayout {
@@ -151,10 +164,11 @@ template <int AL>
 __device__ __forceinline__ void bwd_v4(const unsigned char* co, int a, int len,
                                        double (&dr)[kSegMax], double D, double xl, double xn,
                                        double* xp) {
+    const unsigned char* cb = co + coff<double>(a);
 #pragma unroll
     for (int r = kSegMax - 1; r >= 0; --r) {
         if (r < kSegLen - 1 || r < len) {
-            const Quad<double> c1 = reinterpret_cast<const Quad<double>*>(co + coff<double>(a + r))[1];
+            const Quad<double> c1 = reinterpret_cast<const Quad<double>*>(crow<double, AL == 0 ? 1 : 0>(co, cb, a, r))[1];
             xn = fma(c1.w, xn, fma(xl, c1.z, fma(c1.y, D, dr[r])));
             dr[r] = xn;
         }
@@ -178,7 +192,8 @@ __device__ __forceinline__ void bwd_v4(const unsigned char* co, int a, int len,
     }
 }
 
-template <typename T, int W, int NMAX, bool EXACT = (NMAX <= kSegLen), bool LS = false, int DL = 0>
+template <typename T, int W, int NMAX, bool EXACT = (NMAX <= kSegLen), bool LS = false, int DL = 0,
+          int AC = -1>
 __device__ __forceinline__ void fwd(const T* slab, const unsigned char* co, int a, int lane,
                                     int len, T (&dr)[kSegMax], double* sd, double* sx, double* sr,
                                     double* sl, int tid, int gm = 0) {
@@ -190,12 +205,13 @@ __device__ __forceinline__ void fwd(const T* slab, const unsigned char* co, int 
     const T* lb = slab + q16 * 16 + lane * 16;
     const int x2 = (lane & 7) << 1;
     T fn = T(0);  // the second row of a 16-byte chunk (layout S)
+    const unsigned char* cb = co + coff<T>(a);
     T d = T(0), lx = T(0);
     double br = 0.0, bl = 0.0;
 #pragma unroll
     for (int r = 0; r < NMAX; ++r) {
         if (EXACT || r < kSegLen - 1 || r < len) {
-            const Quad<T>* c = reinterpret_cast<const Quad<T>*>(co + coff<T>(a + r));
+            const Quad<T>* c = reinterpret_cast<const Quad<T>*>(crow<T, AC>(co, cb, a, r));
             const Quad<T> c0 = c[0];
             const T lam = c[1].x;
             T f;
@@ -242,13 +258,14 @@ __device__ __forceinline__ void fwd(const T* slab, const unsigned char* co, int 
 }
 
 // back substitution of one segment from the exact carries, last row first
-template <typename T, int NMAX, bool EXACT = (NMAX <= kSegLen)>
+template <typename T, int NMAX, bool EXACT = (NMAX <= kSegLen), int AC = -1>
 __device__ __forceinline__ void bwd(const unsigned char* co, int a, int len,
                                     const T (&dr)[kSegMax], T D, T xl, T xn, T* xp, int64_t ldx) {
+    const unsigned char* cb = co + coff<T>(a);
 #pragma unroll
     for (int r = NMAX - 1; r >= 0; --r) {
         if (EXACT || r < kSegLen - 1 || r < len) {
-            const Quad<T> c1 = reinterpret_cast<const Quad<T>*>(co + coff<T>(a + r))[1];
+            const Quad<T> c1 = reinterpret_cast<const Quad<T>*>(crow<T, AC>(co, cb, a, r))[1];
             xn = fma(c1.w, xn, fma(xl, c1.z, fma(c1.y, D, dr[r])));
             __stcs(xp + int64_t(r) * ldx, xn);
         }
@@ -398,11 +415,14 @@ __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
         // rows 0..30 unpredicated, the last two under a predicate
         if constexpr (LS) {  // a + 1 = 1 or 2 mod 16 (uniform partition, m % 32 == 0)
             if (((a + 1) & 15) == 1)
-                fwd<T, W, kSegMax, false, LS, 1>(slab, co, a, lane, len, dr, sd, sx, sr, sl, tid, G * m);
+                fwd<T, W, kSegMax, false, LS, 1, 0>(slab, co, a, lane, len, dr, sd, sx, sr, sl, tid, G * m);
             else
-                fwd<T, W, kSegMax, false, LS, 2>(slab, co, a, lane, len, dr, sd, sx, sr, sl, tid, G * m);
-        } else {
-            fwd<T, W, kSegMax, false, LS>(slab, co, a, lane, len, dr, sd, sx, sr, sl, tid, G * m);
+                fwd<T, W, kSegMax, false, LS, 2, 1>(slab, co, a, lane, len, dr, sd, sx, sr, sl, tid, G * m);
+        } else {  // a = 0 or 1 mod 32
+            if ((a & 31) == 0)
+                fwd<T, W, kSegMax, false, LS, 0, 0>(slab, co, a, lane, len, dr, sd, sx, sr, sl, tid, G * m);
+            else
+                fwd<T, W, kSegMax, false, LS, 0, 1>(slab, co, a, lane, len, dr, sd, sx, sr, sl, tid, G * m);
         }
         bar_sync(2 + j, S * W);  // the block's rows swept, its partials visible
         if (g.trace > 2 && tid == 0) {  // force the deferred barrier wait before the stamp
@@ -532,7 +552,11 @@ __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
                 }
             }
         } else if (kk < g.N) {
-            bwd<T, kSegMax, false>(co, a, len, dr, D, xlt, xn, X + int64_t(sgd.a) * g.ldx + kk, g.ldx);
+            T* xp = X + int64_t(sgd.a) * g.ldx + kk;
+            if ((a & 31) == 0)
+                bwd<T, kSegMax, false, 0>(co, a, len, dr, D, xlt, xn, xp, g.ldx);
+            else
+                bwd<T, kSegMax, false, 1>(co, a, len, dr, D, xlt, xn, xp, g.ldx);
         }
         stamp(k, 6);
         if (k == 0) etrace(2);
