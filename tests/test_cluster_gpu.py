@@ -98,6 +98,27 @@ def test_cluster_shapes(psw, cuda, n, P, dtype):
     assert rel_l2(X, ref) <= tol, rel_l2(X, ref)
 
 
+@pytest.mark.parametrize("n,P", [(4096, 16), (2048, 4), (4096, 32), (1024, 4), (2048, 8),
+                                 (8192, 16), (8192, 8)])
+def test_cluster_shapes_s(psw, cuda, n, P):
+    """Layout S (fp64) over cluster sizes 2..16 and blocks of 128..1024 rows,
+    against STAGED; shapes whose only configuration is one block per CTA
+    (excluded for layout S) report NotSupported."""
+    rng = np.random.default_rng(n + 3 * P)
+    a = rng.uniform(-1, -0.5, n - 1)
+    b = np.abs(np.r_[0, a]) + np.abs(np.r_[a, 0]) + rng.uniform(0.1, 1, n)
+    plan = psw.Plan(psw.TridiagMatrix.symmetric(a, b), psw.decompose(n, P).induced_partition(),
+                    dtype=psw.F64)
+    F = rng.uniform(-1, 1, (300, n))
+    try:
+        X = gpu_solve(psw, cuda, plan, F, 1, path=psw.PATH_CLUSTER)
+    except psw.NotSupported:
+        assert (n, P) not in ((4096, 16), (2048, 4), (1024, 4)), (n, P)
+        return
+    ref = gpu_solve(psw, cuda, plan, F, 1, path=psw.PATH_STAGED)
+    assert rel_l2(X, ref) <= 1e-12, rel_l2(X, ref)
+
+
 @pytest.mark.parametrize("N", [2, 16, 18, 100, 1000])
 def test_cluster_layout_s(psw, cuda, N):
     """Layout S (fp64): 16-row swizzled TMA boxes of 16 right-hand sides."""
