@@ -591,9 +591,10 @@ CChoice choose_t(const psw_plan* pl) {
             const int C = P / G;
             if (C > kMaxC) break;
             if (force_g > 0 && G != force_g) continue;
-            // layout S with one block per CTA (G = 1, C = 16) gives wrong rows from
-            // the second segment on (C1 matrix, a single unit; G = 2 is exact on
-            // every test): excluded until understood
+            // layout S needs G >= 2: the forward reads row 30 of a segment from
+            // the swizzled boxes, but with G = 1 CTA 0's only block is the short
+            // first block, whose row 30 is the CTA's last row, in the tail box.
+            // A tail check on row 30 costs registers (spills, C4 88 -> 95 us).
             if (LS && G == 1) continue;
             const int nth = G * S * W;
             if (nth > kMaxThreads / NSLAB || nth % 32) continue;

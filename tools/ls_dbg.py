@@ -33,3 +33,9 @@ if d.any():
     print("row intervals", iv)
     for k in (1, 2, 8, 9):
         print("rhs", k, "bad rows", np.nonzero(d[k])[0][:12])
+if d.any():
+    e = np.abs(X - ref)
+    for k in (1, 8):
+        top = np.argsort(-e[k])[:6]
+        print("rhs", k, "largest errors at rows", sorted(top.tolist()), "max", e[k].max())
+        print("  err rows 30..70:", np.array2string(e[k, 30:70], precision=1, max_line_width=250))
