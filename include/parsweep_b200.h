@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define PSW_ABI_VERSION 2
+#define PSW_ABI_VERSION 3
 
 /* Status codes. The C++ wrapper (parsweep_b200.hpp) maps them back onto the
  * reference exception types of core/errors.hpp:9-62. */
@@ -63,15 +63,17 @@ typedef enum psw_layout { PSW_LAYOUT_R = 0, PSW_LAYOUT_S = 1 } psw_layout;
  * supports the plan/shape: CLUSTER and FUSED keep every RHS tile resident on
  * chip and read F once (layout R, uniform partitions whose blocks fit a
  * cluster; CLUSTER: one CTA per SM holding G blocks, FUSED: 16-CTA clusters);
- * RESWEEP reads F twice and writes X once with per-segment checkpoints
- * (either layout, e.g. the 2^20-row and fp32 configs); STAGED is the general
- * three-kernel path (and the only one returning betas/boundary values). */
+ * CHUNKED runs the RESWEEP kernels over RHS chunks sized for L2, so the
+ * second read of F hits L2 (layout R, narrow systems: the fp32 config);
+ * RESWEEP reads F twice from HBM and writes X once, with a few aggregates per
+ * 256 rows in between (either layout, e.g. the 2^20-row config); STAGED is
+ * the general three-kernel path (and the only one returning betas/boundary
+ * values). */
 typedef enum psw_path {
     PSW_PATH_AUTO = 0,
     PSW_PATH_STAGED = 1,
     PSW_PATH_FUSED = 2,
-    PSW_PATH_PIPE = 3,
-    PSW_PATH_TILE = 4,
+    /* 3, 4: retired paths (PSW_NOT_SUPPORTED) */
     PSW_PATH_CHUNKED = 5,
     PSW_PATH_RESWEEP = 6,
     PSW_PATH_CLUSTER = 7
@@ -204,28 +206,45 @@ int psw_last_path(void);
 
 /* ---- multi-GPU row sharding (dichotomy across devices) ---------------- */
 /* The reference simulates message passing (runtime/run.hpp:30-35,93-94) with
- * logical PEs; here the PEs are GPUs. Rank r of `world` owns the blocks
- * [r*P/world, (r+1)*P/world) of ONE global partition (P = p+1 must be
- * divisible by world) and the rows of those blocks; F/X hold only the owned
- * rows, layout R (row offset psw_shard_row_offset, psw_shard_rows rows).
- * The dichotomy combination is linear in the betas, so each rank forms its
- * share of every boundary value and the only exchange is one sum:
- *   psw_shard_forward   local forward sweep + betas; writes d0 into X and the
- *                       rank's partial boundary values into `partials`
- *                       (device fp64, p x nrhs, [j * nrhs + k])
- *   <all-reduce(sum) of `partials` over the ranks: NCCL / torch.distributed>
- *   psw_shard_backward  back substitution of the owned blocks with the
- *                       reduced boundary values. */
+ * logical PEs; here the PEs are GPUs, one process (or thread) per GPU. Rank r
+ * of `world` owns the blocks [r*P/world, (r+1)*P/world) of ONE global
+ * partition (P = p+1 must be divisible by world) and the rows of those
+ * blocks (the paper's data decomposition); F/X hold only
+ * the owned rows, layout R (row offset psw_shard_row_offset, psw_shard_rows
+ * rows). The dichotomy combination (dichotomy/boundary_solve.hpp:96-121) is
+ * linear in the betas, so each rank forms its share of every boundary value
+ * and the solve's only exchange is one all-reduce(sum) of p x nrhs fp64.
+ *
+ *   psw_shard_solve     forward sweep + betas + the rank's share of the p
+ *                       boundary values, ncclAllReduce over `comm`, back
+ *                       substitution: all on `stream`, CUDA-graph capturable.
+ *   psw_shard_forward / psw_shard_backward   the two halves around a caller-
+ *                       run reduction of `partials` (p x nrhs fp64, [j*nrhs+k]);
+ *                       `workspace` (psw_shard_workspace_bytes) carries the
+ *                       per-run aggregates from one to the other.
+ * A shard plan is created by psw_shard_plan_create; psw_solve refuses it. */
 int psw_shard_plan_create(psw_plan** out, int64_t n, const double* sub, const double* diag,
                           const double* sup, int64_t p, const int64_t* boundaries, int dtype,
                           int device, int rank, int world);
 int64_t psw_shard_partials_count(const psw_plan* plan);
 int64_t psw_shard_row_offset(const psw_plan* plan);
 int64_t psw_shard_rows(const psw_plan* plan);
-int psw_shard_forward(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
-                      int64_t nrhs, double* partials, void* stream);
-int psw_shard_backward(const psw_plan* plan, void* X, int64_t ldx, int64_t nrhs,
-                       const double* partials, void* stream);
+int64_t psw_shard_workspace_bytes(const psw_plan* plan, int64_t nrhs);
+int psw_shard_forward(const psw_plan* plan, const void* F, int64_t ldf, int64_t nrhs,
+                      void* workspace, double* partials, void* stream);
+int psw_shard_backward(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
+                       int64_t nrhs, void* workspace, const double* partials, void* stream);
+
+/* NCCL communicator of the row-sharded solve (NCCL is loaded at run time,
+ * libnccl.so.2; PSW_NCCL_ERROR when it is absent or a call fails). Rank 0
+ * creates the 128-byte unique id, every rank passes it to psw_comm_create
+ * (collective over the `nranks` ranks, like ncclCommInitRank). */
+typedef struct psw_comm psw_comm;
+int psw_comm_unique_id(void* id_out /* 128 bytes */);
+int psw_comm_create(psw_comm** out, int nranks, int rank, const void* id, int device);
+int psw_comm_destroy(psw_comm* comm);
+int psw_shard_solve(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
+                    int64_t nrhs, psw_comm* comm, void* stream);
 
 /* Host-only (no GPU needed): the p x 2P combination matrix of the partition
  * (row j = [MR[j][0..P) | ML[j][0..P)]), i.e. the action of solve_boundaries
@@ -246,9 +265,7 @@ int psw_fill_normal(void* dst, int dtype, int64_t count, uint64_t seed, uint64_t
                     void* stream);
 /* Profiling aid: when `device_buffer` is non-NULL the FUSED kernel writes,
  * per CTA, 16 uint64 slots: clock64() at its phase boundaries (0..8) and
- * %globaltimer at start/end (14, 15); the PIPE kernel writes 4 uint64 per
- * work-item ticket: start, dependencies met, end (%globaltimer ns) and
- * (item type << 32 | SM id). NULL disables tracing (default). */
+ * %globaltimer at start/end (14, 15). NULL disables tracing (default). */
 int psw_debug_trace(void* device_buffer);
 
 /* Write `bytes` of zeros+index pattern over a scratch buffer (L2 flush). */

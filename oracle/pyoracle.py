@@ -337,6 +337,50 @@ class Reference(_Base):
     def hardware_concurrency(self) -> int:
         return int(self.lib.ref_hardware_concurrency())
 
+    def plan(self, sub, diag, sup, bnd, workers: int = 1) -> "RefPlan":
+        """compute_preliminary once (on a WorkerPool of `workers`), then
+        RefPlan.solve(F, nthreads) over disjoint RHS slices."""
+        return RefPlan(self, sub, diag, sup, bnd, workers)
+
+
+class RefPlan:
+    def __init__(self, ref: "Reference", sub, diag, sup, bnd, workers: int):
+        sub, diag, sup = map(_f64, (sub, diag, sup))
+        bnd = np.ascontiguousarray(bnd, dtype=np.int64)
+        L = ref.lib
+        L.ref_plan_create.restype = C.c_void_p
+        L.ref_plan_create.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                      C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+        L.ref_plan_solve.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
+                                     C.c_int64, C.c_int, C.c_void_p, C.c_void_p]
+        L.ref_plan_destroy.argtypes = [C.c_void_p]
+        self.lib, self.n = L, diag.size
+        su = C.c_double(0)
+        bad = np.zeros(1, np.int64)
+        self.h = L.ref_plan_create(diag.size, _dp(sub), _dp(diag), _dp(sup), bnd.size, _ip(bnd),
+                                   workers, C.byref(su), _ip(bad))
+        if not self.h:
+            raise OracleError(-1, int(bad[0]))
+        self.setup_s = su.value
+
+    def solve(self, F, nthreads: int = 1):
+        """Returns (X, solve seconds)."""
+        F = _f64(F)
+        N, n = F.shape
+        X = np.empty_like(F)
+        so = C.c_double(0)
+        bad = np.zeros(1, np.int64)
+        rc = self.lib.ref_plan_solve(self.h, N, _dp(F), n, _dp(X), n, nthreads, C.byref(so),
+                                     _ip(bad))
+        if rc != 0:
+            raise OracleError(rc, int(bad[0]))
+        return X, so.value
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.ref_plan_destroy(self.h)
+            self.h = None
+
 
 def reference_available() -> bool:
     return os.path.exists(REF_SO)

@@ -248,6 +248,70 @@ int ref_solve_rhs_parallel(int64_t n, const double* sub, const double* diag, con
     }, bad);
 }
 
+// CPU baseline with the preliminary built once: the
+// reference's compute_preliminary on a WorkerPool of `workers` threads (its
+// own parallel setup over boundaries, preliminary.hpp:182-195), then any
+// number of solves on `nthreads` std::threads over disjoint RHS slices.
+struct RefPlan {
+    TridiagMatrix A;
+    Partition part;
+    parsweep::PreliminaryData prelim;
+};
+
+void* ref_plan_create(int64_t n, const double* sub, const double* diag, const double* sup,
+                      int64_t p, const int64_t* bnd, int64_t workers, double* setup_s,
+                      int64_t* bad) {
+    RefPlan* out = nullptr;
+    const int rc = guarded([&] {
+        auto A = make_matrix(n, sub, diag, sup);
+        auto part = make_partition(n, p, bnd);
+        part.validate();
+        parsweep::WorkerPool pool(static_cast<std::size_t>(workers < 1 ? 1 : workers));
+        const auto t0 = std::chrono::steady_clock::now();
+        auto prelim = parsweep::compute_preliminary(A, part, parsweep::GRowStrategy::Auto, pool);
+        const auto t1 = std::chrono::steady_clock::now();
+        if (setup_s) *setup_s = std::chrono::duration<double>(t1 - t0).count();
+        out = new RefPlan{std::move(A), std::move(part), std::move(prelim)};
+    }, bad);
+    return rc == 0 ? out : nullptr;
+}
+
+int ref_plan_solve(void* h, int64_t nrhs, const double* F, int64_t ldf, double* X, int64_t ldx,
+                   int nthreads, double* solve_s, int64_t* bad) {
+    return guarded([&] {
+        const RefPlan& rp = *static_cast<const RefPlan*>(h);
+        const int64_t n = static_cast<int64_t>(rp.A.diag.size());
+        int w = nthreads < 1 ? 1 : nthreads;
+        if (w > nrhs) w = static_cast<int>(nrhs > 0 ? nrhs : 1);
+        const int64_t chunk = (nrhs + w - 1) / w;
+        std::vector<std::exception_ptr> errs(static_cast<std::size_t>(w));
+        const auto t0 = std::chrono::steady_clock::now();
+        auto body = [&](int wi) {
+            try {
+                std::vector<parsweep::LocalScratch> pool;
+                for (int64_t k = wi * chunk; k < std::min<int64_t>(nrhs, (wi + 1) * chunk); ++k)
+                    parsweep::solve_with_preliminary_into(
+                        rp.A, rp.prelim,
+                        std::span<const double>(F + k * ldf, static_cast<std::size_t>(n)),
+                        std::span<double>(X + k * ldx, static_cast<std::size_t>(n)),
+                        parsweep::serial_executor(), nullptr, &pool);
+            } catch (...) {
+                errs[static_cast<std::size_t>(wi)] = std::current_exception();
+            }
+        };
+        std::vector<std::thread> th;
+        for (int wi = 1; wi < w; ++wi) th.emplace_back(body, wi);
+        body(0);
+        for (auto& t : th) t.join();
+        if (solve_s)
+            *solve_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        for (auto& e : errs)
+            if (e) std::rethrow_exception(e);
+    }, bad);
+}
+
+void ref_plan_destroy(void* h) { delete static_cast<RefPlan*>(h); }
+
 // ---- ADI consumer (poisson/adi.hpp), §8(f) rank 1 -----------------------
 namespace {
 parsweep::poisson::Grid2D make_grid(int64_t n1, int64_t n2, double h1, double h2, const double* v) {

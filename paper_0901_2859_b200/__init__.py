@@ -32,8 +32,8 @@ import numpy as np
 __all__ = [
     "TridiagMatrix", "Partition", "Decomposition", "decompose", "compute_preliminary", "Plan",
     "solve_batch", "solve_multi", "SolverError", "PivotBreakdown", "TooManyPEs", "NotSupported", "NotSymmetrizable", "OracleFallbackRequired", "CudaError",
-    "F64", "F32", "LAYOUT_R", "LAYOUT_S", "PATH_AUTO", "PATH_STAGED", "PATH_FUSED", "PATH_PIPE", "PATH_TILE", "PATH_CHUNKED", "PATH_RESWEEP", "PATH_CLUSTER", "last_path", "lib",
-    "library_path",
+    "F64", "F32", "LAYOUT_R", "LAYOUT_S", "PATH_AUTO", "PATH_STAGED", "PATH_FUSED", "PATH_CHUNKED",
+    "PATH_RESWEEP", "PATH_CLUSTER", "last_path", "lib", "library_path", "Comm", "NcclError",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -41,7 +41,7 @@ LIB_PATH = os.path.join(HERE, "_lib", "libparsweep_b200.so")
 
 F64, F32 = 0, 1
 LAYOUT_R, LAYOUT_S = 0, 1
-PATH_AUTO, PATH_STAGED, PATH_FUSED, PATH_PIPE, PATH_TILE, PATH_CHUNKED, PATH_RESWEEP, PATH_CLUSTER = 0, 1, 2, 3, 4, 5, 6, 7
+PATH_AUTO, PATH_STAGED, PATH_FUSED, PATH_CHUNKED, PATH_RESWEEP, PATH_CLUSTER = 0, 1, 2, 5, 6, 7
 OK, INVALID_ARGUMENT, PIVOT_BREAKDOWN, TOO_MANY_PES, NOT_SUPPORTED, CUDA_ERROR, NCCL_ERROR, OOM = range(8)
 NOT_SYMMETRIZABLE, ORACLE_FALLBACK_REQUIRED = 8, 9
 # GRowStrategy (dichotomy/preliminary.hpp:18-24)
@@ -83,6 +83,10 @@ class NotSupported(SolverError):
 
 class CudaError(SolverError):
     pass
+
+
+class NcclError(SolverError):
+    """PSW_NCCL_ERROR: NCCL missing or a collective of the row-sharded solve failed."""
 
 
 # ---------------------------------------------------------------- library
@@ -127,8 +131,14 @@ def lib() -> C.CDLL:
         L.psw_shard_row_offset.restype = C.c_int64
         L.psw_shard_rows.argtypes = [vp]
         L.psw_shard_rows.restype = C.c_int64
-        L.psw_shard_forward.argtypes = [vp, vp, C.c_int64, vp, C.c_int64, C.c_int64, vp, vp]
-        L.psw_shard_backward.argtypes = [vp, vp, C.c_int64, C.c_int64, vp, vp]
+        L.psw_shard_workspace_bytes.argtypes = [vp, C.c_int64]
+        L.psw_shard_workspace_bytes.restype = C.c_int64
+        L.psw_shard_forward.argtypes = [vp, vp, C.c_int64, C.c_int64, vp, vp, vp]
+        L.psw_shard_backward.argtypes = [vp, vp, C.c_int64, vp, C.c_int64, C.c_int64, vp, vp, vp]
+        L.psw_shard_solve.argtypes = [vp, vp, C.c_int64, vp, C.c_int64, C.c_int64, vp, vp]
+        L.psw_comm_unique_id.argtypes = [vp]
+        L.psw_comm_create.argtypes = [C.POINTER(vp), C.c_int, C.c_int, vp, C.c_int]
+        L.psw_comm_destroy.argtypes = [vp]
         L.psw_fill_uniform.argtypes = [vp, C.c_int, C.c_int64, C.c_uint64, C.c_uint64, C.c_double,
                                        C.c_double, vp]
         L.psw_fill_normal.argtypes = [vp, C.c_int, C.c_int64, C.c_uint64, C.c_uint64, vp]
@@ -155,6 +165,8 @@ def _raise(rc: int):
         raise OracleFallbackRequired(msg)
     if rc == OOM:
         raise MemoryError(msg)
+    if rc == NCCL_ERROR:
+        raise NcclError(msg)
     raise CudaError(f"status {rc}: {msg}")
 
 
@@ -167,9 +179,8 @@ def last_launch_count() -> int:
     return int(lib().psw_last_launch_count())
 
 
-PATH_NAMES = {PATH_STAGED: "staged", PATH_FUSED: "fused", PATH_PIPE: "pipe", PATH_TILE: "tile",
-              PATH_CHUNKED: "chunked", PATH_RESWEEP: "resweep",
-              PATH_CLUSTER: "cluster"}
+PATH_NAMES = {PATH_STAGED: "staged", PATH_FUSED: "fused", PATH_CHUNKED: "chunked",
+              PATH_RESWEEP: "resweep", PATH_CLUSTER: "cluster"}
 
 
 def last_path() -> str:
@@ -331,6 +342,7 @@ class Plan:
         self.dtype = dtype
         self.device = device
         shard = world is not None
+        self._shard = shard
         self.rank, self.world = (rank or 0), (world or 1)
         b = np.ascontiguousarray(part.boundaries, dtype=np.int64)
         if b.size == 0:
@@ -374,12 +386,18 @@ class Plan:
         (N, n) [k*ld + i]. X defaults to F (in place)."""
         if X is None:
             X = F
+        if layout not in (LAYOUT_R, LAYOUT_S):
+            raise ValueError("layout must be LAYOUT_R or LAYOUT_S")
+        self._check_device_tensor(F, "F")
+        self._check_device_tensor(X, "X")
         if nrhs is None:
             nrhs = F.shape[1] if layout == LAYOUT_R else F.shape[0]
         if ldf is None:
             ldf = F.stride(0)
         if ldx is None:
             ldx = X.stride(0)
+        for t, ld, name in ((F, ldf, "F"), (X, ldx, "X")):
+            self._check_extent(t, ld, nrhs, layout, name)
         s = _stream_ptr(stream)
         opts = None
         if (path != PATH_AUTO or betas_left is not None or betas_right is not None
@@ -397,13 +415,50 @@ class Plan:
         _check(rc)
         return X
 
+    # -- argument checks (a wrong buffer must raise, never reach the kernels)
+    def _check_device_tensor(self, t, name: str):
+        import torch
+        if not isinstance(t, torch.Tensor):
+            raise ValueError(f"{name} must be a CUDA tensor")
+        want = torch.float64 if self.dtype == F64 else torch.float32
+        if t.dtype != want:
+            raise ValueError(f"{name} has dtype {t.dtype}, the plan solves in {want}")
+        if not t.is_cuda or t.device.index != self.device:
+            raise ValueError(f"{name} must live on cuda:{self.device} (got {t.device})")
+        if t.dim() != 2 or t.stride(-1) != 1:
+            raise ValueError(f"{name} must be a 2-D tensor with unit inner stride")
+
+    def _check_extent(self, t, ld: int, nrhs: int, layout: int, name: str):
+        rows = self.rows() if self._shard else self.n
+        if layout == LAYOUT_R:
+            need_rows, need_cols = rows, nrhs
+        else:
+            need_rows, need_cols = nrhs, rows
+        if nrhs < 0 or ld < need_cols:
+            raise ValueError(f"{name}: leading dimension {ld} < {need_cols}")
+        if nrhs == 0:
+            return
+        last = (need_rows - 1) * ld + need_cols  # elements the solve touches
+        if t.shape[0] < need_rows or t.shape[1] < need_cols or \
+                t.storage_offset() + last > t.untyped_storage().nbytes() // t.element_size():
+            raise ValueError(f"{name} of shape {tuple(t.shape)} is too small for "
+                             f"{need_rows} x {need_cols} (layout {'RS'[layout]})")
+
     def solve_host(self, F: np.ndarray, X: np.ndarray | None = None, layout: int = LAYOUT_S):
         """End-to-end solve on host arrays (psw_solve_host)."""
         dt = np.float64 if self.dtype == F64 else np.float32
-        if F.dtype != dt or not F.flags.c_contiguous:
-            raise ValueError("F must be a C-contiguous array of the plan dtype")
+        if layout not in (LAYOUT_R, LAYOUT_S):
+            raise ValueError("layout must be LAYOUT_R or LAYOUT_S")
+        if not isinstance(F, np.ndarray) or F.dtype != dt or not F.flags.c_contiguous or F.ndim != 2:
+            raise ValueError("F must be a C-contiguous 2-D array of the plan dtype")
         if X is None:
             X = np.empty_like(F)
+        if not isinstance(X, np.ndarray) or X.dtype != dt or not X.flags.c_contiguous or \
+                X.shape != F.shape:
+            raise ValueError("X must be a C-contiguous array of F's shape and the plan dtype")
+        if (F.shape[0] if layout == LAYOUT_R else F.shape[1]) != self.n:
+            raise ValueError(f"F must hold n = {self.n} rows per system "
+                             f"({'rows' if layout == LAYOUT_R else 'columns'} of the array)")
         nrhs = F.shape[1] if layout == LAYOUT_R else F.shape[0]
         _check(lib().psw_solve_host(self._h, F.ctypes.data, F.shape[1], X.ctypes.data, X.shape[1],
                                     nrhs, layout))
@@ -419,13 +474,73 @@ class Plan:
     def rows(self) -> int:
         return int(lib().psw_shard_rows(self._h))
 
-    def shard_forward(self, F, X, partials, nrhs: int, stream=None):
-        _check(lib().psw_shard_forward(self._h, _ptr(F), F.stride(0), _ptr(X), X.stride(0), nrhs,
+    def workspace_bytes(self, nrhs: int) -> int:
+        return int(lib().psw_shard_workspace_bytes(self._h, nrhs))
+
+    def shard_forward(self, F, nrhs: int, workspace, partials, stream=None):
+        """K1 + fold + this rank's share of the p boundary values -> partials (p x nrhs fp64)."""
+        self._check_device_tensor(F, "F")
+        self._check_extent(F, F.stride(0), nrhs, LAYOUT_R, "F")
+        _check(lib().psw_shard_forward(self._h, _ptr(F), F.stride(0), nrhs, _ptr(workspace),
                                        _ptr(partials), _stream_ptr(stream)))
 
-    def shard_backward(self, X, partials, nrhs: int, stream=None):
-        _check(lib().psw_shard_backward(self._h, _ptr(X), X.stride(0), nrhs, _ptr(partials),
-                                        _stream_ptr(stream)))
+    def shard_backward(self, F, X, nrhs: int, workspace, partials, stream=None):
+        """Run carries from the reduced boundary values + the second sweep of F -> X."""
+        self._check_device_tensor(F, "F")
+        self._check_device_tensor(X, "X")
+        self._check_extent(F, F.stride(0), nrhs, LAYOUT_R, "F")
+        self._check_extent(X, X.stride(0), nrhs, LAYOUT_R, "X")
+        _check(lib().psw_shard_backward(self._h, _ptr(F), F.stride(0), _ptr(X), X.stride(0), nrhs,
+                                        _ptr(workspace), _ptr(partials), _stream_ptr(stream)))
+
+    def shard_solve(self, F, X, comm: "Comm | None", nrhs: int | None = None, stream=None):
+        """psw_shard_solve: forward, ncclAllReduce over `comm`, backward, on one stream."""
+        self._check_device_tensor(F, "F")
+        self._check_device_tensor(X, "X")
+        if nrhs is None:
+            nrhs = F.shape[1]
+        self._check_extent(F, F.stride(0), nrhs, LAYOUT_R, "F")
+        self._check_extent(X, X.stride(0), nrhs, LAYOUT_R, "X")
+        _check(lib().psw_shard_solve(self._h, _ptr(F), F.stride(0), _ptr(X), X.stride(0), nrhs,
+                                     comm.handle if comm is not None else None,
+                                     _stream_ptr(stream)))
+        return X
+
+
+class Comm:
+    """NCCL communicator of the row-sharded solve (psw_comm_*). `uid` is the
+    128-byte id from Comm.unique_id() on rank 0, shared by the caller."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(lib().psw_comm_unique_id(buf))
+        return buf.raw
+
+    def __init__(self, nranks: int, rank: int, uid: bytes, device: int):
+        if len(uid) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        h = C.c_void_p()
+        buf = C.create_string_buffer(uid, 128)
+        _check(lib().psw_comm_create(C.byref(h), nranks, rank, buf, device))
+        self._h = h
+        self.nranks, self.rank, self.device = nranks, rank, device
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib().psw_comm_destroy(h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def _stream_ptr(stream) -> int | None:

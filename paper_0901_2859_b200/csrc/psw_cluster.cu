@@ -688,22 +688,16 @@ bool encode(CUtensorMap* tm, CUtensorMap* tm1, CUtensorMap* tm2, const void* F, 
 }
 
 // Coefficient tables of every cluster rank in the kernel's shared-memory
-// layout (coff), built once per plan and choice: the kernel fetches its
-// rank's table with one bulk copy instead of scattering rows.
+// layout (coff), built with the plan for the configuration each layout picks:
+// the kernel fetches its rank's table with one bulk copy instead of
+// scattering rows, and a solve never writes to the plan.
 template <typename T>
-int cluster_tables(const psw_plan* pl, const CChoice& ch) {
+int cluster_tables(psw_plan* pl, const CChoice& ch, int layout,
+                   const std::vector<FusedFwd<double>>& ff,
+                   const std::vector<FusedBwd<double>>& fb) {
     const int G = ch.G, C = ch.C, m = int(pl->m);
-    const int64_t key = (int64_t(G) << 32) | (int64_t(C) << 16) | int64_t(sizeof(T));
-    if (pl->d_ctab && pl->ctab_key == key) return PSW_OK;
-    static std::mutex mu;
-    std::lock_guard<std::mutex> lk(mu);
-    if (pl->d_ctab && pl->ctab_key == key) return PSW_OK;
     const int ra = G * m + 1;
     const size_t stride = ((coff<T>(ra) + 16 + 127) / 128) * 128;
-    std::vector<FusedFwd<T>> ff(pl->n);
-    std::vector<FusedBwd<T>> fb(pl->n);
-    PSW_CUDA_TRY(cudaMemcpy(ff.data(), pl->d_ffwd, sizeof(FusedFwd<T>) * pl->n, cudaMemcpyDeviceToHost));
-    PSW_CUDA_TRY(cudaMemcpy(fb.data(), pl->d_fbwd, sizeof(FusedBwd<T>) * pl->n, cudaMemcpyDeviceToHost));
     std::vector<unsigned char> host(stride * C, 0);
     for (int c = 0; c < C; ++c) {
         const int base = c * G * m - 1;
@@ -712,24 +706,27 @@ int cluster_tables(const psw_plan* pl, const CChoice& ch) {
             const int q = base + i;
             if (q < 0 || q >= pl->n) continue;
             Quad<T>* o = reinterpret_cast<Quad<T>*>(host.data() + size_t(c) * stride + coff<T>(i));
-            o[0] = {ff[q].rp, ff[q].ma, ff[q].gr, ff[q].gl};
-            o[1] = {ff[q].lam, fb[q].mu, fb[q].w, fb[q].al};
+            o[0] = {T(ff[q].rp), T(ff[q].ma), T(ff[q].gr), T(ff[q].gl)};
+            o[1] = {T(ff[q].lam), T(fb[q].mu), T(fb[q].w), T(fb[q].al)};
         }
     }
     void* d = nullptr;
     PSW_CUDA_TRY(cudaMalloc(&d, host.size()));
+    pl->d_ctab[layout] = d;
+    pl->ctab_stride[layout] = int64_t(stride);
     PSW_CUDA_TRY(cudaMemcpy(d, host.data(), host.size(), cudaMemcpyHostToDevice));
-    if (pl->d_ctab) cudaFree(pl->d_ctab);
-    pl->d_ctab = d;
-    pl->ctab_key = key;
-    pl->ctab_stride = int64_t(stride);
+    pl->info.device_bytes += int64_t(host.size());
     return PSW_OK;
 }
 
 template <typename T, int W, int NSLAB, bool LS = false, bool V4 = false>
 int launch(const psw_plan* pl, const CChoice& ch, const void* F, int64_t ldf, void* X, int64_t ldx,
            int64_t N, cudaStream_t s, void** ev, int nev) {
-    if (int rc = cluster_tables<T>(pl, ch)) return rc;
+    const int lay = LS ? PSW_LAYOUT_S : PSW_LAYOUT_R;
+    if (!pl->d_ctab[lay]) {
+        set_error(PSW_NOT_SUPPORTED, "cluster tables missing for this layout");
+        return PSW_NOT_SUPPORTED;
+    }
     CUtensorMap tm, tm1, tm2;
     const int H = box_height(int(pl->m));
     if (LS) {
@@ -796,7 +793,8 @@ int launch(const psw_plan* pl, const CChoice& ch, const void* F, int64_t ldf, vo
                                     static_cast<const FusedFwd<T>*>(pl->d_ffwd),
                                     static_cast<const FusedBwd<T>*>(pl->d_fbwd), pl->d_seg,
                                     pl->d_segdesc, pl->d_cmat,
-                                    static_cast<const unsigned char*>(pl->d_ctab), pl->ctab_stride));
+                                    static_cast<const unsigned char*>(pl->d_ctab[lay]),
+                                    pl->ctab_stride[lay]));
     mark(ev, nev, 1, s);
     note_launches(1);
     if (g.trace) {
@@ -896,6 +894,18 @@ int launch(const psw_plan* pl, const CChoice& ch, const void* F, int64_t ldf, vo
 }
 
 }  // namespace
+
+int build_cluster_tables(psw_plan* pl, const std::vector<FusedFwd<double>>& ff,
+                         const std::vector<FusedBwd<double>>& fb) {
+    for (int lay : {PSW_LAYOUT_R, PSW_LAYOUT_S}) {
+        const CChoice ch = choose(pl, lay);
+        if (ch.G <= 0) continue;
+        const int rc = pl->dtype == PSW_F64 ? cluster_tables<double>(pl, ch, lay, ff, fb)
+                                            : cluster_tables<float>(pl, ch, lay, ff, fb);
+        if (rc != PSW_OK) return rc;
+    }
+    return PSW_OK;
+}
 
 bool cluster_supported(const psw_plan* pl, int layout, int64_t N, const void* F, int64_t ldf) {
     if ((layout != PSW_LAYOUT_R && layout != PSW_LAYOUT_S) || N < 1 || N > (int64_t{1} << 31))

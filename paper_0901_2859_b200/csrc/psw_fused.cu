@@ -849,14 +849,17 @@ int build_fused_tables(psw_plan* pl, const std::vector<double>& rp, const std::v
     PSW_CUDA_TRY(cudaMalloc(&pl->d_segoff, sizeof(int32_t) * (P + 1)));
     PSW_CUDA_TRY(cudaMemcpy(pl->d_segoff, off.data(), sizeof(int32_t) * (P + 1), cudaMemcpyHostToDevice));
     pl->info.device_bytes += int64_t(sizeof(SegDesc) * NS + sizeof(int32_t) * (P + 1));
-    return pl->dtype == PSW_F64 ? upload_fused<double>(pl, ff, fb, seg)
-                                : upload_fused<float>(pl, ff, fb, seg);
+    const int rc = pl->dtype == PSW_F64 ? upload_fused<double>(pl, ff, fb, seg)
+                                        : upload_fused<float>(pl, ff, fb, seg);
+    if (rc != PSW_OK) return rc;
+    if (int r = build_rs_tables(pl, desc, seg, ff, fb)) return r;
+    return pl->world == 1 ? build_cluster_tables(pl, ff, fb) : PSW_OK;
 }
 
 int set_trace(void* buf) {
     unsigned long long* p = static_cast<unsigned long long*>(buf);
     PSW_CUDA_TRY(cudaMemcpyToSymbol(g_trace, &p, sizeof(p)));
-    return set_pipe_trace(buf);
+    return PSW_OK;
 }
 
 bool fused_supported(const psw_plan* pl, int layout, int64_t N, const void* F, int64_t ldf) {

@@ -82,6 +82,28 @@ struct SegDesc {  // rows [a, b) of block t
     int32_t a, b, t, pad;
 };
 
+// RESWEEP (psw_resweep.cu): the segments of the plan's own blocks are taken
+// kRsSeg at a time by one CTA ("group"); a run is the part of a group inside
+// one block. Per run the K1 kernel leaves four aggregates per RHS, folded over
+// the run's segments; the matrix-only aggregate of a run is a SegCoef
+// (mu_end = prod mu_end, k1, k2, nu of the composed affine map).
+constexpr int kRsSeg = 8;    // segments per group (one warp each)
+struct RsGroup {
+    int32_t s0, s1;  // segments [s0, s1)
+    int32_t r0, r1;  // runs [r0, r1)
+    int32_t ra, rb;  // rows [ra, rb) (global, 0-based)
+    int32_t pad0, pad1;
+};
+struct RsRun {
+    int32_t s0, s1;  // segments [s0, s1) of block t
+    int32_t t, tl;   // global block, block index local to the plan's range
+};
+// per-row coefficients of the RESWEEP solve kernel (K3)
+template <typename T>
+struct alignas(16) SolveCoef {
+    T rp, ma, lam, mu, w, al;
+};
+
 }  // namespace psw
 
 // The plan: immutable after psw_plan_create.
@@ -115,25 +137,23 @@ struct psw_plan {
     psw::SegDesc* d_segdesc = nullptr; // per segment rows / block
     int32_t* d_segoff = nullptr;       // [P+1] first segment of every block
     // CLUSTER path: per-cluster-rank coefficient tables in the kernel's shared
-    // memory layout, built at the first CLUSTER solve (psw_cluster.cu)
-    mutable void* d_ctab = nullptr;
-    mutable int64_t ctab_key = 0, ctab_stride = 0;
+    // memory layout, one per layout, built with the plan (psw_cluster.cu)
+    void* d_ctab[2] = {nullptr, nullptr};
+    int64_t ctab_stride[2] = {0, 0};
     std::vector<int32_t> seg_off;      // host copy
+
+    // RESWEEP tables over the plan's own segments (psw_resweep.cu)
+    int rs_ngroups = 0, rs_nruns = 0;
+    psw::RsGroup* d_rs_group = nullptr;
+    psw::RsRun* d_rs_run = nullptr;
+    psw::SegCoef* d_rs_runcoef = nullptr;  // composed affine map of every run
+    int32_t* d_rs_runoff = nullptr;        // [Ploc + 1] first run of every own block
+    void* d_scoef = nullptr;               // SolveCoef<T>[n]
 
     // multi-GPU row shard (psw_shard_*); world == 1 for a full plan
     int rank = 0, world = 1;
     int64_t blk0 = 0, blk1 = 0;   // owned blocks [blk0, blk1)
     int64_t row0 = 0, row1 = 0;   // owned rows [row0, row1) (0-based, global)
-    int64_t ncoarse = 0;          // coarse boundaries (world - 1)
-    int64_t npartials = 0;        // partial sums per RHS exchanged
-    // per coarse partial-sum slot: (segment kl, kr, target e); device copy
-    std::vector<int32_t> partial_spec;  // 3 * npartials
-    int32_t* d_partial_spec = nullptr;
-    // coarse items and local items of this rank (level order)
-    std::vector<psw::CombineItem> coarse_items, local_items;
-    psw::CombineItem* d_coarse_items = nullptr;
-    psw::CombineItem* d_local_items = nullptr;
-    int32_t* d_partial_index = nullptr;  // per coarse item: slots of its 3 sums
 };
 
 namespace psw {
@@ -153,37 +173,45 @@ int build_fused_tables(psw_plan* pl, const std::vector<double>& rp, const std::v
 // no FP contraction).
 std::vector<double> combine_matrix(const psw_plan* pl, const std::vector<double>& zr,
                                    const std::vector<double>& zl);
-bool pipe_supported(const psw_plan* plan, int layout, int64_t N, const void* F, int64_t ldf,
-                    const void* X, int64_t ldx);
-int solve_pipe(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx, int64_t N,
-               int layout, cudaStream_t s, void** events, int nevents);
-bool tile_supported(const psw_plan* plan, int layout, int64_t N);
-bool chunked_supported(const psw_plan* plan, int layout, int64_t N);
-int solve_chunked(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
-                  int64_t N, int layout, cudaStream_t s, void** events, int nevents);
 bool cluster_supported(const psw_plan* plan, int layout, int64_t N, const void* F, int64_t ldf);
 int solve_cluster(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
                   int64_t N, int layout, cudaStream_t s, void** events, int nevents);
+// CLUSTER coefficient tables of both layouts (psw_cluster.cu), built with the plan
+int build_cluster_tables(psw_plan* pl, const std::vector<FusedFwd<double>>& ff,
+                         const std::vector<FusedBwd<double>>& fb);
+
+// RESWEEP (psw_resweep.cu): K1 part -> K2 combination -> K3 solve.
 bool resweep_supported(const psw_plan* plan, int layout, int64_t N);
 int solve_resweep(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
                   int64_t N, int layout, cudaStream_t s, void** events, int nevents);
+// the same kernels over RHS chunks sized for L2, chunks on forked streams
+bool chunked_supported(const psw_plan* plan, int layout, int64_t N);
+int solve_chunked(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
+                  int64_t N, int layout, cudaStream_t s, void** events, int nevents);
+// RESWEEP tables (groups, runs, solve coefficients) over the plan's own blocks
+int build_rs_tables(psw_plan* pl, const std::vector<SegDesc>& desc,
+                    const std::vector<SegCoef>& seg, const std::vector<FusedFwd<double>>& ff,
+                    const std::vector<FusedBwd<double>>& fb);
+// row shards (psw_shard.cpp): forward = K1 + fold + the rank's share of the
+// boundary values; backward = carries from the reduced values + K3
+int64_t shard_workspace_bytes(const psw_plan* pl, int64_t N);
+int shard_forward(const psw_plan* pl, const void* F, int64_t ldf, int64_t N, void* ws,
+                  double* partials, cudaStream_t s);
+int shard_backward(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_t ldx,
+                   int64_t N, void* ws, const double* V, cudaStream_t s);
+// AUTO path selection (psw_plan.cpp)
+int auto_path(const psw_plan* pl, const void* F, int64_t ldf, const void* X, int64_t ldx,
+              int64_t N, int layout);
 // the STAGED dichotomy combination kernel (betas -> boundary values V, p x N)
 int launch_combine(const psw_plan* plan, const double* bl, const double* br, int64_t N, double* V,
                    cudaStream_t s);
-int solve_tile(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx, int64_t N,
-               int layout, cudaStream_t s, void** events, int nevents);
 int solve_fused(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
                 int64_t N, int layout, cudaStream_t s, void** events, int nevents);
 // records events[i] (if present) on s
 inline void mark(void** events, int nevents, int i, cudaStream_t s) {
     if (events && i < nevents && events[i]) cudaEventRecord(static_cast<cudaEvent_t>(events[i]), s);
 }
-int shard_forward(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
-                  int64_t N, double* partials, cudaStream_t s);
-int shard_backward(const psw_plan* plan, void* X, int64_t ldx, int64_t N, const double* partials,
-                   cudaStream_t s);
-int set_trace(void* buf);  // psw_debug_trace (FUSED kernel phase stamps, PIPE item trace)
-int set_pipe_trace(void* buf);
+int set_trace(void* buf);  // psw_debug_trace (FUSED kernel phase stamps)
 int fill_uniform(void* dst, int dtype, int64_t count, uint64_t seed, uint64_t offset, double lo,
                  double hi, cudaStream_t s);
 int fill_normal(void* dst, int dtype, int64_t count, uint64_t seed, uint64_t offset,

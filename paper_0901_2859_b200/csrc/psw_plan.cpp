@@ -323,8 +323,9 @@ void free_plan(psw_plan* pl) {
     cudaSetDevice(pl->device);
     void* ptrs[] = {pl->d_fwd, pl->d_bwd, pl->d_blk, pl->d_zr, pl->d_zl, pl->d_items,
                     pl->d_lvl_off, pl->d_ffwd, pl->d_fbwd, pl->d_seg, pl->d_cmat,
-                    pl->d_segdesc, pl->d_segoff, pl->d_ctab,
-                    pl->d_partial_spec, pl->d_coarse_items, pl->d_local_items, pl->d_partial_index};
+                    pl->d_segdesc, pl->d_segoff, pl->d_ctab[0], pl->d_ctab[1],
+                    pl->d_rs_group, pl->d_rs_run, pl->d_rs_runcoef, pl->d_rs_runoff,
+                    pl->d_scoef};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     cudaSetDevice(prev);
@@ -369,7 +370,6 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
                int rank, int world, std::vector<double>* cmat_host = nullptr, bool shard = false,
                int strategy = PSW_GROW_AUTO);
 
-int build_shard_tables(psw_plan* pl, const std::vector<double>& cmat);  // psw_shard.cu
 int device_preliminary(int64_t n, const double* sub, const double* diag, const double* sup,
                        int64_t p, const int64_t* bnd, const std::vector<int32_t>& blk,
                        std::vector<double>& gr, std::vector<double>& gl, std::vector<double>& zr,
@@ -429,6 +429,14 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
     for (int64_t t = 0; t <= p; ++t) {
         pl->blk[2 * t] = int32_t(t == 0 ? 0 : bnd[t - 1] - 1);
         pl->blk[2 * t + 1] = int32_t(t == p ? n : bnd[t] - 1);
+    }
+    // owned blocks and rows: rank r of `world` owns [r P/world, (r+1) P/world)
+    {
+        const int64_t Ploc = pl->P / world;
+        pl->blk0 = int64_t(rank) * Ploc;
+        pl->blk1 = pl->blk0 + Ploc;
+        pl->row0 = pl->blk[2 * pl->blk0];
+        pl->row1 = pl->blk[2 * (pl->blk1 - 1) + 1];
     }
     pl->uniform = (n % pl->P == 0);
     if (pl->uniform) {
@@ -626,10 +634,10 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
     }
     int rc = (dtype == PSW_F64) ? upload<double>(pl, rp, ma, gr, gl, w, alv, zr, zl)
                                 : upload<float>(pl, rp, ma, gr, gl, w, alv, zr, zl);
-    if (rc == PSW_OK && world == 1)
+    if (rc == PSW_OK)
         rc = build_fused_tables(pl, rp, ma, gr, gl, w, alv,
-                                pl->P <= 1024 ? combine_matrix(pl, zr, zl) : std::vector<double>());
-    if (rc == PSW_OK && shard) rc = build_shard_tables(pl, combine_matrix(pl, zr, zl));
+                                pl->P <= 1024 || shard ? combine_matrix(pl, zr, zl)
+                                                       : std::vector<double>());
     cudaSetDevice(prev_dev);
     if (rc != PSW_OK) {
         free_plan(pl);
@@ -709,6 +717,29 @@ std::vector<double> combine_matrix(const psw_plan* pl, const std::vector<double>
     return M;
 }
 
+}  // namespace psw
+
+namespace psw {
+// AUTO path choice (measured on B200): the on-chip paths first
+// (CLUSTER for >= 128 RHS tiles of 128 B, FUSED), then the L2-chunked
+// RESWEEP when a 32-RHS column of F is small next to L2 (its second read
+// then hits L2), then RESWEEP, then STAGED.
+int auto_path(const psw_plan* pl, const void* F, int64_t ldf, const void* X, int64_t ldx,
+              int64_t N, int layout) {
+    (void)X;
+    (void)ldx;
+    const int64_t es = pl->dtype == PSW_F64 ? 8 : 4;
+    if (N * es >= 128 * 128 && cluster_supported(pl, layout, N, F, ldf)) return PSW_PATH_CLUSTER;
+    if (fused_supported(pl, layout, N, F, ldf)) return PSW_PATH_FUSED;
+    if (chunked_supported(pl, layout, N)) {
+        int l2 = 0;
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, pl->device);
+        const int64_t column = pl->n * es * 32;
+        if (l2 > 0 && column * 8 <= l2 && N * es * pl->n > int64_t(l2) / 2) return PSW_PATH_CHUNKED;
+    }
+    if (resweep_supported(pl, layout, N)) return PSW_PATH_RESWEEP;
+    return PSW_PATH_STAGED;
+}
 }  // namespace psw
 
 // ============================ C ABI ========================================
@@ -813,7 +844,7 @@ static int check_solve_args(const psw_plan* plan, const void* F, int64_t ldf, co
         return PSW_INVALID_ARGUMENT;
     }
     if (plan->world != 1) {
-        psw::set_error(PSW_INVALID_ARGUMENT, "sharded plan: use psw_shard_forward/backward");
+        psw::set_error(PSW_INVALID_ARGUMENT, "sharded plan: use psw_shard_solve (or psw_shard_forward/backward)");
         return PSW_INVALID_ARGUMENT;
     }
     return PSW_OK;
@@ -836,83 +867,43 @@ int psw_solve_ex(const psw_plan* plan, const void* F, int64_t ldf, void* X, int6
         opts && (opts->betas_left || opts->betas_right || opts->boundary_values);
     int rc;
     t_last_path = 0;
-    if (path == PSW_PATH_CHUNKED) {
-        t_last_path = PSW_PATH_CHUNKED;
-        if (want_intermediates || !psw::chunked_supported(plan, layout, nrhs)) {
-            psw::set_error(PSW_NOT_SUPPORTED, "chunked path does not support this plan/shape");
-            rc = PSW_NOT_SUPPORTED;
-        } else {
-            rc = psw::solve_chunked(plan, F, ldf, X, ldx, nrhs, layout, s,
-                                    opts ? opts->events : nullptr, opts ? opts->nevents : 0);
-        }
+    void** ev = opts ? opts->events : nullptr;
+    const int nev = opts ? opts->nevents : 0;
+    if (path == PSW_PATH_AUTO && !want_intermediates)
+        path = psw::auto_path(plan, F, ldf, X, ldx, nrhs, layout);
+    t_last_path = path;
+    auto unsupported = [&](const char* name) {
+        psw::set_error(PSW_NOT_SUPPORTED, std::string(name) + " path does not support this plan/shape");
+        return int(PSW_NOT_SUPPORTED);
+    };
+    if (path != PSW_PATH_STAGED && path != PSW_PATH_AUTO && want_intermediates) {
+        rc = unsupported("only the staged");
+    } else if (path == PSW_PATH_CHUNKED) {
+        rc = psw::chunked_supported(plan, layout, nrhs)
+                 ? psw::solve_chunked(plan, F, ldf, X, ldx, nrhs, layout, s, ev, nev)
+                 : unsupported("chunked");
     } else if (path == PSW_PATH_CLUSTER) {
-        t_last_path = PSW_PATH_CLUSTER;
-        if (want_intermediates || !psw::cluster_supported(plan, layout, nrhs, F, ldf)) {
-            psw::set_error(PSW_NOT_SUPPORTED, "cluster path does not support this plan/shape");
-            rc = PSW_NOT_SUPPORTED;
-        } else {
-            rc = psw::solve_cluster(plan, F, ldf, X, ldx, nrhs, layout, s,
-                                    opts ? opts->events : nullptr, opts ? opts->nevents : 0);
-        }
+        rc = psw::cluster_supported(plan, layout, nrhs, F, ldf)
+                 ? psw::solve_cluster(plan, F, ldf, X, ldx, nrhs, layout, s, ev, nev)
+                 : unsupported("cluster");
     } else if (path == PSW_PATH_RESWEEP) {
-        t_last_path = PSW_PATH_RESWEEP;
-        if (want_intermediates || !psw::resweep_supported(plan, layout, nrhs)) {
-            psw::set_error(PSW_NOT_SUPPORTED, "resweep path does not support this plan/shape");
-            rc = PSW_NOT_SUPPORTED;
-        } else {
-            rc = psw::solve_resweep(plan, F, ldf, X, ldx, nrhs, layout, s,
-                                    opts ? opts->events : nullptr, opts ? opts->nevents : 0);
-        }
-    } else if (path == PSW_PATH_TILE) {
-        t_last_path = PSW_PATH_TILE;
-        if (want_intermediates || !psw::tile_supported(plan, layout, nrhs)) {
-            psw::set_error(PSW_NOT_SUPPORTED, "tile path does not support this plan/shape");
-            rc = PSW_NOT_SUPPORTED;
-        } else {
-            rc = psw::solve_tile(plan, F, ldf, X, ldx, nrhs, layout, s,
-                                 opts ? opts->events : nullptr, opts ? opts->nevents : 0);
-        }
-    } else if (path == PSW_PATH_PIPE) {
-        t_last_path = PSW_PATH_PIPE;
-        if (want_intermediates || !psw::pipe_supported(plan, layout, nrhs, F, ldf, X, ldx)) {
-            psw::set_error(PSW_NOT_SUPPORTED, "pipe path does not support this plan/shape");
-            rc = PSW_NOT_SUPPORTED;
-        } else {
-            rc = psw::solve_pipe(plan, F, ldf, X, ldx, nrhs, layout, s,
-                                 opts ? opts->events : nullptr, opts ? opts->nevents : 0);
-        }
-    } else if (path == PSW_PATH_FUSED && !psw::fused_supported(plan, layout, nrhs, F, ldf)) {
-        psw::set_error(PSW_NOT_SUPPORTED, "fused path does not support this plan/shape");
-        rc = PSW_NOT_SUPPORTED;
-    } else if (path == PSW_PATH_AUTO && !want_intermediates &&
-               nrhs * (plan->dtype == PSW_F64 ? 8 : 4) >= 128 * 128 &&
-               psw::cluster_supported(plan, layout, nrhs, F, ldf)) {
-        // >= 128 RHS tiles of 128 B: measured C1 (256 tiles) CLUSTER 88.8 us vs
-        // FUSED 93.2 us; C0 (16 tiles) CLUSTER 22.9 us vs FUSED 14.2 us
-        t_last_path = PSW_PATH_CLUSTER;
-        rc = psw::solve_cluster(plan, F, ldf, X, ldx, nrhs, layout, s,
-                                opts ? opts->events : nullptr, opts ? opts->nevents : 0);
-    } else if ((path == PSW_PATH_FUSED || path == PSW_PATH_AUTO) && !want_intermediates &&
-               psw::fused_supported(plan, layout, nrhs, F, ldf)) {
-        t_last_path = PSW_PATH_FUSED;
-        rc = psw::solve_fused(plan, F, ldf, X, ldx, nrhs, layout, s, opts ? opts->events : nullptr,
-                              opts ? opts->nevents : 0);
-    } else if (path == PSW_PATH_AUTO && !want_intermediates &&
-               psw::resweep_supported(plan, layout, nrhs)) {
-        // beyond the CLUSTER/FUSED paths' reach (large blocks, layout S): 3 s
-        // bytes per unknown instead of STAGED's 4 s (measured C3 4.6 vs 6.3 ms,
-        // C4 rows 126 vs 195 us, C2 fp32 at P = 8..512: 11.1-13.1 vs 12.8-13.9 ms,
-        // profiles/r01_c2_partition_sweep.txt)
-        t_last_path = PSW_PATH_RESWEEP;
-        rc = psw::solve_resweep(plan, F, ldf, X, ldx, nrhs, layout, s,
-                                opts ? opts->events : nullptr, opts ? opts->nevents : 0);
-    } else {
+        rc = psw::resweep_supported(plan, layout, nrhs)
+                 ? psw::solve_resweep(plan, F, ldf, X, ldx, nrhs, layout, s, ev, nev)
+                 : unsupported("resweep");
+    } else if (path == PSW_PATH_FUSED) {
+        rc = psw::fused_supported(plan, layout, nrhs, F, ldf)
+                 ? psw::solve_fused(plan, F, ldf, X, ldx, nrhs, layout, s, ev, nev)
+                 : unsupported("fused");
+    } else if (path == PSW_PATH_STAGED || path == PSW_PATH_AUTO) {
         t_last_path = PSW_PATH_STAGED;
         rc = psw::solve_staged(plan, F, ldf, X, ldx, nrhs, layout, s,
                                opts ? opts->betas_left : nullptr,
                                opts ? opts->betas_right : nullptr,
-                               opts ? opts->boundary_values : nullptr,
-                               opts ? opts->events : nullptr, opts ? opts->nevents : 0);
+                               opts ? opts->boundary_values : nullptr, ev, nev);
+    } else {
+        t_last_path = 0;
+        psw::set_error(PSW_NOT_SUPPORTED, "unknown or retired solve path " + std::to_string(path));
+        rc = PSW_NOT_SUPPORTED;
     }
     if (prev != plan->device) cudaSetDevice(prev);
     return rc;

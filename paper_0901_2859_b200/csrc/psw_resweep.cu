@@ -1,6 +1,13 @@
 // RESWEEP solve path: F is read twice and X written once (3 s bytes per
-// unknown instead of the STAGED path's 4 s); nothing of size n x N besides F
-// and X touches HBM. Any partition; both layouts.
+// unknown; the intermediates are a few aggregates per 256 rows), any
+// partition, both layouts. The same kernels serve three drivers:
+//   solve_resweep   all RHS at once (the 2^20-row config C3: one 16-RHS
+//                   column of F is 128 MB, no single-read scheme fits on chip)
+//   solve_chunked   RHS chunks sized for L2 on forked streams: K3's second
+//                   read of a chunk hits L2, so HBM sees F once (fp32 C2:
+//                   a 32-RHS column of F is 8 MB)
+//   shard_forward / shard_backward   a rank's own blocks of a row-sharded
+//                   solve (psw_shard.cpp), around one all-reduce
 //
 // Every block is cut into segments of kSegLen rows (the last one of a block
 // takes the rest, build_fused_tables). In the affine form of the unit-row
@@ -10,23 +17,28 @@
 // a segment [a, b) swept from a zero carry (d~) is exact after
 // d_q = d~_q + mu_q D_{a-1}, and its back substitution after the carry
 // x_a = Lam~ + D_{a-1} K1 + x_l K2 + nu x_b (Lam~ = sum lam_q d~_q).
+// A CTA ("group") takes kRsSeg consecutive segments x 32 RHS (warp = segment,
+// lane = RHS); the part of a group inside one block is a "run", whose
+// segments compose into one affine map of the same form (run SegCoef).
 //
-//   K1 part     one thread per (rhs k, segment): the segment's F rows (all
-//               loads in flight), d~ from zero, Lam~ and the two beta dot
-//               products of the segment (betas.hpp:42-57 split by segment).
-//   K2 comb     per (rhs k, block t): forward fold of the segment partials
-//               (exact carries D_{a-1}, block betas), boundary values V
-//               (P <= 64: the tabulated combination matrix, psw_plan.cpp
-//               combine_matrix; otherwise the STAGED level-order dichotomy,
-//               boundary_solve.hpp:96-121), backward fold (x_b per segment).
-//   K3 solve    one thread per (rhs k, segment): F rows read again, forward
-//               sweep from the exact carry, back substitution from the exact
-//               x_b, X streamed out.
-// K3 walks the segments in the reverse of K1's order: the F rows K1 read
-// last are still in L2 when K3 starts (C1: F = 128 MB, L2 = 126 MB).
+//   K1 part    the group's F rows (all loads in flight), d~ from zero, Lam~
+//              and the two beta dot products per segment (betas.hpp:42-57
+//              split by segment); one warp per run folds its segments:
+//              run d~ end, run Lam, run beta partials -> scratch.
+//   K2         per (RHS, block): forward fold over the block's runs (exact
+//              run carries D_in, block betas), boundary values V (P <= 64:
+//              the tabulated combination matrix, psw_plan.cpp
+//              combine_matrix; otherwise the STAGED level-order dichotomy,
+//              boundary_solve.hpp:96-121), backward fold (x at every run's end).
+//   K3 solve   F rows read again, d~ from zero, one warp per run rebuilds
+//              the exact segment carries from the run's (D_in, x_B), back
+//              substitution, X streamed out. Groups in the reverse of K1's
+//              order (the rows K1 read last are the likeliest L2 hits).
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 #include <type_traits>
+#include <vector>
 
 #include "psw_device.cuh"
 #include "psw_internal.h"
@@ -34,294 +46,34 @@
 namespace psw {
 namespace {
 
-constexpr int kThreads = 128;
+constexpr int kRsThreads = kRsSeg * 32;
 constexpr int kSegMax = kSegLen + 1;
+constexpr int kRsRows = kRsSeg * kSegMax;  // coefficient rows staged per group (bound)
+constexpr int kSPitch = kSegMax;           // layout S tile pitch (odd: conflict-free columns)
 
-// Scratch per (segment s, rhs k), [s * N + k]:
-//   pd  K1: d~ at the segment end      -> K2: D_{a-1} (exact carry into s)
-//   px  K1: Lam~                       -> K2: Lam~ + D_{a-1} K1
-//   pr  K1: segment right-beta partial -> K2: x_b (x at the row after s)
-//   pl  K1: segment left-beta partial
-template <typename T>
-struct Scratch {
-    T* pd;
-    T* px;
-    T* pr;  // partial sums accumulated in double, stored in the solve precision
-    T* pl;
-    int64_t ld;  // row pitch (>= N, a multiple of 32)
+// Per (run r, rhs k), [r * ld + k], all fp64:
+//   dt   K1: run d~ end (zero carry)  -> K2: D_in (exact carry into the run)
+//   lam  K1: run Lam (zero D_in, x_l, x_B)
+//   br   K1: run right-beta partial   -> K2: x_B (x at the row after the run)
+//   bl   K1: run left-beta partial
+struct RsScratch {
+    double* dt;
+    double* lam;
+    double* br;
+    double* bl;
+    int64_t ld;
 };
 
-// ------------------------------------------------------------------ K1
 template <typename T>
-__global__ void __launch_bounds__(kThreads) rs_part_kernel(
-    const T* __restrict__ F, int64_t ldf, int64_t N, const SegDesc* __restrict__ desc,
-    const FusedFwd<T>* __restrict__ ff, Scratch<T> sc) {
-    __shared__ FusedFwd<T> cs[kSegMax];
-    const int s = blockIdx.y;
-    const int64_t k = int64_t(blockIdx.x) * kThreads + threadIdx.x;
-    const bool kv = k < N;
-    const SegDesc sd = desc[s];
-    const int a = sd.a, len = sd.b - sd.a;
-    const T* fp = F + int64_t(a) * ldf + (kv ? k : 0);
-    // segments of >= 31 rows (every segment of a uniform partition) run
-    // their first 31 rows unpredicated: a fully predicated 33-row sweep is
-    // several times slower
-    T d = T(0), lx = T(0);
-    double br = 0.0, bl = 0.0;
-    auto sweep = [&](auto full) {
-        constexpr bool FULL = decltype(full)::value;
-        T v[kSegMax];
-        if (kv) {
-#pragma unroll
-            for (int r = 0; r < kSegMax; ++r)
-                if ((FULL && r < kSegLen - 1) || r < len) v[r] = fp[int64_t(r) * ldf];
-        }
-        for (int i = threadIdx.x; i < len; i += kThreads) cs[i] = ff[a + i];
-        __syncthreads();
-        if (!kv) return;
-#pragma unroll
-        for (int r = 0; r < kSegMax; ++r) {
-            if ((FULL && r < kSegLen - 1) || r < len) {
-                const FusedFwd<T> c = cs[r];
-                d = fma(c.ma, d, v[r] * c.rp);
-                br = fma(double(v[r]), double(c.gr), br);
-                bl = fma(double(v[r]), double(c.gl), bl);
-                lx = fma(c.lam, d, lx);
-            }
-        }
-    };
-    if (len >= kSegLen - 1)
-        sweep(std::true_type{});
-    else
-        sweep(std::false_type{});
-    if (!kv) return;
-    const int64_t o = int64_t(s) * sc.ld + k;
-    sc.pd[o] = d;
-    sc.px[o] = lx;
-    sc.pr[o] = T(br);
-    sc.pl[o] = T(bl);
+__device__ __forceinline__ T ld_stream(const T* p) {
+    return __ldcs(p);
 }
 
-// ------------------------------------------------------------------ K2
-// Forward fold of block t for rhs k: exact carries and block betas.
-template <typename T, int U = 8>
-__device__ __forceinline__ void fold_fwd(const Scratch<T>& sc, const SegCoef* __restrict__ segc,
-                                         int s0, int s1, int64_t N, int64_t k, double& R,
-                                         double& L) {
-    // U segments' partials in flight per thread
-    double D = 0.0;
-    R = 0.0;
-    L = 0.0;
-    for (int lo = s0; lo < s1; lo += U) {
-        T dv[U], xv[U], rv[U], lv[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            if (lo + u < s1) {
-                const int64_t o = int64_t(lo + u) * sc.ld + k;
-                dv[u] = sc.pd[o];
-                xv[u] = sc.px[o];
-                rv[u] = sc.pr[o];
-                lv[u] = sc.pl[o];
-            }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            if (lo + u < s1) {
-                const SegCoef c = segc[lo + u];
-                const int64_t o = int64_t(lo + u) * sc.ld + k;
-                sc.pd[o] = T(D);
-                sc.px[o] = T(fma(D, c.k1, double(xv[u])));
-                R += double(rv[u]);
-                L += double(lv[u]);
-                D = fma(c.mu_end, D, double(dv[u]));
-            }
-    }
-}
-
-// Backward fold of block t for rhs k from x at row e_t: x_b of every segment.
-template <typename T>
-__device__ __forceinline__ void fold_bwd(const Scratch<T>& sc, const SegCoef* __restrict__ segc,
-                                         int s0, int s1, int64_t N, int64_t k, double xl,
-                                         double xb) {
-    constexpr int U = 8;
-    for (int hi = s1; hi > s0; hi -= U) {
-        T av[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            if (hi - 1 - u >= s0) av[u] = sc.px[int64_t(hi - 1 - u) * sc.ld + k];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int sg = hi - 1 - u;
-            if (sg >= s0) {
-                const SegCoef c = segc[sg];
-                sc.pr[int64_t(sg) * sc.ld + k] = T(xb);
-                xb = fma(c.nu, xb, fma(xl, c.k2, double(av[u])));
-            }
-        }
-    }
-}
-
-// P <= kCombMaxP with a combination matrix: one CTA per 32 RHS, warp w
-// handles blocks w, w + kCombWarps, ... in both phases; the block betas of
-// the CTA's RHS meet in shared memory.
-constexpr int kCombWarps = 16;
-constexpr int kCombMaxP = 64;
-
-// one boundary value: row m of the combination matrix times the betas
-__device__ __forceinline__ double cmat_row(const double* __restrict__ m,
-                                           const double (*sb)[32], int len, int lane) {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int u = 0;
-    for (; u + 4 <= len; u += 4) {
-        a0 = fma(m[u], sb[u][lane], a0);
-        a1 = fma(m[u + 1], sb[u + 1][lane], a1);
-        a2 = fma(m[u + 2], sb[u + 2][lane], a2);
-        a3 = fma(m[u + 3], sb[u + 3][lane], a3);
-    }
-    for (; u < len; ++u) a0 = fma(m[u], sb[u][lane], a0);
-    return (a0 + a1) + (a2 + a3);
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kCombWarps * 32) rs_comb_kernel(
-    int64_t N, int P, int p, const int32_t* __restrict__ segoff, const SegCoef* __restrict__ segc,
-    const double* __restrict__ gcmat, Scratch<T> sc, double* __restrict__ V) {
-    __shared__ double sb[2 * kCombMaxP][32];  // [u] right_u, [P + u] left_u
-    extern __shared__ double cmat[];           // p x 2P combination matrix
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < p * 2 * P; i += blockDim.x) cmat[i] = gcmat[i];
-    const int64_t k = int64_t(blockIdx.x) * 32 + lane;
-    const bool kv = k < N;
-    for (int t = warp; t < P; t += kCombWarps) {
-        double R = 0.0, L = 0.0;
-        if (kv) fold_fwd(sc, segc, segoff[t], segoff[t + 1], N, k, R, L);
-        sb[t][lane] = t < p ? R : 0.0;      // betas.hpp:46-49
-        sb[P + t][lane] = t > 0 ? L : 0.0;  // betas.hpp:51-55
-    }
-    __syncthreads();
-    if (!kv) return;
-    for (int t = warp; t < P; t += kCombWarps) {
-        const double xl = t > 0 ? cmat_row(cmat + int64_t(t - 1) * 2 * P, sb, 2 * P, lane) : 0.0;
-        const double xb = t < p ? cmat_row(cmat + int64_t(t) * 2 * P, sb, 2 * P, lane) : 0.0;
-        if (t < p) V[int64_t(t) * sc.ld + k] = xb;
-        fold_bwd(sc, segc, segoff[t], segoff[t + 1], N, k, xl, xb);
-    }
-}
-
-// General P: the folds one thread per (rhs k, block t) around the STAGED
-// combination kernel.
-template <typename T>
-__global__ void __launch_bounds__(kThreads) rs_fold_kernel(
-    int64_t N, int p, const int32_t* __restrict__ segoff, const SegCoef* __restrict__ segc,
-    Scratch<T> sc, double* __restrict__ bl, double* __restrict__ br) {
-    const int t = blockIdx.y;
-    const int64_t k = int64_t(blockIdx.x) * kThreads + threadIdx.x;
-    if (k >= N) return;
-    double R, L;
-    // fp32: 16 segments in flight (the split fold is latency-bound: C2 comb
-    // 1.39 -> 1.08 ms); fp64 keeps 8 (16 costs occupancy: C3 comb 0.47 -> 0.60 ms)
-    fold_fwd<T, sizeof(T) == 4 ? 16 : 8>(sc, segc, segoff[t], segoff[t + 1], N, k, R, L);
-    if (t < p) br[int64_t(t) * sc.ld + k] = R;
-    if (t > 0) bl[int64_t(t) * sc.ld + k] = L;
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kThreads) rs_carry_kernel(
-    int64_t N, int p, const int32_t* __restrict__ segoff, const SegCoef* __restrict__ segc,
-    Scratch<T> sc, const double* __restrict__ V) {
-    const int t = blockIdx.y;
-    const int64_t k = int64_t(blockIdx.x) * kThreads + threadIdx.x;
-    if (k >= N) return;
-    const double xl = t > 0 ? V[int64_t(t - 1) * sc.ld + k] : 0.0;
-    const double xb = t < p ? V[int64_t(t) * sc.ld + k] : 0.0;
-    fold_bwd(sc, segc, segoff[t], segoff[t + 1], N, k, xl, xb);
-}
-
-// Boundary values from the combination matrix, one thread per (rhs k,
-// boundary j): V[j] = sum_u MR[j][u] right_u + ML[j][u] left_u
-// (right_p and left_0 do not exist, betas.hpp:46-55).
-__global__ void __launch_bounds__(kThreads) rs_vmat_kernel(
-    int64_t N, int64_t ld, int P, int p, const double* __restrict__ cmat,
-    const double* __restrict__ bl, const double* __restrict__ br, double* __restrict__ V) {
-    const int j = blockIdx.y;
-    const int64_t k = int64_t(blockIdx.x) * kThreads + threadIdx.x;
-    if (k >= N) return;
-    const double* m = cmat + int64_t(j) * 2 * P;
-    double a0 = 0.0, a1 = 0.0;
-#pragma unroll 4
-    for (int u = 0; u < P; ++u) {
-        if (u < p) a0 = fma(m[u], br[int64_t(u) * ld + k], a0);
-        if (u > 0) a1 = fma(m[P + u], bl[int64_t(u) * ld + k], a1);
-    }
-    V[int64_t(j) * ld + k] = a0 + a1;
-}
-
-// ------------------------------------------------------------------ K3
-template <typename T>
-__global__ void __launch_bounds__(kThreads, 4) rs_solve_kernel(
-    const T* F, int64_t ldf, T* X, int64_t ldx, int64_t N, const SegDesc* __restrict__ desc,
-    const FwdCoef<T>* __restrict__ cf, const BwdCoef<T>* __restrict__ cb, Scratch<T> sc,
-    const double* __restrict__ V, int NS) {
-    __shared__ FwdCoef<T> csf[kSegMax];
-    __shared__ BwdCoef<T> csb[kSegMax];
-    const int s = NS - 1 - int(blockIdx.y);  // reverse of K1's order (L2 reuse)
-    const int64_t k = int64_t(blockIdx.x) * kThreads + threadIdx.x;
-    const bool kv = k < N;
-    const SegDesc sd = desc[s];
-    const int a = sd.a, len = sd.b - sd.a, t = sd.t;
-    const T* fp = F + int64_t(a) * ldf + (kv ? k : 0);
-    auto sweep = [&](auto full) {
-        constexpr bool FULL = decltype(full)::value;
-        T v[kSegMax];
-        if (kv) {
-#pragma unroll
-            for (int r = 0; r < kSegMax; ++r)
-                if ((FULL && r < kSegLen - 1) || r < len) v[r] = __ldcs(fp + int64_t(r) * ldf);
-        }
-        for (int i = threadIdx.x; i < len; i += kThreads) {
-            csf[i] = cf[a + i];
-            csb[i] = cb[a + i];
-        }
-        __syncthreads();
-        if (!kv) return;
-        const int64_t o = int64_t(s) * sc.ld + k;
-        T d = sc.pd[o];
-        T xn = T(sc.pr[o]);
-        const T xl = t > 0 ? T(V[int64_t(t - 1) * sc.ld + k]) : T(0);
-#pragma unroll
-        for (int r = 0; r < kSegMax; ++r) {
-            if ((FULL && r < kSegLen - 1) || r < len) {
-                d = fma(csf[r].ma, d, v[r] * csf[r].rp);
-                v[r] = d;
-            }
-        }
-        T* xp = X + int64_t(a) * ldx + k;
-#pragma unroll
-        for (int r = kSegMax - 1; r >= 0; --r) {
-            if ((FULL && r < kSegLen - 1) || r < len) {
-                xn = fma(csb[r].al, xn, fma(xl, csb[r].w, v[r]));
-                __stcs(xp + int64_t(r) * ldx, xn);
-            }
-        }
-    };
-    if (len >= kSegLen - 1)
-        sweep(std::true_type{});
-    else
-        sweep(std::false_type{});
-}
-
-// ------------------------------------------------------------ layout S
-// F[k * ldf + i]: every RHS is contiguous. One warp per (32 RHS, segment):
-// the segment's rows of its 32 RHS are loaded coalesced (cp.async, 256
-// contiguous bytes per instruction) into a [rhs][row] shared tile with an
-// odd row pitch (conflict-free per-lane sweeps), lane r sweeps RHS r. Four
-// warps of a CTA share one segment (its coefficient rows are staged once).
-constexpr int kSWarps = 4;
-constexpr int kSPitch = kSegMax;  // 33: odd pitch, conflict-free column access
-
+// layout S: the rows [a, a+len) of RHS k0..k0+nk-1 into tile[rhs][row]
+// (cp.async, 32 consecutive rows of one RHS per instruction)
 template <typename T>
 __device__ __forceinline__ void s_tile_load(T (*tile)[kSPitch], const T* src, int64_t ld, int len,
                                             int nk, int lane) {
-    // rows 0..31 by lane, row 32 (a 33-row segment) by lane = rhs
 #pragma unroll 4
     for (int j = 0; j < 32; ++j)
         if (j < nk && lane < len) {
@@ -339,215 +91,760 @@ __device__ __forceinline__ void s_tile_load(T (*tile)[kSPitch], const T* src, in
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kSWarps * 32) rs_part_s_kernel(
-    const T* __restrict__ F, int64_t ldf, int64_t N, const SegDesc* __restrict__ desc,
-    const FusedFwd<T>* __restrict__ ff, Scratch<T> sc) {
-    __shared__ T tiles[kSWarps][32][kSPitch];
-    __shared__ FusedFwd<T> cs[kSegMax];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int s = blockIdx.y;
-    const int64_t k0 = (int64_t(blockIdx.x) * kSWarps + warp) * 32;
-    const int nk = k0 < N ? int(N - k0 < 32 ? N - k0 : 32) : 0;
-    const SegDesc sd = desc[s];
-    const int a = sd.a, len = sd.b - sd.a;
-    if (nk > 0) s_tile_load(tiles[warp], F + k0 * ldf + a, ldf, len, nk, lane);
-    for (int i = threadIdx.x; i < len; i += kSWarps * 32) cs[i] = ff[a + i];
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncthreads();
-    if (lane >= nk) return;
-    const T* col = tiles[warp][lane];
-    T d = T(0), lx = T(0);
-    double br = 0.0, bl = 0.0;
-    auto sweep = [&](auto full) {
-        constexpr bool FULL = decltype(full)::value;
-#pragma unroll
-        for (int r = 0; r < kSegMax; ++r) {
-            if ((FULL && r < kSegLen - 1) || r < len) {
-                const FusedFwd<T> c = cs[r];
-                const T f = col[r];
-                d = fma(c.ma, d, f * c.rp);
-                br = fma(double(f), double(c.gr), br);
-                bl = fma(double(f), double(c.gl), bl);
-                lx = fma(c.lam, d, lx);
-            }
-        }
-    };
-    if (len >= kSegLen - 1)
-        sweep(std::true_type{});
-    else
-        sweep(std::false_type{});
-    const int64_t o = int64_t(s) * sc.ld + k0 + lane;
-    sc.pd[o] = d;
-    sc.px[o] = lx;
-    sc.pr[o] = T(br);
-    sc.pl[o] = T(bl);
+// row r of a segment of length len is swept: the first kSegLen - 1 rows
+// unpredicated when the segment is full length (every segment of a uniform
+// partition: 31, 32 or 33 rows), else row by row
+template <bool FULL>
+__device__ __forceinline__ bool row_on(int r, int len) {
+    return (FULL && r < kSegLen - 1) || r < len;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kSWarps * 32) rs_solve_s_kernel(
-    const T* F, int64_t ldf, T* X, int64_t ldx, int64_t N, const SegDesc* __restrict__ desc,
-    const FwdCoef<T>* __restrict__ cf, const BwdCoef<T>* __restrict__ cb, Scratch<T> sc,
-    const double* __restrict__ V, int NS) {
-    __shared__ T tiles[kSWarps][32][kSPitch];
-    __shared__ FwdCoef<T> csf[kSegMax];
-    __shared__ BwdCoef<T> csb[kSegMax];
+// ------------------------------------------------------------------ K1
+template <typename T, bool LS>
+__global__ void __launch_bounds__(kRsThreads) rs_part_kernel(
+    const T* __restrict__ F, int64_t ldf, int64_t N, int32_t row0,
+    const RsGroup* __restrict__ groups, const RsRun* __restrict__ runs,
+    const SegDesc* __restrict__ desc, const SegCoef* __restrict__ segc,
+    const FusedFwd<T>* __restrict__ ff, RsScratch sc) {
+    __shared__ FusedFwd<T> cs[kRsRows];
+    __shared__ double s_d[kRsSeg][32], s_l[kRsSeg][32], s_r[kRsSeg][32], s_b[kRsSeg][32];
+    extern __shared__ __align__(16) unsigned char dyn[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int s = NS - 1 - int(blockIdx.y);  // reverse of K1's order (L2 reuse)
-    const int64_t k0 = (int64_t(blockIdx.x) * kSWarps + warp) * 32;
-    const int nk = k0 < N ? int(N - k0 < 32 ? N - k0 : 32) : 0;
-    const SegDesc sd = desc[s];
-    const int a = sd.a, len = sd.b - sd.a, t = sd.t;
-    if (nk > 0) s_tile_load(tiles[warp], F + k0 * ldf + a, ldf, len, nk, lane);
-    for (int i = threadIdx.x; i < len; i += kSWarps * 32) {
-        csf[i] = cf[a + i];
-        csb[i] = cb[a + i];
+    const RsGroup g = groups[blockIdx.y];
+    const int64_t k0 = int64_t(blockIdx.x) * 32;
+    const int64_t k = k0 + lane;
+    const int nk = int(N - k0 < 32 ? N - k0 : 32);
+    const bool kv = lane < nk;
+    const int sg = g.s0 + warp;
+    const bool sv = sg < g.s1;
+    int a = g.ra, len = 0;
+    if (sv) {
+        const SegDesc d = desc[sg];
+        a = d.a;
+        len = d.b - d.a;
     }
-    T d = T(0), xn = T(0), xl = T(0);
-    if (lane < nk) {  // the carries' loads overlap the tile's
-        const int64_t o = int64_t(s) * sc.ld + k0 + lane;
-        d = sc.pd[o];
-        xn = T(sc.pr[o]);
-        if (t > 0) xl = T(V[int64_t(t - 1) * sc.ld + k0 + lane]);
+    T v[kSegMax];
+    T(*tile)[kSPitch] = reinterpret_cast<T(*)[kSPitch]>(dyn) + warp * 32;
+    if constexpr (LS) {
+        if (sv) s_tile_load(tile, F + k0 * ldf + (a - row0), ldf, len, nk, lane);
+    } else if (kv && sv) {
+        const T* fp = F + int64_t(a - row0) * ldf + k;
+        if (len >= kSegLen - 1) {
+#pragma unroll
+            for (int r = 0; r < kSegMax; ++r)
+                if (row_on<true>(r, len)) v[r] = fp[int64_t(r) * ldf];
+        } else {
+#pragma unroll
+            for (int r = 0; r < kSegMax; ++r)
+                if (row_on<false>(r, len)) v[r] = fp[int64_t(r) * ldf];
+        }
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    for (int i = threadIdx.x; i < g.rb - g.ra; i += kRsThreads) cs[i] = ff[g.ra + i];
+    if constexpr (LS) asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
-    if (nk == 0) return;
-    T* col = tiles[warp][lane];
-    auto sweep = [&](auto full) {
-        constexpr bool FULL = decltype(full)::value;
+    T d = T(0), lx = T(0);
+    double br = 0.0, bl = 0.0;
+    if (kv && sv) {
+        const FusedFwd<T>* c = cs + (a - g.ra);
+        auto sweep = [&](auto full) {
+            constexpr bool FULL = decltype(full)::value;
 #pragma unroll
-        for (int r = 0; r < kSegMax; ++r) {
-            if ((FULL && r < kSegLen - 1) || r < len) {
-                d = fma(csf[r].ma, d, col[r] * csf[r].rp);
-                col[r] = d;
+            for (int r = 0; r < kSegMax; ++r) {
+                if (row_on<FULL>(r, len)) {
+                    const FusedFwd<T> q = c[r];
+                    const T f = LS ? tile[lane][r] : v[r];
+                    d = fma(q.ma, d, f * q.rp);
+                    br = fma(double(f), double(q.gr), br);
+                    bl = fma(double(f), double(q.gl), bl);
+                    lx = fma(q.lam, d, lx);
+                }
             }
-        }
-#pragma unroll
-        for (int r = kSegMax - 1; r >= 0; --r) {
-            if ((FULL && r < kSegLen - 1) || r < len) {
-                xn = fma(csb[r].al, xn, fma(xl, csb[r].w, col[r]));
-                col[r] = xn;
-            }
-        }
-    };
-    if (lane < nk) {
+        };
         if (len >= kSegLen - 1)
             sweep(std::true_type{});
         else
             sweep(std::false_type{});
     }
-    __syncwarp();
-    // coalesced write-back: RHS j's rows by lane (row 32 by lane = rhs)
-    T* dst = X + k0 * ldx + a;
+    s_d[warp][lane] = double(d);
+    s_l[warp][lane] = double(lx);
+    s_r[warp][lane] = br;
+    s_b[warp][lane] = bl;
+    __syncthreads();
+    const int run = g.r0 + warp;
+    if (run < g.r1 && kv) {
+        const RsRun rr = runs[run];
+        double D = 0.0, lam = 0.0, nupre = 1.0, R = 0.0, L = 0.0;
+        for (int s = rr.s0; s < rr.s1; ++s) {
+            const int j = s - g.s0;
+            const SegCoef q = segc[s];
+            lam = fma(nupre, fma(D, q.k1, s_l[j][lane]), lam);
+            D = fma(q.mu_end, D, s_d[j][lane]);
+            nupre *= q.nu;
+            R += s_r[j][lane];
+            L += s_b[j][lane];
+        }
+        const int64_t o = int64_t(run) * sc.ld + k;
+        sc.dt[o] = D;
+        sc.lam[o] = lam;
+        sc.br[o] = R;
+        sc.bl[o] = L;
+    }
+}
+
+// ------------------------------------------------------------------ K2
+// Forward fold of one block's runs [r0, r1) for rhs k: the exact carry into
+// every run (stored in place of its d~ end) and the block betas.
+__device__ __forceinline__ void fold_fwd(const RsScratch& sc, const SegCoef* __restrict__ rc,
+                                         int r0, int r1, int64_t k, double& R, double& L) {
+    constexpr int U = 8;  // runs' partials in flight per thread
+    double D = 0.0;
+    R = 0.0;
+    L = 0.0;
+    for (int lo = r0; lo < r1; lo += U) {
+        double dv[U], rv[U], lv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (lo + u < r1) {
+                const int64_t o = int64_t(lo + u) * sc.ld + k;
+                dv[u] = sc.dt[o];
+                rv[u] = sc.br[o];
+                lv[u] = sc.bl[o];
+            }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (lo + u < r1) {
+                sc.dt[int64_t(lo + u) * sc.ld + k] = D;
+                R += rv[u];
+                L += lv[u];
+                D = fma(rc[lo + u].mu_end, D, dv[u]);
+            }
+    }
+}
+
+// Backward fold of one block's runs from x at the block's closing row (x_b)
+// with the block's left boundary value xl: x at the end of every run.
+__device__ __forceinline__ void fold_bwd(const RsScratch& sc, const SegCoef* __restrict__ rc,
+                                         int r0, int r1, int64_t k, double xl, double xb) {
+    constexpr int U = 8;
+    for (int hi = r1; hi > r0; hi -= U) {
+        double lv[U], dv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (hi - 1 - u >= r0) {
+                const int64_t o = int64_t(hi - 1 - u) * sc.ld + k;
+                lv[u] = sc.lam[o];
+                dv[u] = sc.dt[o];
+            }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int r = hi - 1 - u;
+            if (r >= r0) {
+                const SegCoef q = rc[r];
+                sc.br[int64_t(r) * sc.ld + k] = xb;
+                xb = fma(q.nu, xb, fma(xl, q.k2, fma(dv[u], q.k1, lv[u])));
+            }
+        }
+    }
+}
+
+// P <= kCombMaxP with a combination matrix (whole-system plans): one CTA per
+// 32 RHS, warp w handles blocks w, w + kCombWarps, ... in both phases; the
+// block betas of the CTA's RHS meet in shared memory.
+constexpr int kCombWarps = 16;
+constexpr int kCombMaxP = 64;
+
+__device__ __forceinline__ double cmat_row(const double* __restrict__ m, const double (*sb)[32],
+                                           int len, int lane) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int u = 0;
+    for (; u + 4 <= len; u += 4) {
+        a0 = fma(m[u], sb[u][lane], a0);
+        a1 = fma(m[u + 1], sb[u + 1][lane], a1);
+        a2 = fma(m[u + 2], sb[u + 2][lane], a2);
+        a3 = fma(m[u + 3], sb[u + 3][lane], a3);
+    }
+    for (; u < len; ++u) a0 = fma(m[u], sb[u][lane], a0);
+    return (a0 + a1) + (a2 + a3);
+}
+
+__global__ void __launch_bounds__(kCombWarps * 32) rs_comb_kernel(
+    int64_t N, int P, int p, const int32_t* __restrict__ runoff, const SegCoef* __restrict__ rc,
+    const double* __restrict__ gcmat, RsScratch sc, double* __restrict__ V, int64_t ldv) {
+    __shared__ double sb[2 * kCombMaxP][32];  // [u] right_u, [P + u] left_u
+    extern __shared__ double cmat[];           // p x 2P combination matrix
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < p * 2 * P; i += blockDim.x) cmat[i] = gcmat[i];
+    const int64_t k = int64_t(blockIdx.x) * 32 + lane;
+    const bool kv = k < N;
+    for (int t = warp; t < P; t += kCombWarps) {
+        double R = 0.0, L = 0.0;
+        if (kv) fold_fwd(sc, rc, runoff[t], runoff[t + 1], k, R, L);
+        sb[t][lane] = t < p ? R : 0.0;      // betas.hpp:46-49
+        sb[P + t][lane] = t > 0 ? L : 0.0;  // betas.hpp:51-55
+    }
+    __syncthreads();
+    if (!kv) return;
+    for (int t = warp; t < P; t += kCombWarps) {
+        const double xl = t > 0 ? cmat_row(cmat + int64_t(t - 1) * 2 * P, sb, 2 * P, lane) : 0.0;
+        const double xb = t < p ? cmat_row(cmat + int64_t(t) * 2 * P, sb, 2 * P, lane) : 0.0;
+        if (t < p) V[int64_t(t) * ldv + k] = xb;
+        fold_bwd(sc, rc, runoff[t], runoff[t + 1], k, xl, xb);
+    }
+}
+
+// General P and row shards: the folds one thread per (rhs k, own block tl)
+// around the combination. Betas land at [tl * ld + k].
+__global__ void __launch_bounds__(128) rs_fold_kernel(int64_t N, const int32_t* __restrict__ runoff,
+                                                      const SegCoef* __restrict__ rc, RsScratch sc,
+                                                      double* __restrict__ bl,
+                                                      double* __restrict__ br) {
+    const int tl = blockIdx.y;
+    const int64_t k = int64_t(blockIdx.x) * 128 + threadIdx.x;
+    if (k >= N) return;
+    double R, L;
+    fold_fwd(sc, rc, runoff[tl], runoff[tl + 1], k, R, L);
+    br[int64_t(tl) * sc.ld + k] = R;
+    bl[int64_t(tl) * sc.ld + k] = L;
+}
+
+__global__ void __launch_bounds__(128) rs_carry_kernel(int64_t N, int p, int t0,
+                                                       const int32_t* __restrict__ runoff,
+                                                       const SegCoef* __restrict__ rc,
+                                                       RsScratch sc, const double* __restrict__ V,
+                                                       int64_t ldv) {
+    const int tl = blockIdx.y, t = t0 + tl;
+    const int64_t k = int64_t(blockIdx.x) * 128 + threadIdx.x;
+    if (k >= N) return;
+    const double xl = t > 0 ? V[int64_t(t - 1) * ldv + k] : 0.0;
+    const double xb = t < p ? V[int64_t(t) * ldv + k] : 0.0;
+    fold_bwd(sc, rc, runoff[tl], runoff[tl + 1], k, xl, xb);
+}
+
+// Row shards: the rank's share of every boundary value, one thread per
+// (rhs k, boundary j): V_r[j] = sum over own blocks t of MR[j][t] right_t +
+// ML[j][t] left_t (right_p and left_0 do not exist, betas.hpp:46-55).
+__global__ void __launch_bounds__(128) rs_vpart_kernel(int64_t N, int64_t ld, int P, int p, int t0,
+                                                       int nb, const double* __restrict__ cmat,
+                                                       const double* __restrict__ bl,
+                                                       const double* __restrict__ br,
+                                                       double* __restrict__ out) {
+    const int j = blockIdx.y;
+    const int64_t k = int64_t(blockIdx.x) * 128 + threadIdx.x;
+    if (k >= N) return;
+    const double* m = cmat + int64_t(j) * 2 * P;
+    double a0 = 0.0, a1 = 0.0;
+    for (int tl = 0; tl < nb; ++tl) {
+        const int t = t0 + tl;
+        if (t < p) a0 = fma(m[t], br[int64_t(tl) * ld + k], a0);
+        if (t > 0) a1 = fma(m[P + t], bl[int64_t(tl) * ld + k], a1);
+    }
+    out[int64_t(j) * N + k] = a0 + a1;
+}
+
+// ------------------------------------------------------------------ K3
+template <typename T, bool LS, bool STREAM>
+__global__ void __launch_bounds__(kRsThreads, 2) rs_solve_kernel(
+    const T* F, int64_t ldf, T* X, int64_t ldx, int64_t N, int32_t row0, int ngroups,
+    const RsGroup* __restrict__ groups, const RsRun* __restrict__ runs,
+    const SegDesc* __restrict__ desc, const SegCoef* __restrict__ segc,
+    const SolveCoef<T>* __restrict__ sco, RsScratch sc, const double* __restrict__ V,
+    int64_t ldv) {
+    __shared__ SolveCoef<T> cs[kRsRows];
+    __shared__ double s_d[kRsSeg][32], s_l[kRsSeg][32];
+    extern __shared__ __align__(16) unsigned char dyn[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const RsGroup g = groups[ngroups - 1 - int(blockIdx.y)];  // reverse of K1's order
+    const int64_t k0 = int64_t(blockIdx.x) * 32;
+    const int64_t k = k0 + lane;
+    const int nk = int(N - k0 < 32 ? N - k0 : 32);
+    const bool kv = lane < nk;
+    const int sg = g.s0 + warp;
+    const bool sv = sg < g.s1;
+    int a = g.ra, len = 0, t = 0;
+    if (sv) {
+        const SegDesc d = desc[sg];
+        a = d.a;
+        len = d.b - d.a;
+        t = d.t;
+    }
+    T v[kSegMax];
+    T(*tile)[kSPitch] = reinterpret_cast<T(*)[kSPitch]>(dyn) + warp * 32;
+    if constexpr (LS) {
+        if (sv) s_tile_load(tile, F + k0 * ldf + (a - row0), ldf, len, nk, lane);
+    } else if (kv && sv) {
+        const T* fp = F + int64_t(a - row0) * ldf + k;
+        if (len >= kSegLen - 1) {
+#pragma unroll
+            for (int r = 0; r < kSegMax; ++r)
+                if (row_on<true>(r, len)) v[r] = STREAM ? ld_stream(fp + int64_t(r) * ldf) : fp[int64_t(r) * ldf];
+        } else {
+#pragma unroll
+            for (int r = 0; r < kSegMax; ++r)
+                if (row_on<false>(r, len)) v[r] = STREAM ? ld_stream(fp + int64_t(r) * ldf) : fp[int64_t(r) * ldf];
+        }
+    }
+    for (int i = threadIdx.x; i < g.rb - g.ra; i += kRsThreads) cs[i] = sco[g.ra + i];
+    if constexpr (LS) asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    const SolveCoef<T>* c = cs + (a - g.ra);
+    const bool on = kv && sv;
+    // forward from a zero carry, d~ in place of f
+    T d = T(0), lx = T(0);
+    auto fwd = [&](auto full) {
+        constexpr bool FULL = decltype(full)::value;
+#pragma unroll
+        for (int r = 0; r < kSegMax; ++r) {
+            if (row_on<FULL>(r, len)) {
+                const SolveCoef<T> q = c[r];
+                const T f = LS ? tile[lane][r] : v[r];
+                d = fma(q.ma, d, f * q.rp);
+                lx = fma(q.lam, d, lx);
+                if (LS)
+                    tile[lane][r] = d;
+                else
+                    v[r] = d;
+            }
+        }
+    };
+    if (on) {
+        if (len >= kSegLen - 1)
+            fwd(std::true_type{});
+        else
+            fwd(std::false_type{});
+    }
+    s_d[warp][lane] = double(d);
+    s_l[warp][lane] = double(lx);
+    __syncthreads();
+    // exact segment carries of run g.r0 + warp from its (D_in, x_B)
+    const int run = g.r0 + warp;
+    if (run < g.r1 && kv) {
+        const RsRun rr = runs[run];
+        const int64_t o = int64_t(run) * sc.ld + k;
+        double D = sc.dt[o], x = sc.br[o];
+        const double xl = rr.t > 0 ? V[int64_t(rr.t - 1) * ldv + k] : 0.0;
+        for (int s = rr.s0; s < rr.s1; ++s) {
+            const int j = s - g.s0;
+            const double dd = s_d[j][lane];
+            s_d[j][lane] = D;
+            D = fma(segc[s].mu_end, D, dd);
+        }
+        for (int s = rr.s1 - 1; s >= rr.s0; --s) {
+            const int j = s - g.s0;
+            const SegCoef q = segc[s];
+            const double lam = s_l[j][lane];
+            s_l[j][lane] = x;
+            x = fma(q.nu, x, fma(xl, q.k2, fma(s_d[j][lane], q.k1, lam)));
+        }
+    }
+    __syncthreads();
+    if (on) {
+        const T D = T(s_d[warp][lane]);
+        T x = T(s_l[warp][lane]);
+        const T xl = t > 0 ? T(V[int64_t(t - 1) * ldv + k]) : T(0);
+        T* xp = X + int64_t(a - row0) * ldx + k;
+        auto bwd = [&](auto full) {
+            constexpr bool FULL = decltype(full)::value;
+#pragma unroll
+            for (int r = kSegMax - 1; r >= 0; --r) {
+                if (row_on<FULL>(r, len)) {
+                    const SolveCoef<T> q = c[r];
+                    const T dq = fma(q.mu, D, LS ? tile[lane][r] : v[r]);
+                    x = fma(q.al, x, fma(xl, q.w, dq));
+                    if (LS)
+                        tile[lane][r] = x;
+                    else
+                        __stcs(xp + int64_t(r) * ldx, x);
+                }
+            }
+        };
+        if (len >= kSegLen - 1)
+            bwd(std::true_type{});
+        else
+            bwd(std::false_type{});
+    }
+    if constexpr (LS) {
+        __syncwarp();
+        if (sv) {  // coalesced write-back: RHS j's rows by lane (row 32 by lane = rhs)
+            T* dst = X + k0 * ldx + (a - row0);
 #pragma unroll 4
-    for (int j = 0; j < 32; ++j)
-        if (j < nk && lane < len) __stcs(dst + int64_t(j) * ldx + lane, tiles[warp][j][lane]);
-    if (len > 32 && lane < nk) __stcs(dst + int64_t(lane) * ldx + 32, tiles[warp][lane][32]);
+            for (int j = 0; j < 32; ++j)
+                if (j < nk && lane < len) __stcs(dst + int64_t(j) * ldx + lane, tile[j][lane]);
+            if (len > 32 && lane < nk) __stcs(dst + int64_t(lane) * ldx + 32, tile[lane][32]);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ host
+struct Work {
+    RsScratch sc;
+    double* bl;  // own blocks x ld
+    double* br;
+    double* V;   // p x ldv (whole-system solves; shards pass their own)
+    int64_t ldv;
+};
+
+int64_t pad32(int64_t N) { return (N + 31) / 32 * 32; }
+
+size_t work_bytes(const psw_plan* pl, int64_t N, bool withV) {
+    const int64_t ld = pad32(N);
+    const int64_t nb = pl->blk1 - pl->blk0;
+    size_t b = sizeof(double) * size_t(ld) * (4 * size_t(pl->rs_nruns) + 2 * size_t(nb));
+    if (withV) b += sizeof(double) * size_t(ld) * size_t(std::max<int64_t>(pl->p, 1));
+    return b + 256;
+}
+
+Work carve(const psw_plan* pl, int64_t N, void* mem, bool withV) {
+    const int64_t ld = pad32(N);
+    const int64_t nb = pl->blk1 - pl->blk0;
+    double* c = static_cast<double*>(mem);
+    Work w;
+    w.sc.ld = ld;
+    const size_t rn = size_t(pl->rs_nruns) * size_t(ld);
+    w.sc.dt = c;
+    w.sc.lam = c + rn;
+    w.sc.br = c + 2 * rn;
+    w.sc.bl = c + 3 * rn;
+    w.bl = c + 4 * rn;
+    w.br = w.bl + size_t(nb) * size_t(ld);
+    w.V = withV ? w.br + size_t(nb) * size_t(ld) : nullptr;
+    w.ldv = ld;
+    return w;
+}
+
+template <typename T, bool LS>
+size_t tile_smem() {
+    return LS ? sizeof(T) * kRsSeg * 32 * kSPitch : 0;
+}
+
+template <typename T, bool LS>
+int launch_part(const psw_plan* pl, const T* F, int64_t ldf, int64_t N, const Work& w,
+                cudaStream_t s) {
+    const size_t dyn = tile_smem<T, LS>();
+    auto kern = rs_part_kernel<T, LS>;
+    if (dyn > 0) {
+        static std::once_flag once;
+        cudaError_t e = cudaSuccess;
+        std::call_once(once, [&] {
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
+        });
+        PSW_CUDA_TRY(e);
+    }
+    const dim3 grid(unsigned((N + 31) / 32), unsigned(pl->rs_ngroups));
+    kern<<<grid, kRsThreads, dyn, s>>>(F, ldf, N, int32_t(pl->row0), pl->d_rs_group, pl->d_rs_run,
+                                      pl->d_segdesc, pl->d_seg,
+                                      static_cast<const FusedFwd<T>*>(pl->d_ffwd), w.sc);
+    return PSW_OK;
+}
+
+template <typename T, bool LS, bool STREAM>
+int launch_solve_t(const psw_plan* pl, const T* F, int64_t ldf, T* X, int64_t ldx, int64_t N,
+                   const Work& w, const double* V, int64_t ldv, cudaStream_t s) {
+    const size_t dyn = tile_smem<T, LS>();
+    auto kern = rs_solve_kernel<T, LS, STREAM>;
+    if (dyn > 0) {
+        static std::once_flag once;
+        cudaError_t e = cudaSuccess;
+        std::call_once(once, [&] {
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
+        });
+        PSW_CUDA_TRY(e);
+    }
+    const dim3 grid(unsigned((N + 31) / 32), unsigned(pl->rs_ngroups));
+    kern<<<grid, kRsThreads, dyn, s>>>(F, ldf, X, ldx, N, int32_t(pl->row0), pl->rs_ngroups,
+                                      pl->d_rs_group, pl->d_rs_run, pl->d_segdesc, pl->d_seg,
+                                      static_cast<const SolveCoef<T>*>(pl->d_scoef), w.sc, V, ldv);
+    return PSW_OK;
+}
+
+template <typename T, bool LS>
+int launch_solve(const psw_plan* pl, const T* F, int64_t ldf, T* X, int64_t ldx, int64_t N,
+                 const Work& w, const double* V, int64_t ldv, bool stream_loads, cudaStream_t s) {
+    return stream_loads ? launch_solve_t<T, LS, true>(pl, F, ldf, X, ldx, N, w, V, ldv, s)
+                        : launch_solve_t<T, LS, false>(pl, F, ldf, X, ldx, N, w, V, ldv, s);
+}
+
+// K2 of a whole-system plan: boundary values into w.V, run carries in place
+int launch_comb(const psw_plan* pl, int64_t N, const Work& w, cudaStream_t s, int64_t& launches) {
+    const int P = int(pl->P), p = int(pl->p);
+    const unsigned gx = unsigned((N + 127) / 128);
+    if (pl->d_cmat && P <= kCombMaxP) {
+        const size_t cmb = sizeof(double) * size_t(std::max(p, 1)) * 2 * P;
+        static std::once_flag once;
+        cudaError_t e = cudaSuccess;
+        std::call_once(once, [&] {
+            e = cudaFuncSetAttribute(rs_comb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(sizeof(double) * (kCombMaxP - 1) * 2 * kCombMaxP));
+        });
+        PSW_CUDA_TRY(e);
+        rs_comb_kernel<<<unsigned((N + 31) / 32), kCombWarps * 32, cmb, s>>>(
+            N, P, p, pl->d_rs_runoff, pl->d_rs_runcoef, pl->d_cmat, w.sc, w.V, w.ldv);
+        ++launches;
+        return PSW_OK;
+    }
+    rs_fold_kernel<<<dim3(gx, unsigned(P)), 128, 0, s>>>(N, pl->d_rs_runoff, pl->d_rs_runcoef,
+                                                         w.sc, w.bl, w.br);
+    ++launches;
+    if (p > 0) {
+        // the combination runs over the padded pitch (columns >= N unused)
+        if (int rc = launch_combine(pl, w.bl, w.br, w.sc.ld, w.V, s)) return rc;
+        ++launches;
+    }
+    rs_carry_kernel<<<dim3(gx, unsigned(P)), 128, 0, s>>>(N, p, 0, pl->d_rs_runoff,
+                                                          pl->d_rs_runcoef, w.sc, w.V, w.ldv);
+    ++launches;
+    return PSW_OK;
 }
 
 template <typename T>
-int launch_resweep(const psw_plan* pl, const void* Fv, int64_t ldf, void* Xv, int64_t ldx,
-                   int64_t N, int layout, cudaStream_t s, void** ev, int nev) {
+int solve_all(const psw_plan* pl, const void* Fv, int64_t ldf, void* Xv, int64_t ldx, int64_t N,
+              int layout, const Work& w, bool stream_loads, cudaStream_t s, void** ev, int nev,
+              int64_t& launches) {
     const T* F = static_cast<const T*>(Fv);
     T* X = static_cast<T*>(Xv);
-    const int P = int(pl->P), p = int(pl->p);
-    const int NS = pl->seg_off.back();
-    const int64_t ld = (N + 31) / 32 * 32;  // scratch row pitch
-    const size_t sn = size_t(NS) * size_t(ld);
-    const size_t need = sn * 4 * sizeof(T) +
-                        sizeof(double) * size_t(ld) * (2 * size_t(P) + size_t(std::max(p, 1))) + 256;
-    void* scratch = nullptr;
-    PSW_CUDA_TRY(cudaMallocAsync(&scratch, need, s));
-    char* c = static_cast<char*>(scratch);
-    Scratch<T> sc;
-    sc.ld = ld;
-    double* bl = reinterpret_cast<double*>(c);
-    double* br = bl + size_t(P) * ld;
-    double* V = br + size_t(P) * ld;
-    sc.pr = reinterpret_cast<T*>(V + size_t(std::max(p, 1)) * ld);
-    sc.pl = sc.pr + sn;
-    sc.pd = sc.pl + sn;
-    sc.px = sc.pd + sn;
-    const unsigned gx = unsigned((N + kThreads - 1) / kThreads);
-    const auto* desc = pl->d_segdesc;
-    const unsigned gs = unsigned((N + kSWarps * 32 - 1) / (kSWarps * 32));
     mark(ev, nev, 0, s);
-    if (layout == PSW_LAYOUT_S)
-        rs_part_s_kernel<T><<<dim3(gs, unsigned(NS)), kSWarps * 32, 0, s>>>(
-            F, ldf, N, desc, static_cast<const FusedFwd<T>*>(pl->d_ffwd), sc);
-    else
-        rs_part_kernel<T><<<dim3(gx, unsigned(NS)), kThreads, 0, s>>>(
-            F, ldf, N, desc, static_cast<const FusedFwd<T>*>(pl->d_ffwd), sc);
+    int rc = layout == PSW_LAYOUT_S ? launch_part<T, true>(pl, F, ldf, N, w, s)
+                                    : launch_part<T, false>(pl, F, ldf, N, w, s);
+    if (rc) return rc;
+    ++launches;
     mark(ev, nev, 1, s);
-    int64_t launches = 1;
-    // fused fold + combination + carries when there are enough 32-RHS CTAs
-    // to fill the GPU, otherwise one kernel per step over (rhs, block) threads
-    int nsm = 0;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, pl->device);
-    const bool cm = pl->d_cmat && P <= kCombMaxP;
-    static const int fused_comb = [] {  // PSW_RESWEEP_COMB=0: always the split kernels
-        const char* e = std::getenv("PSW_RESWEEP_COMB");
-        return e ? std::atoi(e) : 1;
-    }();
-    if (cm && fused_comb && (N + 31) / 32 >= nsm / 2 && int64_t(NS) * 4 <= 512) {
-        const size_t cmb = sizeof(double) * size_t(p) * 2 * P;
-        PSW_CUDA_TRY(cudaFuncSetAttribute(rs_comb_kernel<T>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(cmb)));
-        rs_comb_kernel<T><<<unsigned((N + 31) / 32), kCombWarps * 32, cmb, s>>>(
-            N, P, p, pl->d_segoff, pl->d_seg, pl->d_cmat, sc, V);
-        ++launches;
-    } else {
-        rs_fold_kernel<T><<<dim3(gx, unsigned(P)), kThreads, 0, s>>>(N, p, pl->d_segoff,
-                                                                     pl->d_seg, sc, bl, br);
-        ++launches;
-        if (p > 0 && cm) {
-            rs_vmat_kernel<<<dim3(gx, unsigned(p)), kThreads, 0, s>>>(N, ld, P, p, pl->d_cmat, bl,
-                                                                      br, V);
-            ++launches;
-        } else if (p > 0) {
-            // the combination runs over the padded pitch (columns >= N unused)
-            int rc = launch_combine(pl, bl, br, ld, V, s);
-            if (rc != PSW_OK) {
-                cudaFreeAsync(scratch, s);
-                return rc;
-            }
-            ++launches;
-        }
-        rs_carry_kernel<T><<<dim3(gx, unsigned(P)), kThreads, 0, s>>>(N, p, pl->d_segoff,
-                                                                      pl->d_seg, sc, V);
-        ++launches;
-    }
+    if ((rc = launch_comb(pl, N, w, s, launches))) return rc;
     mark(ev, nev, 2, s);
-    if (layout == PSW_LAYOUT_S)
-        rs_solve_s_kernel<T><<<dim3(gs, unsigned(NS)), kSWarps * 32, 0, s>>>(
-            F, ldf, X, ldx, N, desc, static_cast<const FwdCoef<T>*>(pl->d_fwd),
-            static_cast<const BwdCoef<T>*>(pl->d_bwd), sc, V, NS);
-    else
-        rs_solve_kernel<T><<<dim3(gx, unsigned(NS)), kThreads, 0, s>>>(
-            F, ldf, X, ldx, N, desc, static_cast<const FwdCoef<T>*>(pl->d_fwd),
-            static_cast<const BwdCoef<T>*>(pl->d_bwd), sc, V, NS);
+    rc = layout == PSW_LAYOUT_S
+             ? launch_solve<T, true>(pl, F, ldf, X, ldx, N, w, w.V, w.ldv, stream_loads, s)
+             : launch_solve<T, false>(pl, F, ldf, X, ldx, N, w, w.V, w.ldv, stream_loads, s);
+    if (rc) return rc;
     ++launches;
     mark(ev, nev, 3, s);
+    return PSW_OK;
+}
+
+int solve_all_dt(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_t ldx, int64_t N,
+                 int layout, const Work& w, bool stream_loads, cudaStream_t s, void** ev, int nev,
+                 int64_t& launches) {
+    return pl->dtype == PSW_F64
+               ? solve_all<double>(pl, F, ldf, X, ldx, N, layout, w, stream_loads, s, ev, nev, launches)
+               : solve_all<float>(pl, F, ldf, X, ldx, N, layout, w, stream_loads, s, ev, nev, launches);
+}
+
+// ---- chunked driver: internal streams, one set per device ----------------
+constexpr int kMaxChunkStreams = 4;
+struct ChunkStreams {
+    std::mutex mu;
+    bool ready = false;
+    cudaStream_t st[kMaxChunkStreams] = {};
+};
+ChunkStreams& chunk_streams(int dev) {
+    static std::mutex mu;
+    static std::vector<ChunkStreams*> v;
+    std::lock_guard<std::mutex> lk(mu);
+    if (size_t(dev) >= v.size()) v.resize(size_t(dev) + 1, nullptr);
+    if (!v[size_t(dev)]) v[size_t(dev)] = new ChunkStreams();  // lives for the process
+    return *v[size_t(dev)];
+}
+
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+
+// RHS per chunk: the chunk's F fits a quarter of L2 (the chunk in K1, its
+// re-read in K3 and the neighbouring streams' chunks share it)
+int64_t chunk_rhs(const psw_plan* pl, int64_t N) {
+    const int es = pl->dtype == PSW_F64 ? 8 : 4;
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, pl->device);
+    const int64_t mb = env_int("PSW_CHUNK_MB", 0);
+    const int64_t budget = mb > 0 ? mb << 20 : int64_t(l2 > 0 ? l2 : (96 << 20)) / 4;
+    int64_t c = budget / (int64_t(pl->n) * es) / 32 * 32;
+    return std::min<int64_t>(std::max<int64_t>(c, 32), N);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ tables
+int build_rs_tables(psw_plan* pl, const std::vector<SegDesc>& desc,
+                    const std::vector<SegCoef>& seg, const std::vector<FusedFwd<double>>& ff,
+                    const std::vector<FusedBwd<double>>& fb) {
+    const int s_begin = pl->seg_off[size_t(pl->blk0)], s_end = pl->seg_off[size_t(pl->blk1)];
+    std::vector<RsGroup> groups;
+    std::vector<RsRun> runs;
+    std::vector<SegCoef> rcoef;
+    std::vector<int32_t> runoff(size_t(pl->blk1 - pl->blk0) + 1, 0);
+    for (int g0 = s_begin; g0 < s_end; g0 += kRsSeg) {
+        const int g1 = std::min(g0 + kRsSeg, s_end);
+        RsGroup g{g0, g1, int32_t(runs.size()), 0, desc[size_t(g0)].a, desc[size_t(g1 - 1)].b, 0, 0};
+        for (int s = g0; s < g1;) {
+            const int t = desc[size_t(s)].t;
+            int e = s;
+            while (e < g1 && desc[size_t(e)].t == t) ++e;
+            // compose the segments' affine maps (psw_internal.h): with
+            // D_{a-1} = Drel + MUpre D_in along the run and x_a(s) = Lam~_s +
+            // D_{a-1} K1_s + x_l K2_s + nu_s x_b(s)
+            double mu = 1.0, k1 = 0.0, k2 = 0.0, nu = 1.0;
+            for (int q = s; q < e; ++q) {
+                const SegCoef& c = seg[size_t(q)];
+                k1 += nu * mu * c.k1;
+                k2 += nu * c.k2;
+                mu *= c.mu_end;
+                nu *= c.nu;
+            }
+            runs.push_back({s, e, t, int32_t(t - pl->blk0)});
+            rcoef.push_back({mu, k1, k2, nu});
+            s = e;
+        }
+        g.r1 = int32_t(runs.size());
+        groups.push_back(g);
+    }
+    for (size_t r = 0; r < runs.size(); ++r) runoff[size_t(runs[r].tl) + 1] = int32_t(r + 1);
+    for (size_t i = 1; i < runoff.size(); ++i) runoff[i] = std::max(runoff[i], runoff[i - 1]);
+    pl->rs_ngroups = int(groups.size());
+    pl->rs_nruns = int(runs.size());
+    // per-row solve coefficients (rp, ma, lam from the forward table, mu, w,
+    // al from the backward one)
+    const int64_t n = pl->n;
+    const size_t es = pl->dtype == PSW_F64 ? sizeof(SolveCoef<double>) : sizeof(SolveCoef<float>);
+    std::vector<unsigned char> sco(size_t(n) * es);
+    for (int64_t q = 0; q < n; ++q) {
+        const FusedFwd<double>& a = ff[size_t(q)];
+        const FusedBwd<double>& b = fb[size_t(q)];
+        if (pl->dtype == PSW_F64)
+            reinterpret_cast<SolveCoef<double>*>(sco.data())[q] = {a.rp, a.ma, a.lam, b.mu, b.w, b.al};
+        else
+            reinterpret_cast<SolveCoef<float>*>(sco.data())[q] = {
+                float(a.rp), float(a.ma), float(a.lam), float(b.mu), float(b.w), float(b.al)};
+    }
+    auto up = [&](void** dst, const void* src, size_t bytes) -> int {
+        PSW_CUDA_TRY(cudaMalloc(dst, std::max<size_t>(bytes, 16)));
+        if (bytes) PSW_CUDA_TRY(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
+        pl->info.device_bytes += int64_t(bytes);
+        return PSW_OK;
+    };
+    if (int rc = up(reinterpret_cast<void**>(&pl->d_rs_group), groups.data(), sizeof(RsGroup) * groups.size())) return rc;
+    if (int rc = up(reinterpret_cast<void**>(&pl->d_rs_run), runs.data(), sizeof(RsRun) * runs.size())) return rc;
+    if (int rc = up(reinterpret_cast<void**>(&pl->d_rs_runcoef), rcoef.data(), sizeof(SegCoef) * rcoef.size())) return rc;
+    if (int rc = up(reinterpret_cast<void**>(&pl->d_rs_runoff), runoff.data(), sizeof(int32_t) * runoff.size())) return rc;
+    return up(&pl->d_scoef, sco.data(), sco.size());
+}
+
+// ------------------------------------------------------------------ drivers
+bool resweep_supported(const psw_plan* pl, int layout, int64_t N) {
+    if (pl->world != 1 || (layout != PSW_LAYOUT_R && layout != PSW_LAYOUT_S) || N < 1) return false;
+    return pl->d_rs_group && pl->rs_ngroups > 0 && pl->rs_ngroups < 65536 && pl->P < 65536 &&
+           (N + 31) / 32 < (int64_t{1} << 31);
+}
+
+int solve_resweep(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_t ldx, int64_t N,
+                  int layout, cudaStream_t s, void** ev, int nev) {
+    void* mem = nullptr;
+    PSW_CUDA_TRY(cudaMallocAsync(&mem, work_bytes(pl, N, true), s));
+    const Work w = carve(pl, N, mem, true);
+    int64_t launches = 0;
+    int rc = solve_all_dt(pl, F, ldf, X, ldx, N, layout, w, true, s, ev, nev, launches);
     cudaError_t e = cudaGetLastError();
-    cudaFreeAsync(scratch, s);
+    cudaFreeAsync(mem, s);
+    if (rc != PSW_OK) return rc;
     if (e != cudaSuccess) return cuda_fail(e, "resweep kernels");
     note_launches(launches);
     return PSW_OK;
 }
 
-}  // namespace
-
-bool resweep_supported(const psw_plan* pl, int layout, int64_t N) {
-    if (pl->world != 1 || (layout != PSW_LAYOUT_R && layout != PSW_LAYOUT_S) || N < 1) return false;
-    if (!pl->d_segdesc || !pl->d_ffwd || pl->seg_off.empty()) return false;
-    return pl->seg_off.back() < 65536 && pl->P < 65536;  // grid.y
+bool chunked_supported(const psw_plan* pl, int layout, int64_t N) {
+    return layout == PSW_LAYOUT_R && resweep_supported(pl, layout, N);
 }
 
-int solve_resweep(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_t ldx, int64_t N,
+int solve_chunked(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_t ldx, int64_t N,
                   int layout, cudaStream_t s, void** ev, int nev) {
-    return pl->dtype == PSW_F64 ? launch_resweep<double>(pl, F, ldf, X, ldx, N, layout, s, ev, nev)
-                                : launch_resweep<float>(pl, F, ldf, X, ldx, N, layout, s, ev, nev);
+    const int es = pl->dtype == PSW_F64 ? 8 : 4;
+    const int64_t c = chunk_rhs(pl, N);
+    const int64_t nchunks = (N + c - 1) / c;
+    const int nst = int(std::min<int64_t>(std::max(1, std::min(env_int("PSW_CHUNK_STREAMS", 3),
+                                                               kMaxChunkStreams)),
+                                          nchunks));
+    const size_t wb = (work_bytes(pl, c, true) + 255) & ~size_t(255);
+    void* mem = nullptr;
+    PSW_CUDA_TRY(cudaMallocAsync(&mem, wb * size_t(nst), s));
+    ChunkStreams& cs = chunk_streams(pl->device);
+    std::lock_guard<std::mutex> lk(cs.mu);
+    if (!cs.ready) {
+        for (int i = 0; i < kMaxChunkStreams; ++i)
+            PSW_CUDA_TRY(cudaStreamCreateWithFlags(&cs.st[i], cudaStreamNonBlocking));
+        cs.ready = true;
+    }
+    cudaEvent_t fork = nullptr, join[kMaxChunkStreams] = {};
+    PSW_CUDA_TRY(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    for (int i = 0; i < nst; ++i) PSW_CUDA_TRY(cudaEventCreateWithFlags(&join[i], cudaEventDisableTiming));
+    mark(ev, nev, 0, s);
+    PSW_CUDA_TRY(cudaEventRecord(fork, s));
+    for (int i = 0; i < nst; ++i) PSW_CUDA_TRY(cudaStreamWaitEvent(cs.st[i], fork, 0));
+    int64_t launches = 0;
+    int rc = PSW_OK;
+    for (int64_t ci = 0; ci < nchunks && rc == PSW_OK; ++ci) {
+        const int si = int(ci % nst);
+        const int64_t k0 = ci * c, kc = std::min(c, N - k0);
+        const Work w = carve(pl, kc, static_cast<char*>(mem) + wb * size_t(si), true);
+        rc = solve_all_dt(pl, static_cast<const char*>(F) + k0 * es, ldf,
+                          static_cast<char*>(X) + k0 * es, ldx, kc, layout, w, false, cs.st[si],
+                          nullptr, 0, launches);
+    }
+    for (int i = 0; i < nst; ++i) {
+        cudaEventRecord(join[i], cs.st[i]);
+        cudaStreamWaitEvent(s, join[i], 0);
+    }
+    mark(ev, nev, 1, s);
+    cudaError_t e = cudaGetLastError();
+    cudaFreeAsync(mem, s);
+    cudaEventDestroy(fork);
+    for (int i = 0; i < nst; ++i) cudaEventDestroy(join[i]);
+    if (rc != PSW_OK) return rc;
+    if (e != cudaSuccess) return cuda_fail(e, "chunked kernels");
+    note_launches(launches);
+    return PSW_OK;
+}
+
+// ------------------------------------------------------------------ shards
+int64_t shard_workspace_bytes(const psw_plan* pl, int64_t N) {
+    return int64_t(work_bytes(pl, N, false));
+}
+
+int shard_forward(const psw_plan* pl, const void* Fv, int64_t ldf, int64_t N, void* ws,
+                  double* partials, cudaStream_t s) {
+    const Work w = carve(pl, N, ws, false);
+    const int nb = int(pl->blk1 - pl->blk0), p = int(pl->p);
+    int rc = pl->dtype == PSW_F64
+                 ? launch_part<double, false>(pl, static_cast<const double*>(Fv), ldf, N, w, s)
+                 : launch_part<float, false>(pl, static_cast<const float*>(Fv), ldf, N, w, s);
+    if (rc) return rc;
+    const unsigned gx = unsigned((N + 127) / 128);
+    rs_fold_kernel<<<dim3(gx, unsigned(nb)), 128, 0, s>>>(N, pl->d_rs_runoff, pl->d_rs_runcoef,
+                                                          w.sc, w.bl, w.br);
+    int64_t launches = 2;
+    if (p > 0) {
+        rs_vpart_kernel<<<dim3(gx, unsigned(p)), 128, 0, s>>>(N, w.sc.ld, int(pl->P), p,
+                                                              int(pl->blk0), nb, pl->d_cmat, w.bl,
+                                                              w.br, partials);
+        ++launches;
+    }
+    PSW_CUDA_TRY(cudaGetLastError());
+    note_launches(launches);
+    return PSW_OK;
+}
+
+int shard_backward(const psw_plan* pl, const void* Fv, int64_t ldf, void* Xv, int64_t ldx,
+                   int64_t N, void* ws, const double* V, cudaStream_t s) {
+    const Work w = carve(pl, N, ws, false);
+    const int nb = int(pl->blk1 - pl->blk0), p = int(pl->p);
+    const unsigned gx = unsigned((N + 127) / 128);
+    rs_carry_kernel<<<dim3(gx, unsigned(nb)), 128, 0, s>>>(N, p, int(pl->blk0), pl->d_rs_runoff,
+                                                           pl->d_rs_runcoef, w.sc, V, N);
+    int rc = pl->dtype == PSW_F64
+                 ? launch_solve<double, false>(pl, static_cast<const double*>(Fv), ldf,
+                                               static_cast<double*>(Xv), ldx, N, w, V, N, true, s)
+                 : launch_solve<float, false>(pl, static_cast<const float*>(Fv), ldf,
+                                              static_cast<float*>(Xv), ldx, N, w, V, N, true, s);
+    if (rc) return rc;
+    PSW_CUDA_TRY(cudaGetLastError());
+    note_launches(2);
+    return PSW_OK;
 }
 
 }  // namespace psw

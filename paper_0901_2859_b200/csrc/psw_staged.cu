@@ -513,73 +513,6 @@ int solve_staged(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_
     return rc;
 }
 
-// ------------------------------------------------------------ row shards
-namespace {
-// partials[j * N + k] = sum over the rank's blocks t of
-//   MR[j][t] right_t[k] + ML[j][t] left_t[k]        (combination matrix rows)
-__global__ void __launch_bounds__(kThreads) shard_partials_kernel(
-    const double* __restrict__ bl, const double* __restrict__ br, int64_t N, int p, int P,
-    int t0, int t1, const double* __restrict__ cmat, double* __restrict__ out) {
-    const int j = blockIdx.y;
-    const int64_t k = int64_t(blockIdx.x) * kThreads + threadIdx.x;
-    if (k >= N) return;
-    const double* Mr = cmat + int64_t(j) * 2 * P;
-    double s = 0.0;
-    for (int t = t0; t < t1; ++t) {
-        const int64_t i = int64_t(t - t0) * N + k;
-        if (t < p) s = fma(Mr[t], br[i], s);
-        if (t > 0) s = fma(Mr[P + t], bl[i], s);
-    }
-    out[int64_t(j) * N + k] = s;
-}
-}  // namespace
-
-int shard_forward(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_t ldx,
-                  int64_t N, double* partials, cudaStream_t s) {
-    const int t0 = int(pl->blk0), nb = int(pl->blk1 - pl->blk0), p = int(pl->p);
-    double* scratch = nullptr;
-    PSW_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&scratch), sizeof(double) * 2 * nb * N, s));
-    double* bl = scratch;
-    double* br = scratch + int64_t(nb) * N;
-    const dim3 grid(unsigned((N + kThreads - 1) / kThreads), unsigned(nb));
-    const int row_off = int(pl->row0);
-    if (pl->dtype == PSW_F64)
-        fwd_r_kernel<double><<<grid, kThreads, 0, s>>>(
-            static_cast<const double*>(F), ldf, static_cast<double*>(X), ldx, N, pl->d_blk,
-            static_cast<const FwdCoef<double>*>(pl->d_fwd), bl, br, p, t0, row_off);
-    else
-        fwd_r_kernel<float><<<grid, kThreads, 0, s>>>(
-            static_cast<const float*>(F), ldf, static_cast<float*>(X), ldx, N, pl->d_blk,
-            static_cast<const FwdCoef<float>*>(pl->d_fwd), bl, br, p, t0, row_off);
-    int64_t launches = 1;
-    if (p > 0) {
-        shard_partials_kernel<<<dim3(grid.x, unsigned(p)), kThreads, 0, s>>>(
-            bl, br, N, p, int(pl->P), t0, t0 + nb, pl->d_cmat, partials);
-        ++launches;
-    }
-    cudaFreeAsync(scratch, s);
-    PSW_CUDA_TRY(cudaGetLastError());
-    note_launches(launches);
-    return PSW_OK;
-}
-
-int shard_backward(const psw_plan* pl, void* X, int64_t ldx, int64_t N, const double* V,
-                   cudaStream_t s) {
-    const int t0 = int(pl->blk0), nb = int(pl->blk1 - pl->blk0), p = int(pl->p);
-    const dim3 grid(unsigned((N + kThreads - 1) / kThreads), unsigned(nb));
-    if (pl->dtype == PSW_F64)
-        bwd_r_kernel<double><<<grid, kThreads, 0, s>>>(
-            static_cast<double*>(X), ldx, N, pl->d_blk,
-            static_cast<const BwdCoef<double>*>(pl->d_bwd), V, p, t0, int(pl->row0));
-    else
-        bwd_r_kernel<float><<<grid, kThreads, 0, s>>>(
-            static_cast<float*>(X), ldx, N, pl->d_blk,
-            static_cast<const BwdCoef<float>*>(pl->d_bwd), V, p, t0, int(pl->row0));
-    PSW_CUDA_TRY(cudaGetLastError());
-    note_launches(1);
-    return PSW_OK;
-}
-
 // ------------------------------------------------------------ data fill
 namespace {
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {

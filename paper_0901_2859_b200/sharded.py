@@ -76,37 +76,81 @@ def rhs_slice(nrhs: int, world: int, rank: int) -> tuple[int, int]:
 class ShardedSolver:
     """Row-sharded solve of A X = F over a torch.distributed process group.
 
-    `plan` defaults to the rank's CUDA shard plan (psw_shard_plan_create);
-    anything with the same four methods (shard_forward, shard_backward,
-    partials_count, row_offset/rows) can stand in, which is how the CPU
-    (gloo) tests drive this orchestration without a GPU."""
+    On GPUs the exchange is inside the C ABI: psw_shard_solve runs the
+    forward sweep, an ncclAllReduce over the solver's own NCCL communicator
+    (created from a unique id that rank 0 broadcasts over `group`) and the
+    backward sweep on one stream. With `use_nccl=False`, or a `plan` stand-in
+    (the CPU gloo tests), the two halves run around
+    torch.distributed.all_reduce of the p x N partial boundary values.
+    A stand-in needs workspace_bytes / shard_forward / shard_backward /
+    row_offset / rows with the Plan signatures."""
 
     def __init__(self, A: TridiagMatrix, part: Partition, dtype: int = F64, device: int = 0,
-                 group=None, plan=None):
+                 group=None, plan=None, use_nccl: bool | None = None):
         import torch.distributed as dist
         self.dist = dist
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.shard = shard_layout(A.n(), part, self.world)[self.rank]
+        own_plan = plan is None
         self.plan = plan if plan is not None else Plan(A, part, dtype=dtype, device=device,
                                                        rank=self.rank, world=self.world)
         self.p = part.p()
         self.comm_bytes_per_rhs = 8 * self.p
+        self.device = device
+        self.comm = None
+        if use_nccl is None:
+            use_nccl = own_plan
+        if use_nccl:
+            from . import Comm
+            box = [Comm.unique_id() if self.rank == 0 else None]
+            dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group else 0,
+                                       group=group)
+            self.comm = Comm(self.world, self.rank, box[0], device)
+
+    def close(self):
+        if self.comm is not None:
+            self.comm.close()
+            self.comm = None
 
     def solve(self, F_local, X_local=None, nrhs: int | None = None, stream=None):
         """F_local: (rows, N) owned rows of the series (layout R); X_local
         defaults to F_local (in place). Returns X_local."""
-        import torch
         if X_local is None:
             X_local = F_local
         N = F_local.shape[1] if nrhs is None else nrhs
-        partials = torch.zeros((max(self.p, 1), N), dtype=torch.float64, device=F_local.device)
-        self.plan.shard_forward(F_local, X_local, partials, N, stream=stream)
-        if self.p > 0 and self.world > 1:
-            self.dist.all_reduce(partials, op=self.dist.ReduceOp.SUM, group=self.group)
-        self.plan.shard_backward(X_local, partials, N, stream=stream)
+        if self.comm is not None:
+            return self.plan.shard_solve(F_local, X_local, self.comm, N, stream=stream)
+        import contextlib
+
+        import torch
+        on_gpu = getattr(F_local, "is_cuda", False)
+        # the zero fill, the all-reduce and both halves are ordered on one stream
+        ctx = torch.cuda.stream(stream) if on_gpu and stream is not None else contextlib.nullcontext()
+        with ctx:
+            ws = torch.empty(max(self.plan.workspace_bytes(N), 1), dtype=torch.uint8,
+                             device=F_local.device)
+            partials = torch.zeros((max(self.p, 1), N), dtype=torch.float64, device=F_local.device)
+            cur = torch.cuda.current_stream() if on_gpu else None
+            self.plan.shard_forward(F_local, N, ws, partials, stream=cur)
+            if self.p > 0 and self.world > 1:
+                self.dist.all_reduce(partials, op=self.dist.ReduceOp.SUM, group=self.group)
+            self.plan.shard_backward(F_local, X_local, N, ws, partials, stream=cur)
         return X_local
+
+    def solve_host(self, F_host, X_host=None, stream=None):
+        """End to end from pinned host rows: H2D of this rank's F rows, the
+        sharded solve, D2H of its X rows (the bench's e2e leg)."""
+        import torch
+        if X_host is None:
+            X_host = torch.empty_like(F_host)
+        dev = torch.device("cuda", self.device)
+        Fd = F_host.to(dev, non_blocking=True)
+        self.solve(Fd, Fd, stream=stream)
+        X_host.copy_(Fd, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        return X_host
 
 
 __all__ = ["Shard", "shard_layout", "combine_matrix", "rhs_slice", "ShardedSolver", "LAYOUT_R"]

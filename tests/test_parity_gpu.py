@@ -291,7 +291,7 @@ def test_nonsymmetric_strategies(psw, cuda, kind, strategy):
         return
     plan = psw.Plan(A, part, strategy=strategy)
     assert plan.info["strategy_used"] == pre["strategy_used"]
-    for path in (psw.PATH_STAGED, psw.PATH_AUTO, psw.PATH_TILE):
+    for path in (psw.PATH_STAGED, psw.PATH_AUTO, psw.PATH_RESWEEP):
         for layout in (0, 1):
             X = gpu_solve(psw, cuda, plan, g["F"], layout, path=path)
             assert rel_l2(X, want) <= FP64_TOL, (path, layout, rel_l2(X, want))

@@ -62,3 +62,69 @@ def test_resweep_config_C1(psw, cuda):
     Xs = X[:, cuda.from_numpy(ks).cuda()].T.cpu().numpy()
     want = Oracle().solve_batch_threads(a, b, a, np.array(part.boundaries), Fs, 8)[0]
     assert rel_l2(Xs, want) <= FP64_TOL
+
+
+@pytest.mark.parametrize("chunk_mb", ["1", "3"])
+@pytest.mark.parametrize("name", ["c1_n4096_P16", "c4_n4096_P16", "c0_n1024_P4", "decomp_n333_P9",
+                                  "rand_n200_p7"])
+def test_chunked_golden(psw, cuda, name, chunk_mb, monkeypatch):
+    """CHUNKED: the RESWEEP kernels over RHS chunks on forked streams (small
+    chunks forced through PSW_CHUNK_MB so every case has several)."""
+    monkeypatch.setenv("PSW_CHUNK_MB", chunk_mb)
+    g = load_golden(name)
+    plan = plan_for(psw, g)
+    F = np.concatenate([g["F"]] * 8, axis=0)  # >= 8 chunks' worth of RHS
+    want = np.concatenate([g["X"]] * 8, axis=0)
+    X = gpu_solve(psw, cuda, plan, F, 0, path=psw.PATH_CHUNKED)
+    X2 = gpu_solve(psw, cuda, plan, F, 0, path=psw.PATH_CHUNKED, inplace=False, pad=5)
+    assert rel_l2(X, want) <= FP64_TOL
+    assert np.array_equal(X, X2)
+
+
+@pytest.mark.parametrize("name", ["c2_n8192_P8", "c2_n8192_P64", "c2_n8192_P512"])
+def test_chunked_fp32(psw, cuda, name, monkeypatch):
+    monkeypatch.setenv("PSW_CHUNK_MB", "1")
+    g = load_golden(name)
+    plan = plan_for(psw, g, dtype=psw.F32)
+    F = np.concatenate([g["F"]] * 4, axis=0)
+    X = gpu_solve(psw, cuda, plan, F, 0, path=psw.PATH_CHUNKED)
+    assert rel_l2(X, np.concatenate([g["X"]] * 4, axis=0)) <= FP32_TOL
+
+
+def test_chunked_rejects_layout_s(psw, cuda):
+    g = load_golden("c1_n4096_P16")
+    plan = plan_for(psw, g)
+    with pytest.raises(psw.NotSupported):
+        gpu_solve(psw, cuda, plan, g["F"], 1, path=psw.PATH_CHUNKED)
+
+
+def test_resweep_c3_full(psw, cuda):
+    """The headline config C3 at full size (n = 2^20, N = 1024) on the
+    default path: a seeded RHS subset against the oracle, the rest through
+    the size-independent backward error ||A x - f|| / ||f||."""
+    from oracle.pyoracle import Oracle
+    from paper_0901_2859_b200.configs import CONFIGS
+    cfg = CONFIGS["C3"]
+    a, b = cfg.matrix_ab(0)
+    A = psw.TridiagMatrix.symmetric(a, b)
+    part = psw.decompose(cfg.n, cfg.P).induced_partition()
+    plan = psw.Plan(A, part)
+    F = cuda.empty((cfg.n, cfg.nrhs), dtype=cuda.float64, device="cuda")
+    psw.fill_uniform(F, 3, -1.0, 1.0)
+    X = cuda.empty_like(F)
+    plan.solve(F, X)
+    assert psw.last_path() == "resweep"
+    ks = np.arange(0, cfg.nrhs, 97)
+    idx = cuda.from_numpy(ks).cuda()
+    Fs = F[:, idx].T.cpu().numpy()
+    Xs = X[:, idx].T.cpu().numpy()
+    want = Oracle().solve_batch_threads(a, b, a, np.array(part.boundaries), Fs, 8)[0]
+    assert rel_l2(Xs, want) <= FP64_TOL
+    # every RHS: residual of the tridiagonal product on the device
+    ad = cuda.from_numpy(a).cuda()
+    bd = cuda.from_numpy(b).cuda()
+    R = bd[:, None] * X
+    R[1:] += ad[:, None] * X[:-1]
+    R[:-1] += ad[:, None] * X[1:]
+    res = ((R - F).norm(dim=0) / F.norm(dim=0)).max()
+    assert float(res) <= 1e-13

@@ -66,7 +66,10 @@ class CpuShardPlan:
         f[self.shard.row0:self.shard.row1] = F_local[:, k].numpy()
         return f
 
-    def shard_forward(self, F, X, partials, N, stream=None):
+    def workspace_bytes(self, N):
+        return 1
+
+    def shard_forward(self, F, N, ws, partials, stream=None):
         import torch
         for k in range(N):
             f = self._full(F, k)
@@ -77,7 +80,7 @@ class CpuShardPlan:
             partials[:, k] = torch.from_numpy(v)
         self._F = F.clone()
 
-    def shard_backward(self, X, partials, N, stream=None):
+    def shard_backward(self, F, X, N, ws, partials, stream=None):
         import torch
         V = partials.numpy()
         g = self.g
@@ -109,6 +112,7 @@ def _worker(rank, world, port, name, q):
         plan = CpuShardPlan(Oracle(), g, shard, combine_matrix(A, part))
         solver = ShardedSolver(A, part, plan=plan)
         assert solver.shard == shard and solver.comm_bytes_per_rhs == 8 * part.p()
+        assert solver.comm is None  # a stand-in plan: the exchange is torch.distributed (gloo)
         F_local = torch.from_numpy(np.ascontiguousarray(g["F"].T[shard.row0:shard.row1]))
         X_local = torch.zeros_like(F_local)
         solver.solve(F_local, X_local)
