@@ -38,6 +38,8 @@ __all__ = [
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libparsweep_b200.so")
+if os.environ.get("PSW_LIB_VARIANT"):  # experiments: _lib/<variant>/ built with other constants
+    LIB_PATH = os.path.join(HERE, "_lib", os.environ["PSW_LIB_VARIANT"], "libparsweep_b200.so")
 
 F64, F32 = 0, 1
 LAYOUT_R, LAYOUT_S = 0, 1

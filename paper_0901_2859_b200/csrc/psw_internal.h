@@ -87,16 +87,30 @@ struct SegDesc {  // rows [a, b) of block t
 // one block. Per run the K1 kernel leaves four aggregates per RHS, folded over
 // the run's segments; the matrix-only aggregate of a run is a SegCoef
 // (mu_end = prod mu_end, k1, k2, nu of the composed affine map).
-constexpr int kRsSeg = 8;    // segments per group (one warp each)
+#ifndef PSW_RSSEG
+#define PSW_RSSEG 8
+#endif
+constexpr int kRsSeg = PSW_RSSEG;  // segments per group (one warp each)
 struct RsGroup {
     int32_t s0, s1;  // segments [s0, s1)
     int32_t r0, r1;  // runs [r0, r1)
     int32_t ra, rb;  // rows [ra, rb) (global, 0-based)
-    int32_t pad0, pad1;
+    int32_t t0;      // global block of the first run (run j is block t0 + j)
+    int32_t pad1;
 };
 struct RsRun {
     int32_t s0, s1;  // segments [s0, s1) of block t
     int32_t t, tl;   // global block, block index local to the plan's range
+};
+// RESWEEP K3 (TMA): the exact carries of segment slot w of a group in closed
+// form over its run (the serial run fold unrolled): with dd_i / lam_i the
+// zero-carry segment end values and Lam~ of the run's slots,
+//   D_w = P D_in + sum_i A[i] dd_i
+//   x_w = Q x_B + K2 x_l + K1 D_in + sum_j B[j] lam_j + sum_i C[i] dd_i
+// (weights are zero outside w's run; psw_resweep.cu build_rs_tables)
+struct CarryW {
+    double P, Q, K1, K2;
+    double A[8], B[8], C[8];
 };
 // per-row coefficients of the RESWEEP solve kernel (K3)
 template <typename T>
@@ -143,12 +157,13 @@ struct psw_plan {
     std::vector<int32_t> seg_off;      // host copy
 
     // RESWEEP tables over the plan's own segments (psw_resweep.cu)
-    int rs_ngroups = 0, rs_nruns = 0;
+    int rs_ngroups = 0, rs_nruns = 0, rs_maxruns = 0;  // maxruns: most runs in one group
     psw::RsGroup* d_rs_group = nullptr;
     psw::RsRun* d_rs_run = nullptr;
     psw::SegCoef* d_rs_runcoef = nullptr;  // composed affine map of every run
     int32_t* d_rs_runoff = nullptr;        // [Ploc + 1] first run of every own block
     void* d_scoef = nullptr;               // SolveCoef<T>[n]
+    psw::CarryW* d_rs_cw = nullptr;        // [group][kRsSeg] closed-form carry weights
 
     // multi-GPU row shard (psw_shard_*); world == 1 for a full plan
     int rank = 0, world = 1;

@@ -325,7 +325,7 @@ void free_plan(psw_plan* pl) {
                     pl->d_lvl_off, pl->d_ffwd, pl->d_fbwd, pl->d_seg, pl->d_cmat,
                     pl->d_segdesc, pl->d_segoff, pl->d_ctab[0], pl->d_ctab[1],
                     pl->d_rs_group, pl->d_rs_run, pl->d_rs_runcoef, pl->d_rs_runoff,
-                    pl->d_scoef};
+                    pl->d_scoef, pl->d_rs_cw};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     cudaSetDevice(prev);

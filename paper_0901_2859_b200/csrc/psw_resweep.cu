@@ -42,14 +42,17 @@
 
 #include "psw_device.cuh"
 #include "psw_internal.h"
+#include "psw_tma.cuh"
 
 namespace psw {
 namespace {
 
 constexpr int kRsThreads = kRsSeg * 32;
+constexpr int kRsMinBlocks = 512 / kRsThreads;  // 16 warps per SM
 constexpr int kSegMax = kSegLen + 1;
 constexpr int kRsRows = kRsSeg * kSegMax;  // coefficient rows staged per group (bound)
 constexpr int kSPitch = kSegMax;           // layout S tile pitch (odd: conflict-free columns)
+constexpr int kTmaRows = 256;              // rows per group at most (one TMA stage)
 
 // Per (run r, rhs k), [r * ld + k], all fp64:
 //   dt   K1: run d~ end (zero carry)  -> K2: D_in (exact carry into the run)
@@ -101,12 +104,13 @@ __device__ __forceinline__ bool row_on(int r, int len) {
 
 // ------------------------------------------------------------------ K1
 template <typename T, bool LS>
-__global__ void __launch_bounds__(kRsThreads) rs_part_kernel(
+__global__ void __launch_bounds__(kRsThreads, kRsMinBlocks) rs_part_kernel(
     const T* __restrict__ F, int64_t ldf, int64_t N, int32_t row0,
     const RsGroup* __restrict__ groups, const RsRun* __restrict__ runs,
     const SegDesc* __restrict__ desc, const SegCoef* __restrict__ segc,
     const FusedFwd<T>* __restrict__ ff, RsScratch sc) {
     __shared__ FusedFwd<T> cs[kRsRows];
+    __shared__ SegCoef s_sc[kRsSeg];
     __shared__ double s_d[kRsSeg][32], s_l[kRsSeg][32], s_r[kRsSeg][32], s_b[kRsSeg][32];
     extern __shared__ __align__(16) unsigned char dyn[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -140,6 +144,7 @@ __global__ void __launch_bounds__(kRsThreads) rs_part_kernel(
         }
     }
     for (int i = threadIdx.x; i < g.rb - g.ra; i += kRsThreads) cs[i] = ff[g.ra + i];
+    if (threadIdx.x < g.s1 - g.s0) s_sc[threadIdx.x] = segc[g.s0 + threadIdx.x];
     if constexpr (LS) asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     T d = T(0), lx = T(0);
@@ -176,7 +181,7 @@ __global__ void __launch_bounds__(kRsThreads) rs_part_kernel(
         double D = 0.0, lam = 0.0, nupre = 1.0, R = 0.0, L = 0.0;
         for (int s = rr.s0; s < rr.s1; ++s) {
             const int j = s - g.s0;
-            const SegCoef q = segc[s];
+            const SegCoef q = s_sc[j];
             lam = fma(nupre, fma(D, q.k1, s_l[j][lane]), lam);
             D = fma(q.mu_end, D, s_d[j][lane]);
             nupre *= q.nu;
@@ -343,17 +348,19 @@ __global__ void __launch_bounds__(128) rs_vpart_kernel(int64_t N, int64_t ld, in
 
 // ------------------------------------------------------------------ K3
 template <typename T, bool LS, bool STREAM>
-__global__ void __launch_bounds__(kRsThreads, 2) rs_solve_kernel(
+__global__ void __launch_bounds__(kRsThreads, kRsMinBlocks) rs_solve_kernel(
     const T* F, int64_t ldf, T* X, int64_t ldx, int64_t N, int32_t row0, int ngroups,
     const RsGroup* __restrict__ groups, const RsRun* __restrict__ runs,
     const SegDesc* __restrict__ desc, const SegCoef* __restrict__ segc,
-    const SolveCoef<T>* __restrict__ sco, RsScratch sc, const double* __restrict__ V,
-    int64_t ldv) {
+    const SolveCoef<T>* __restrict__ sco, const CarryW* __restrict__ cw, RsScratch sc,
+    const double* __restrict__ V, int64_t ldv) {
     __shared__ SolveCoef<T> cs[kRsRows];
+    __shared__ CarryW s_cw[kRsSeg];
     __shared__ double s_d[kRsSeg][32], s_l[kRsSeg][32];
     extern __shared__ __align__(16) unsigned char dyn[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const RsGroup g = groups[ngroups - 1 - int(blockIdx.y)];  // reverse of K1's order
+    const int gi = ngroups - 1 - int(blockIdx.y);  // reverse of K1's order
+    const RsGroup g = groups[gi];
     const int64_t k0 = int64_t(blockIdx.x) * 32;
     const int64_t k = k0 + lane;
     const int nk = int(N - k0 < 32 ? N - k0 : 32);
@@ -367,6 +374,16 @@ __global__ void __launch_bounds__(kRsThreads, 2) rs_solve_kernel(
         len = d.b - d.a;
         t = d.t;
     }
+    // everything the carry phase needs is requested before F: the run's
+    // (D_in, x_B) and left boundary value (= this segment's x_l)
+    double rD = 0.0, rx = 0.0, rxl = 0.0;
+    if (sv && kv) {
+        const int64_t o = int64_t(g.r0 + (t - g.t0)) * sc.ld + k;
+        rD = sc.dt[o];
+        rx = sc.br[o];
+        rxl = t > 0 ? V[int64_t(t - 1) * ldv + k] : 0.0;
+    }
+    const T xl = T(rxl);
     T v[kSegMax];
     T(*tile)[kSPitch] = reinterpret_cast<T(*)[kSPitch]>(dyn) + warp * 32;
     if constexpr (LS) {
@@ -384,6 +401,8 @@ __global__ void __launch_bounds__(kRsThreads, 2) rs_solve_kernel(
         }
     }
     for (int i = threadIdx.x; i < g.rb - g.ra; i += kRsThreads) cs[i] = sco[g.ra + i];
+    for (int i = threadIdx.x; i < (g.s1 - g.s0) * int(sizeof(CarryW) / 8); i += kRsThreads)
+        reinterpret_cast<double*>(s_cw)[i] = reinterpret_cast<const double*>(cw + int64_t(gi) * kRsSeg)[i];
     if constexpr (LS) asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     const SolveCoef<T>* c = cs + (a - g.ra);
@@ -415,32 +434,25 @@ __global__ void __launch_bounds__(kRsThreads, 2) rs_solve_kernel(
     s_d[warp][lane] = double(d);
     s_l[warp][lane] = double(lx);
     __syncthreads();
-    // exact segment carries of run g.r0 + warp from its (D_in, x_B)
-    const int run = g.r0 + warp;
-    if (run < g.r1 && kv) {
-        const RsRun rr = runs[run];
-        const int64_t o = int64_t(run) * sc.ld + k;
-        double D = sc.dt[o], x = sc.br[o];
-        const double xl = rr.t > 0 ? V[int64_t(rr.t - 1) * ldv + k] : 0.0;
-        for (int s = rr.s0; s < rr.s1; ++s) {
-            const int j = s - g.s0;
-            const double dd = s_d[j][lane];
-            s_d[j][lane] = D;
-            D = fma(segc[s].mu_end, D, dd);
-        }
-        for (int s = rr.s1 - 1; s >= rr.s0; --s) {
-            const int j = s - g.s0;
-            const SegCoef q = segc[s];
-            const double lam = s_l[j][lane];
-            s_l[j][lane] = x;
-            x = fma(q.nu, x, fma(xl, q.k2, fma(s_d[j][lane], q.k1, lam)));
-        }
-    }
-    __syncthreads();
+    // the segment's exact carries in closed form over its run (CarryW, as
+    // rs_solve_tma: both kernels round alike)
+    double dc = 0.0, xc = 0.0;
     if (on) {
-        const T D = T(s_d[warp][lane]);
-        T x = T(s_l[warp][lane]);
-        const T xl = t > 0 ? T(V[int64_t(t - 1) * ldv + k]) : T(0);
+        const CarryW& q = s_cw[warp];
+        const int ns = g.s1 - g.s0;
+        dc = q.P * rD;
+        xc = fma(q.Q, rx, fma(q.K2, rxl, q.K1 * rD));
+#pragma unroll
+        for (int i = 0; i < kRsSeg; ++i)
+            if (i < ns) {
+                const double dd = s_d[i][lane];
+                dc = fma(q.A[i], dd, dc);
+                xc = fma(q.C[i], dd, fma(q.B[i], s_l[i][lane], xc));
+            }
+    }
+    if (on) {
+        const T D = T(dc);
+        T x = T(xc);
         T* xp = X + int64_t(a - row0) * ldx + k;
         auto bwd = [&](auto full) {
             constexpr bool FULL = decltype(full)::value;
@@ -483,10 +495,10 @@ struct Work {
     int64_t ldv;
 };
 
-int64_t pad32(int64_t N) { return (N + 31) / 32 * 32; }
+int64_t pad64(int64_t N) { return (N + 63) / 64 * 64; }  // a whole TMA chunk of fp32 RHS
 
 size_t work_bytes(const psw_plan* pl, int64_t N, bool withV) {
-    const int64_t ld = pad32(N);
+    const int64_t ld = pad64(N);
     const int64_t nb = pl->blk1 - pl->blk0;
     size_t b = sizeof(double) * size_t(ld) * (4 * size_t(pl->rs_nruns) + 2 * size_t(nb));
     if (withV) b += sizeof(double) * size_t(ld) * size_t(std::max<int64_t>(pl->p, 1));
@@ -494,7 +506,7 @@ size_t work_bytes(const psw_plan* pl, int64_t N, bool withV) {
 }
 
 Work carve(const psw_plan* pl, int64_t N, void* mem, bool withV) {
-    const int64_t ld = pad32(N);
+    const int64_t ld = pad64(N);
     const int64_t nb = pl->blk1 - pl->blk0;
     double* c = static_cast<double*>(mem);
     Work w;
@@ -511,6 +523,8 @@ Work carve(const psw_plan* pl, int64_t N, void* mem, bool withV) {
     return w;
 }
 
+#include "psw_rs_tma.cuh"
+
 template <typename T, bool LS>
 size_t tile_smem() {
     return LS ? sizeof(T) * kRsSeg * 32 * kSPitch : 0;
@@ -519,6 +533,10 @@ size_t tile_smem() {
 template <typename T, bool LS>
 int launch_part(const psw_plan* pl, const T* F, int64_t ldf, int64_t N, const Work& w,
                 cudaStream_t s) {
+    if constexpr (!LS) {
+        int rc = PSW_OK;
+        if (launch_part_tma<T>(pl, F, ldf, N, w.sc, s, rc)) return rc;
+    }
     const size_t dyn = tile_smem<T, LS>();
     auto kern = rs_part_kernel<T, LS>;
     if (dyn > 0) {
@@ -552,13 +570,18 @@ int launch_solve_t(const psw_plan* pl, const T* F, int64_t ldf, T* X, int64_t ld
     const dim3 grid(unsigned((N + 31) / 32), unsigned(pl->rs_ngroups));
     kern<<<grid, kRsThreads, dyn, s>>>(F, ldf, X, ldx, N, int32_t(pl->row0), pl->rs_ngroups,
                                       pl->d_rs_group, pl->d_rs_run, pl->d_segdesc, pl->d_seg,
-                                      static_cast<const SolveCoef<T>*>(pl->d_scoef), w.sc, V, ldv);
+                                      static_cast<const SolveCoef<T>*>(pl->d_scoef), pl->d_rs_cw, w.sc,
+                                      V, ldv);
     return PSW_OK;
 }
 
 template <typename T, bool LS>
 int launch_solve(const psw_plan* pl, const T* F, int64_t ldf, T* X, int64_t ldx, int64_t N,
                  const Work& w, const double* V, int64_t ldv, bool stream_loads, cudaStream_t s) {
+    if constexpr (!LS) {
+        int rc = PSW_OK;
+        if (launch_solve_tma<T>(pl, F, ldf, X, ldx, N, w.sc, V, ldv, s, rc)) return rc;
+    }
     return stream_loads ? launch_solve_t<T, LS, true>(pl, F, ldf, X, ldx, N, w, V, ldv, s)
                         : launch_solve_t<T, LS, false>(pl, F, ldf, X, ldx, N, w, V, ldv, s);
 }
@@ -670,9 +693,13 @@ int build_rs_tables(psw_plan* pl, const std::vector<SegDesc>& desc,
     std::vector<RsRun> runs;
     std::vector<SegCoef> rcoef;
     std::vector<int32_t> runoff(size_t(pl->blk1 - pl->blk0) + 1, 0);
-    for (int g0 = s_begin; g0 < s_end; g0 += kRsSeg) {
-        const int g1 = std::min(g0 + kRsSeg, s_end);
-        RsGroup g{g0, g1, int32_t(runs.size()), 0, desc[size_t(g0)].a, desc[size_t(g1 - 1)].b, 0, 0};
+    for (int g0 = s_begin, g1 = 0; g0 < s_end; g0 = g1) {
+        // kRsSeg segments, at most kTmaRows rows (one TMA stage)
+        g1 = g0 + 1;
+        while (g1 < s_end && g1 - g0 < kRsSeg && desc[size_t(g1)].b - desc[size_t(g0)].a <= kTmaRows)
+            ++g1;
+        RsGroup g{g0, g1, int32_t(runs.size()), 0, desc[size_t(g0)].a, desc[size_t(g1 - 1)].b,
+                  desc[size_t(g0)].t, 0};
         for (int s = g0; s < g1;) {
             const int t = desc[size_t(s)].t;
             int e = s;
@@ -693,7 +720,46 @@ int build_rs_tables(psw_plan* pl, const std::vector<SegDesc>& desc,
             s = e;
         }
         g.r1 = int32_t(runs.size());
+        pl->rs_maxruns = std::max(pl->rs_maxruns, int(g.r1 - g.r0));
         groups.push_back(g);
+    }
+    static_assert(kRsSeg <= 8, "CarryW holds 8 slots");
+    // closed-form carry weights per group slot (CarryW, psw_internal.h)
+    std::vector<CarryW> cw(groups.size() * kRsSeg, CarryW{});
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+        const RsGroup& g = groups[gi];
+        const int ns = g.s1 - g.s0;
+        for (int w = 0; w < ns; ++w) {
+            const int t = desc[size_t(g.s0 + w)].t;
+            int lo = w, hi = w + 1;  // the run's slots [lo, hi)
+            while (lo > 0 && desc[size_t(g.s0 + lo - 1)].t == t) --lo;
+            while (hi < ns && desc[size_t(g.s0 + hi)].t == t) ++hi;
+            auto sc = [&](int i) -> const SegCoef& { return seg[size_t(g.s0 + i)]; };
+            // Pr[j] = prod mu over [lo, j); Am[j][i] = prod mu over (i, j)
+            double Pr[8], Am[8][8] = {};
+            for (int j = lo; j < hi; ++j) {
+                Pr[j] = 1.0;
+                for (int l = lo; l < j; ++l) Pr[j] *= sc(l).mu_end;
+                for (int i = lo; i < j; ++i) {
+                    double a = 1.0;
+                    for (int l = i + 1; l < j; ++l) a *= sc(l).mu_end;
+                    Am[j][i] = a;
+                }
+            }
+            CarryW& c = cw[gi * kRsSeg + size_t(w)];
+            c.P = Pr[w];
+            for (int i = lo; i < w; ++i) c.A[i] = Am[w][i];
+            c.Q = 1.0;
+            for (int l = w + 1; l < hi; ++l) c.Q *= sc(l).nu;
+            for (int j = w + 1; j < hi; ++j) {
+                double b = 1.0;  // prod nu over (w, j)
+                for (int l = w + 1; l < j; ++l) b *= sc(l).nu;
+                c.B[j] = b;
+                c.K2 += b * sc(j).k2;
+                c.K1 += b * sc(j).k1 * Pr[j];
+                for (int i = lo; i < j; ++i) c.C[i] += b * sc(j).k1 * Am[j][i];
+            }
+        }
     }
     for (size_t r = 0; r < runs.size(); ++r) runoff[size_t(runs[r].tl) + 1] = int32_t(r + 1);
     for (size_t i = 1; i < runoff.size(); ++i) runoff[i] = std::max(runoff[i], runoff[i - 1]);
@@ -723,6 +789,7 @@ int build_rs_tables(psw_plan* pl, const std::vector<SegDesc>& desc,
     if (int rc = up(reinterpret_cast<void**>(&pl->d_rs_run), runs.data(), sizeof(RsRun) * runs.size())) return rc;
     if (int rc = up(reinterpret_cast<void**>(&pl->d_rs_runcoef), rcoef.data(), sizeof(SegCoef) * rcoef.size())) return rc;
     if (int rc = up(reinterpret_cast<void**>(&pl->d_rs_runoff), runoff.data(), sizeof(int32_t) * runoff.size())) return rc;
+    if (int rc = up(reinterpret_cast<void**>(&pl->d_rs_cw), cw.data(), sizeof(CarryW) * cw.size())) return rc;
     return up(&pl->d_scoef, sco.data(), sco.size());
 }
 

@@ -70,7 +70,7 @@ def test_full_size_residual_C2_fp32(psw, cuda):
     cuda.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("path", ["AUTO", "STAGED", "TILE"])
+@pytest.mark.parametrize("path", ["AUTO", "STAGED", "RESWEEP", "CLUSTER"])
 def test_linearity_C1(psw, cuda, path):
     cfg, a, b, plan, tdt, lay, shape = _config(psw, cuda, "C1")
     p = getattr(psw, "PATH_" + path)
