@@ -108,44 +108,60 @@ extern "C" int psw_solve_host(const psw_plan* plan, const void* F, int64_t ldf, 
 
     HostPipe& st = pipe_for(plan->device);
     std::lock_guard<std::mutex> lk(st.mu);
-    if (int rc = st.init()) return rc;
-    if (int rc = st.reserve(kSlots * slot_bytes)) return rc;
-    // the pipeline starts after any earlier work of this thread's device
+    int rc = st.init();
+    if (rc == PSW_OK) rc = st.reserve(kSlots * slot_bytes);
+    if (rc != PSW_OK) {
+        cudaSetDevice(prev);
+        return rc;
+    }
+    // the pipeline starts after any earlier work of this thread's device.
+    // A failing call stops issuing, but every copy already queued is waited
+    // for below before returning (the caller may free F and X afterwards),
+    // and the caller's device is restored on every path.
     int64_t launches = 0;
-    int rc = PSW_OK;
+#define PSW_HOST_TRY(expr)                                        \
+    do {                                                          \
+        if (rc == PSW_OK) {                                       \
+            const cudaError_t _e = (expr);                        \
+            if (_e != cudaSuccess) rc = psw::cuda_fail(_e, #expr); \
+        }                                                         \
+    } while (0)
     for (int64_t ci = 0; ci < nchunks && rc == PSW_OK; ++ci) {
         const int slot = int(ci % kSlots);
         const int64_t k0 = ci * c, kc = std::min(c, nrhs - k0);
         char* dbuf = static_cast<char*>(st.buf) + slot * slot_bytes;
         const int64_t dld = layout == PSW_LAYOUT_R ? kc : n;
-        if (ci >= kSlots) PSW_CUDA_TRY(cudaStreamWaitEvent(st.h2d, st.freed[slot], 0));
+        if (ci >= kSlots) PSW_HOST_TRY(cudaStreamWaitEvent(st.h2d, st.freed[slot], 0));
         if (layout == PSW_LAYOUT_R)
-            PSW_CUDA_TRY(cudaMemcpy2DAsync(dbuf, size_t(kc) * es,
+            PSW_HOST_TRY(cudaMemcpy2DAsync(dbuf, size_t(kc) * es,
                                            static_cast<const char*>(F) + size_t(k0) * es,
                                            size_t(ldf) * es, size_t(kc) * es, size_t(n),
                                            cudaMemcpyHostToDevice, st.h2d));
         else
-            PSW_CUDA_TRY(cudaMemcpy2DAsync(dbuf, size_t(n) * es,
+            PSW_HOST_TRY(cudaMemcpy2DAsync(dbuf, size_t(n) * es,
                                            static_cast<const char*>(F) + size_t(k0) * size_t(ldf) * es,
                                            size_t(ldf) * es, size_t(n) * es, size_t(kc),
                                            cudaMemcpyHostToDevice, st.h2d));
-        PSW_CUDA_TRY(cudaEventRecord(st.up[slot], st.h2d));
-        PSW_CUDA_TRY(cudaStreamWaitEvent(st.comp, st.up[slot], 0));
-        rc = psw_solve(plan, dbuf, dld, dbuf, dld, kc, layout, st.comp);
-        launches += psw_last_launch_count();
+        PSW_HOST_TRY(cudaEventRecord(st.up[slot], st.h2d));
+        PSW_HOST_TRY(cudaStreamWaitEvent(st.comp, st.up[slot], 0));
+        if (rc == PSW_OK) {
+            rc = psw_solve(plan, dbuf, dld, dbuf, dld, kc, layout, st.comp);
+            launches += psw_last_launch_count();
+        }
         if (rc != PSW_OK) break;
-        PSW_CUDA_TRY(cudaEventRecord(st.done[slot], st.comp));
-        PSW_CUDA_TRY(cudaStreamWaitEvent(st.d2h, st.done[slot], 0));
+        PSW_HOST_TRY(cudaEventRecord(st.done[slot], st.comp));
+        PSW_HOST_TRY(cudaStreamWaitEvent(st.d2h, st.done[slot], 0));
         if (layout == PSW_LAYOUT_R)
-            PSW_CUDA_TRY(cudaMemcpy2DAsync(static_cast<char*>(X) + size_t(k0) * es, size_t(ldx) * es,
+            PSW_HOST_TRY(cudaMemcpy2DAsync(static_cast<char*>(X) + size_t(k0) * es, size_t(ldx) * es,
                                            dbuf, size_t(kc) * es, size_t(kc) * es, size_t(n),
                                            cudaMemcpyDeviceToHost, st.d2h));
         else
-            PSW_CUDA_TRY(cudaMemcpy2DAsync(static_cast<char*>(X) + size_t(k0) * size_t(ldx) * es,
+            PSW_HOST_TRY(cudaMemcpy2DAsync(static_cast<char*>(X) + size_t(k0) * size_t(ldx) * es,
                                            size_t(ldx) * es, dbuf, size_t(n) * es, size_t(n) * es,
                                            size_t(kc), cudaMemcpyDeviceToHost, st.d2h));
-        PSW_CUDA_TRY(cudaEventRecord(st.freed[slot], st.d2h));
+        PSW_HOST_TRY(cudaEventRecord(st.freed[slot], st.d2h));
     }
+#undef PSW_HOST_TRY
     cudaError_t e1 = cudaStreamSynchronize(st.d2h);
     cudaError_t e2 = cudaStreamSynchronize(st.comp);
     cudaStreamSynchronize(st.h2d);

@@ -211,9 +211,9 @@ int build_rs_tables(psw_plan* pl, const std::vector<SegDesc>& desc,
 // boundary values; backward = carries from the reduced values + K3
 int64_t shard_workspace_bytes(const psw_plan* pl, int64_t N);
 int shard_forward(const psw_plan* pl, const void* F, int64_t ldf, int64_t N, void* ws,
-                  double* partials, cudaStream_t s);
+                  double* partials, int64_t ldv, cudaStream_t s);
 int shard_backward(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_t ldx,
-                   int64_t N, void* ws, const double* V, cudaStream_t s);
+                   int64_t N, void* ws, const double* V, int64_t ldv, cudaStream_t s);
 // AUTO path selection (psw_plan.cpp)
 int auto_path(const psw_plan* pl, const void* F, int64_t ldf, const void* X, int64_t ldx,
               int64_t N, int layout);
@@ -227,6 +227,12 @@ inline void mark(void** events, int nevents, int i, cudaStream_t s) {
     if (events && i < nevents && events[i]) cudaEventRecord(static_cast<cudaEvent_t>(events[i]), s);
 }
 int set_trace(void* buf);  // psw_debug_trace (FUSED kernel phase stamps)
+// Stream-ordered scratch from a library-owned memory pool per device that
+// keeps its memory mapped between solves (the default pool trims at every
+// synchronisation, and remapping ~0.1 GB of per-solve scratch costs more
+// than a small kernel).
+cudaError_t scratch_alloc(void** p, size_t bytes, int device, cudaStream_t s);
+cudaError_t scratch_free(void* p, cudaStream_t s);
 int fill_uniform(void* dst, int dtype, int64_t count, uint64_t seed, uint64_t offset, double lo,
                  double hi, cudaStream_t s);
 int fill_normal(void* dst, int dtype, int64_t count, uint64_t seed, uint64_t offset,

@@ -89,7 +89,7 @@ int launch_multi(const psw_plan* const* plans, int64_t N, const void* Fv, int64_
     const size_t tab_b = sizeof(void*) * tab.size();
     const size_t need = tab_b + sizeof(double) * size_t(N) * (2 * size_t(P) + size_t(p > 0 ? p : 1));
     void* scratch = nullptr;
-    PSW_CUDA_TRY(cudaMallocAsync(&scratch, need, s));
+    PSW_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&scratch), need, p0->device, s));
     PSW_CUDA_TRY(cudaMemcpyAsync(scratch, tab.data(), tab_b, cudaMemcpyHostToDevice, s));
     PSW_CUDA_TRY(cudaStreamSynchronize(s));  // the host table goes out of scope
     auto** dtab = static_cast<const void**>(scratch);
@@ -112,7 +112,7 @@ int launch_multi(const psw_plan* const* plans, int64_t N, const void* Fv, int64_
         V, p);
     ++launches;
     cudaError_t e = cudaGetLastError();
-    cudaFreeAsync(scratch, s);
+    scratch_free(scratch, s);
     if (e != cudaSuccess) return cuda_fail(e, "multi-plan kernels");
     note_launches(launches);
     return PSW_OK;

@@ -724,6 +724,31 @@ namespace psw {
 // (CLUSTER for >= 128 RHS tiles of 128 B, FUSED), then the L2-chunked
 // RESWEEP when a 32-RHS column of F is small next to L2 (its second read
 // then hits L2), then RESWEEP, then STAGED.
+cudaError_t scratch_alloc(void** p, size_t bytes, int device, cudaStream_t s) {
+    static std::mutex mu;
+    static std::vector<cudaMemPool_t> pools;
+    cudaMemPool_t pool = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (size_t(device) >= pools.size()) pools.resize(size_t(device) + 1, nullptr);
+        if (!pools[size_t(device)]) {
+            cudaMemPoolProps props{};
+            props.allocType = cudaMemAllocationTypePinned;
+            props.location.type = cudaMemLocationTypeDevice;
+            props.location.id = device;
+            cudaMemPool_t np = nullptr;
+            if (cudaError_t e = cudaMemPoolCreate(&np, &props)) return e;
+            uint64_t keep = ~uint64_t(0);
+            cudaMemPoolSetAttribute(np, cudaMemPoolAttrReleaseThreshold, &keep);
+            pools[size_t(device)] = np;  // lives for the process
+        }
+        pool = pools[size_t(device)];
+    }
+    return cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
+
+cudaError_t scratch_free(void* p, cudaStream_t s) { return cudaFreeAsync(p, s); }
+
 int auto_path(const psw_plan* pl, const void* F, int64_t ldf, const void* X, int64_t ldx,
               int64_t N, int layout) {
     (void)X;
@@ -731,12 +756,9 @@ int auto_path(const psw_plan* pl, const void* F, int64_t ldf, const void* X, int
     const int64_t es = pl->dtype == PSW_F64 ? 8 : 4;
     if (N * es >= 128 * 128 && cluster_supported(pl, layout, N, F, ldf)) return PSW_PATH_CLUSTER;
     if (fused_supported(pl, layout, N, F, ldf)) return PSW_PATH_FUSED;
-    if (chunked_supported(pl, layout, N)) {
-        int l2 = 0;
-        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, pl->device);
-        const int64_t column = pl->n * es * 32;
-        if (l2 > 0 && column * 8 <= l2 && N * es * pl->n > int64_t(l2) / 2) return PSW_PATH_CHUNKED;
-    }
+    // CHUNKED (RESWEEP over L2-sized RHS chunks) is explicit only: on the fp32
+    // config its per-chunk launches cost more than the re-read they save
+    // (27 vs 10.2 ms, round 2)
     if (resweep_supported(pl, layout, N)) return PSW_PATH_RESWEEP;
     return PSW_PATH_STAGED;
 }

@@ -305,6 +305,8 @@ __global__ void __launch_bounds__(128) rs_fold_kernel(int64_t N, const int32_t* 
                                                       double* __restrict__ br) {
     const int tl = blockIdx.y;
     const int64_t k = int64_t(blockIdx.x) * 128 + threadIdx.x;
+    pdl_trigger();
+    pdl_wait();  // K1's run aggregates
     if (k >= N) return;
     double R, L;
     fold_fwd(sc, rc, runoff[tl], runoff[tl + 1], k, R, L);
@@ -319,10 +321,49 @@ __global__ void __launch_bounds__(128) rs_carry_kernel(int64_t N, int p, int t0,
                                                        int64_t ldv) {
     const int tl = blockIdx.y, t = t0 + tl;
     const int64_t k = int64_t(blockIdx.x) * 128 + threadIdx.x;
+    pdl_trigger();
+    pdl_wait();  // the boundary values
     if (k >= N) return;
     const double xl = t > 0 ? V[int64_t(t - 1) * ldv + k] : 0.0;
     const double xb = t < p ? V[int64_t(t) * ldv + k] : 0.0;
     fold_bwd(sc, rc, runoff[tl], runoff[tl + 1], k, xl, xb);
+}
+
+// Whole-system boundary values V = MR right + ML left (P <= kCombMaxP): CTA
+// (x, y) forms rows 8y .. 8y + 7 of V for 32 RHS; the CTA's betas and its
+// eight combination-matrix rows are staged in shared memory first (all
+// loads in flight), warp w then forms row 8y + w.
+__global__ void __launch_bounds__(256) rs_vmat_kernel(int64_t N, int64_t ld, int P, int p,
+                                                      const double* __restrict__ gcmat,
+                                                      const double* __restrict__ bl,
+                                                      const double* __restrict__ br,
+                                                      double* __restrict__ V, int64_t ldv) {
+    extern __shared__ double sbv[];  // [2P][32] betas: right_u, then left_u; [8][2P] rows
+    double* sm = sbv + 2 * P * 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t k0 = int64_t(blockIdx.x) * 32;
+    const int j0 = int(blockIdx.y) * 8;
+    const int nj = min(8, p - j0);
+    for (int i = threadIdx.x; i < nj * 2 * P; i += blockDim.x) sm[i] = gcmat[int64_t(j0) * 2 * P + i];
+    pdl_trigger();
+    pdl_wait();  // the folds' block betas
+    for (int i = threadIdx.x; i < 2 * P * 32; i += blockDim.x) {
+        const int u = i >> 5, l = i & 31;
+        const int64_t k = k0 + l;
+        double v = 0.0;
+        if (k < N) {
+            if (u < P)
+                v = u < p ? br[int64_t(u) * ld + k] : 0.0;  // betas.hpp:46-49
+            else
+                v = u - P > 0 ? bl[int64_t(u - P) * ld + k] : 0.0;  // betas.hpp:51-55
+        }
+        sbv[i] = v;
+    }
+    __syncthreads();
+    const int64_t k = k0 + lane;
+    if (k >= N || warp >= nj) return;
+    const double(*sb)[32] = reinterpret_cast<const double(*)[32]>(sbv);
+    V[int64_t(j0 + warp) * ldv + k] = cmat_row(sm + warp * 2 * P, sb, 2 * P, lane);
 }
 
 // Row shards: the rank's share of every boundary value, one thread per
@@ -332,7 +373,7 @@ __global__ void __launch_bounds__(128) rs_vpart_kernel(int64_t N, int64_t ld, in
                                                        int nb, const double* __restrict__ cmat,
                                                        const double* __restrict__ bl,
                                                        const double* __restrict__ br,
-                                                       double* __restrict__ out) {
+                                                       double* __restrict__ out, int64_t ldo) {
     const int j = blockIdx.y;
     const int64_t k = int64_t(blockIdx.x) * 128 + threadIdx.x;
     if (k >= N) return;
@@ -343,7 +384,7 @@ __global__ void __launch_bounds__(128) rs_vpart_kernel(int64_t N, int64_t ld, in
         if (t < p) a0 = fma(m[t], br[int64_t(tl) * ld + k], a0);
         if (t > 0) a1 = fma(m[P + t], bl[int64_t(tl) * ld + k], a1);
     }
-    out[int64_t(j) * N + k] = a0 + a1;
+    out[int64_t(j) * ldo + k] = a0 + a1;
 }
 
 // ------------------------------------------------------------------ K3
@@ -586,11 +627,19 @@ int launch_solve(const psw_plan* pl, const T* F, int64_t ldf, T* X, int64_t ldx,
                         : launch_solve_t<T, LS, false>(pl, F, ldf, X, ldx, N, w, V, ldv, s);
 }
 
-// K2 of a whole-system plan: boundary values into w.V, run carries in place
+// K2 of a whole-system plan: boundary values into w.V, run carries in place.
+// fold (one thread per RHS and block) -> V (the combination matrix for
+// P <= kCombMaxP, else the STAGED dichotomy) -> carry (RHS x block), each a
+// programmatic dependent launch of the one before. PSW_RESWEEP_COMB=1: the
+// single-kernel rs_comb_kernel (one CTA per 32 RHS).
 int launch_comb(const psw_plan* pl, int64_t N, const Work& w, cudaStream_t s, int64_t& launches) {
     const int P = int(pl->P), p = int(pl->p);
     const unsigned gx = unsigned((N + 127) / 128);
-    if (pl->d_cmat && P <= kCombMaxP) {
+    static const int single = [] {
+        const char* e = std::getenv("PSW_RESWEEP_COMB");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (single == 1 && pl->d_cmat && P <= kCombMaxP) {
         const size_t cmb = sizeof(double) * size_t(std::max(p, 1)) * 2 * P;
         static std::once_flag once;
         cudaError_t e = cudaSuccess;
@@ -604,16 +653,22 @@ int launch_comb(const psw_plan* pl, int64_t N, const Work& w, cudaStream_t s, in
         ++launches;
         return PSW_OK;
     }
-    rs_fold_kernel<<<dim3(gx, unsigned(P)), 128, 0, s>>>(N, pl->d_rs_runoff, pl->d_rs_runcoef,
-                                                         w.sc, w.bl, w.br);
+    PSW_CUDA_TRY(launch_pdl(rs_fold_kernel, dim3(gx, unsigned(P)), dim3(128), 0, s, N,
+                            pl->d_rs_runoff, pl->d_rs_runcoef, w.sc, w.bl, w.br));
     ++launches;
     if (p > 0) {
-        // the combination runs over the padded pitch (columns >= N unused)
-        if (int rc = launch_combine(pl, w.bl, w.br, w.sc.ld, w.V, s)) return rc;
+        if (pl->d_cmat && P <= kCombMaxP) {
+            PSW_CUDA_TRY(launch_pdl(rs_vmat_kernel, dim3(unsigned((N + 31) / 32), unsigned((p + 7) / 8)),
+                                    dim3(256), sizeof(double) * 2 * P * 40, s, N, w.sc.ld, P, p,
+                                    pl->d_cmat, w.bl, w.br, w.V, w.ldv));
+        } else {
+            // the combination runs over the padded pitch (columns >= N unused)
+            if (int rc = launch_combine(pl, w.bl, w.br, w.sc.ld, w.V, s)) return rc;
+        }
         ++launches;
     }
-    rs_carry_kernel<<<dim3(gx, unsigned(P)), 128, 0, s>>>(N, p, 0, pl->d_rs_runoff,
-                                                          pl->d_rs_runcoef, w.sc, w.V, w.ldv);
+    PSW_CUDA_TRY(launch_pdl(rs_carry_kernel, dim3(gx, unsigned(P)), dim3(128), 0, s, N, p, 0,
+                            pl->d_rs_runoff, pl->d_rs_runcoef, w.sc, w.V, w.ldv));
     ++launches;
     return PSW_OK;
 }
@@ -803,12 +858,12 @@ bool resweep_supported(const psw_plan* pl, int layout, int64_t N) {
 int solve_resweep(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_t ldx, int64_t N,
                   int layout, cudaStream_t s, void** ev, int nev) {
     void* mem = nullptr;
-    PSW_CUDA_TRY(cudaMallocAsync(&mem, work_bytes(pl, N, true), s));
+    PSW_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&mem), work_bytes(pl, N, true), pl->device, s));
     const Work w = carve(pl, N, mem, true);
     int64_t launches = 0;
     int rc = solve_all_dt(pl, F, ldf, X, ldx, N, layout, w, true, s, ev, nev, launches);
     cudaError_t e = cudaGetLastError();
-    cudaFreeAsync(mem, s);
+    scratch_free(mem, s);
     if (rc != PSW_OK) return rc;
     if (e != cudaSuccess) return cuda_fail(e, "resweep kernels");
     note_launches(launches);
@@ -829,7 +884,7 @@ int solve_chunked(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64
                                           nchunks));
     const size_t wb = (work_bytes(pl, c, true) + 255) & ~size_t(255);
     void* mem = nullptr;
-    PSW_CUDA_TRY(cudaMallocAsync(&mem, wb * size_t(nst), s));
+    PSW_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&mem), wb * size_t(nst), pl->device, s));
     ChunkStreams& cs = chunk_streams(pl->device);
     std::lock_guard<std::mutex> lk(cs.mu);
     if (!cs.ready) {
@@ -859,7 +914,7 @@ int solve_chunked(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64
     }
     mark(ev, nev, 1, s);
     cudaError_t e = cudaGetLastError();
-    cudaFreeAsync(mem, s);
+    scratch_free(mem, s);
     cudaEventDestroy(fork);
     for (int i = 0; i < nst; ++i) cudaEventDestroy(join[i]);
     if (rc != PSW_OK) return rc;
@@ -874,7 +929,7 @@ int64_t shard_workspace_bytes(const psw_plan* pl, int64_t N) {
 }
 
 int shard_forward(const psw_plan* pl, const void* Fv, int64_t ldf, int64_t N, void* ws,
-                  double* partials, cudaStream_t s) {
+                  double* partials, int64_t ldv, cudaStream_t s) {
     const Work w = carve(pl, N, ws, false);
     const int nb = int(pl->blk1 - pl->blk0), p = int(pl->p);
     int rc = pl->dtype == PSW_F64
@@ -888,7 +943,7 @@ int shard_forward(const psw_plan* pl, const void* Fv, int64_t ldf, int64_t N, vo
     if (p > 0) {
         rs_vpart_kernel<<<dim3(gx, unsigned(p)), 128, 0, s>>>(N, w.sc.ld, int(pl->P), p,
                                                               int(pl->blk0), nb, pl->d_cmat, w.bl,
-                                                              w.br, partials);
+                                                              w.br, partials, ldv);
         ++launches;
     }
     PSW_CUDA_TRY(cudaGetLastError());
@@ -897,17 +952,17 @@ int shard_forward(const psw_plan* pl, const void* Fv, int64_t ldf, int64_t N, vo
 }
 
 int shard_backward(const psw_plan* pl, const void* Fv, int64_t ldf, void* Xv, int64_t ldx,
-                   int64_t N, void* ws, const double* V, cudaStream_t s) {
+                   int64_t N, void* ws, const double* V, int64_t ldv, cudaStream_t s) {
     const Work w = carve(pl, N, ws, false);
     const int nb = int(pl->blk1 - pl->blk0), p = int(pl->p);
     const unsigned gx = unsigned((N + 127) / 128);
     rs_carry_kernel<<<dim3(gx, unsigned(nb)), 128, 0, s>>>(N, p, int(pl->blk0), pl->d_rs_runoff,
-                                                           pl->d_rs_runcoef, w.sc, V, N);
+                                                           pl->d_rs_runcoef, w.sc, V, ldv);
     int rc = pl->dtype == PSW_F64
                  ? launch_solve<double, false>(pl, static_cast<const double*>(Fv), ldf,
-                                               static_cast<double*>(Xv), ldx, N, w, V, N, true, s)
+                                               static_cast<double*>(Xv), ldx, N, w, V, ldv, true, s)
                  : launch_solve<float, false>(pl, static_cast<const float*>(Fv), ldf,
-                                              static_cast<float*>(Xv), ldx, N, w, V, N, true, s);
+                                              static_cast<float*>(Xv), ldx, N, w, V, ldv, true, s);
     if (rc) return rc;
     PSW_CUDA_TRY(cudaGetLastError());
     note_launches(2);

@@ -94,6 +94,24 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 
 // Producer: everything a tile needs, in the order the consumers take them.
 // Coef = FusedFwd<T> (K1) or SolveCoef<T> (K3); AUX: K3's carries.
+constexpr int kTmaMaxStages = 4;
+
+// K3 carries of one tile: [D_in | x_B | x_l] x runs, W doubles each
+template <typename T>
+__device__ __forceinline__ void tma_aux(const RsGroup& G, int col, const TmaSched& sch,
+                                        const RsScratch& sc, const double* __restrict__ V,
+                                        int64_t ldv, unsigned char* stage, uint64_t* bar) {
+    constexpr int W = kTmaRowBytes / int(sizeof(T));
+    double* aux = reinterpret_cast<double*>(stage + size_t(kTmaRows) * kTmaRowBytes);
+    for (int j = 0; j < G.r1 - G.r0; ++j) {
+        const int64_t o = int64_t(G.r0 + j) * sc.ld + col;
+        bulk_load(aux + (0 * sch.mr + j) * W, sc.dt + o, W * 8, bar);
+        bulk_load(aux + (1 * sch.mr + j) * W, sc.br + o, W * 8, bar);
+        const int t = G.t0 + j;
+        if (t > 0) bulk_load(aux + (2 * sch.mr + j) * W, V + int64_t(t - 1) * ldv + col, W * 8, bar);
+    }
+}
+
 template <typename T, typename Coef, bool AUX>
 __device__ __forceinline__ void tma_produce(const CUtensorMap* m32, const CUtensorMap* m1,
                                             const TmaSched& sch, int32_t row0,
@@ -112,6 +130,8 @@ __device__ __forceinline__ void tma_produce(const CUtensorMap* m32, const CUtens
     const uint64_t pol = AUX && sch.reverse ? policy_evict_first() : policy_evict_normal();
     TileIt it;
     RsGroup G{};
+    RsGroup pend_g[kTmaMaxStages];
+    int pend_c[kTmaMaxStages];
     int i = 0;
     bool ok = it.start(sch);
     if (ok) G = groups[it.g];
@@ -144,14 +164,21 @@ __device__ __forceinline__ void tma_produce(const CUtensorMap* m32, const CUtens
             tma_load_2d_hint(stage + size_t(j) * 32 * kTmaRowBytes, m32, col, r0 + 32 * j, &full[st], pol);
         for (int r = n32 * 32; r < rows; ++r)
             tma_load_2d_hint(stage + size_t(r) * kTmaRowBytes, m1, col, r0 + r, &full[st], pol);
-        if (AUX) {  // [D_in | x_B | x_l] x runs, W doubles each
-            double* aux = reinterpret_cast<double*>(stage + size_t(kTmaRows) * kTmaRowBytes);
-            for (int j = 0; j < nr; ++j) {
-                const int64_t o = int64_t(G.r0 + j) * sc.ld + col;
-                bulk_load(aux + (0 * sch.mr + j) * W, sc.dt + o, W * 8, &full[st]);
-                bulk_load(aux + (1 * sch.mr + j) * W, sc.br + o, W * 8, &full[st]);
-                const int t = G.t0 + j;
-                if (t > 0) bulk_load(aux + (2 * sch.mr + j) * W, V + int64_t(t - 1) * ldv + col, W * 8, &full[st]);
+        if (AUX) {
+            // K3 is a programmatic dependent launch of the carry kernel: the
+            // first S tiles' F rows go out before waiting for the carries
+            if (i < kTmaMaxStages) {
+                pend_g[i] = G;
+                pend_c[i] = col;
+            }
+            const bool last = !TileIt(it).next(sch);
+            if (i == sch.stages - 1 || (i < sch.stages && last)) {
+                pdl_wait();
+                for (int q = 0; q <= i; ++q)
+                    tma_aux<T>(pend_g[q], pend_c[q], sch, sc, V, ldv,
+                               stage0 + size_t(q) * stage_bytes, &full[q]);
+            } else if (i >= sch.stages) {
+                tma_aux<T>(G, col, sch, sc, V, ldv, stage, &full[st]);
             }
         }
         ok = it.next(sch);
@@ -174,6 +201,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rs_part_tma(
     uint64_t* full = reinterpret_cast<uint64_t*>(xch + 4 * kRsSeg * W);
     uint64_t* empty = full + sch.stages;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    pdl_trigger();  // the fold kernel may be scheduled as K1's CTAs retire
     if (threadIdx.x == 0) {
         for (int s = 0; s < sch.stages; ++s) {
             mbar_init(&full[s], 1);
@@ -763,7 +791,7 @@ bool tma_plan(const psw_plan* pl, int64_t N, TmaSched& sch, size_t& stage_bytes,
     stage_bytes = size_t(kTmaRows) * kTmaRowBytes + (AUX ? size_t(3) * sch.mr * W * 8 : 0);
     cbuf_bytes = size_t(AUX ? kMetaK3 : kMetaK1) + size_t(kTmaRows) * sizeof(Coef);
     const size_t xch = size_t(AUX ? 2 : 4) * kRsSeg * W * 8;
-    sch.stages = tma_env("PSW_TMA_STAGES", 3);
+    sch.stages = std::min(tma_env("PSW_TMA_STAGES", 3), kTmaMaxStages);
     while (sch.stages > 2 && tma_smem(sch.stages, stage_bytes, cbuf_bytes, xch) > size_t(maxs))
         --sch.stages;
     smem = tma_smem(sch.stages, stage_bytes, cbuf_bytes, xch);
@@ -854,10 +882,12 @@ bool launch_solve_tma(const psw_plan* pl, const T* F, int64_t ldf, T* X, int64_t
                 rc = cuda_fail(e, "rs_solve_tma_st attribute");
                 return true;
             }
-            kern<<<tma_grid(pl, sch), kTmaThreads, smem, s>>>(
-                m32, m1, x32, x1, N, int32_t(pl->row0), sch, pl->d_rs_group, pl->d_rs_run,
-                pl->d_segdesc, pl->d_seg, static_cast<const SolveCoef<T>*>(pl->d_scoef), pl->d_rs_cw,
-                sc, V, ldv, uint32_t(sb), uint32_t(cb));
+            if (cudaError_t e = launch_pdl(kern, dim3(tma_grid(pl, sch)), dim3(kTmaThreads), smem, s,
+                                           m32, m1, x32, x1, N, int32_t(pl->row0), sch,
+                                           pl->d_rs_group, pl->d_rs_run, pl->d_segdesc, pl->d_seg,
+                                           static_cast<const SolveCoef<T>*>(pl->d_scoef),
+                                           pl->d_rs_cw, sc, V, ldv, uint32_t(sb), uint32_t(cb)))
+                rc = cuda_fail(e, "rs_solve_tma_st launch");
             return true;
         }
     }

@@ -134,7 +134,7 @@ int psw_shard_forward(const psw_plan* plan, const void* F, int64_t ldf, int64_t 
     }
     if (nrhs == 0) return PSW_OK;
     return on_device(plan->device, [&] {
-        return psw::shard_forward(plan, F, ldf, nrhs, workspace, partials,
+        return psw::shard_forward(plan, F, ldf, nrhs, workspace, partials, nrhs,
                                   static_cast<cudaStream_t>(stream));
     });
 }
@@ -150,7 +150,7 @@ int psw_shard_backward(const psw_plan* plan, const void* F, int64_t ldf, void* X
     }
     if (nrhs == 0) return PSW_OK;
     return on_device(plan->device, [&] {
-        return psw::shard_backward(plan, F, ldf, X, ldx, nrhs, workspace, partials,
+        return psw::shard_backward(plan, F, ldf, X, ldx, nrhs, workspace, partials, nrhs,
                                    static_cast<cudaStream_t>(stream));
     });
 }
@@ -227,19 +227,22 @@ int psw_shard_solve(const psw_plan* plan, const void* F, int64_t ldf, void* X, i
     return on_device(plan->device, [&]() -> int {
         const int64_t p = plan->p;
         const size_t ws = (size_t(psw::shard_workspace_bytes(plan, nrhs)) + 255) & ~size_t(255);
-        const size_t vb = sizeof(double) * size_t(p > 0 ? p : 1) * size_t(nrhs);
+        // boundary values at a pitch of whole 64-RHS chunks (the TMA solve
+        // kernel copies them chunk by chunk); the padding rides along in the sum
+        const int64_t ldv = (nrhs + 63) / 64 * 64;
+        const size_t vb = sizeof(double) * size_t(p > 0 ? p : 1) * size_t(ldv);
         void* mem = nullptr;
-        PSW_CUDA_TRY(cudaMallocAsync(&mem, ws + vb, s));
+        PSW_CUDA_TRY(psw::scratch_alloc(&mem, ws + vb, plan->device, s));
         double* V = reinterpret_cast<double*>(static_cast<char*>(mem) + ws);
-        int rc = psw::shard_forward(plan, F, ldf, nrhs, mem, V, s);
+        int rc = psw::shard_forward(plan, F, ldf, nrhs, mem, V, ldv, s);
         // the exchange (a 1-rank communicator still runs NCCL's in-place sum)
         if (rc == PSW_OK && p > 0 && comm) {
-            if (ncclResult_t r = nccl().AllReduce(V, V, size_t(p) * size_t(nrhs), ncclFloat64,
+            if (ncclResult_t r = nccl().AllReduce(V, V, size_t(p) * size_t(ldv), ncclFloat64,
                                                   ncclSum, comm->comm, s))
                 rc = nccl_fail(r, "ncclAllReduce");
         }
-        if (rc == PSW_OK) rc = psw::shard_backward(plan, F, ldf, X, ldx, nrhs, mem, V, s);
-        cudaFreeAsync(mem, s);
+        if (rc == PSW_OK) rc = psw::shard_backward(plan, F, ldf, X, ldx, nrhs, mem, V, ldv, s);
+        psw::scratch_free(mem, s);
         return rc;
     });
 }

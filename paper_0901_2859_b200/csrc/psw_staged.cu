@@ -500,7 +500,7 @@ int solve_staged(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_
     if (!br) need += sizeof(double) * P * N;
     if (!V) need += sizeof(double) * (p > 0 ? p : 1) * N;
     if (need) {
-        PSW_CUDA_TRY(cudaMallocAsync(&scratch, need, s));
+        PSW_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&scratch), need, pl->device, s));
         char* c = static_cast<char*>(scratch);
         if (!bl) { bl = reinterpret_cast<double*>(c); c += sizeof(double) * P * N; }
         if (!br) { br = reinterpret_cast<double*>(c); c += sizeof(double) * P * N; }
@@ -509,7 +509,7 @@ int solve_staged(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_
     int rc = pl->dtype == PSW_F64
                  ? launch_staged<double>(pl, F, ldf, X, ldx, N, layout, s, bl, br, V, events, nevents)
                  : launch_staged<float>(pl, F, ldf, X, ldx, N, layout, s, bl, br, V, events, nevents);
-    if (scratch) cudaFreeAsync(scratch, s);
+    if (scratch) scratch_free(scratch, s);
     return rc;
 }
 

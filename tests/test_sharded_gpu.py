@@ -155,3 +155,26 @@ def test_shard_rejects_bad_world(psw, cuda):
     comm.close()
     with pytest.raises(ValueError):  # a shard plan refuses psw_solve
         plan.solve(F, F.clone())
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_rhs_slices_equal_full_batch(psw, cuda, world):
+    """RHS-sharded comparison mode: each rank's slice of one batch (rhs_slice)
+    solved on its own is bitwise the full-batch solve of those RHS (RESWEEP:
+    the per-RHS arithmetic does not depend on the batch width)."""
+    from paper_0901_2859_b200.configs import CONFIGS
+    from paper_0901_2859_b200.sharded import rhs_slice
+    cfg = CONFIGS["C3"].with_(n=65536, nrhs=256)
+    a, b = cfg.matrix_ab(0)
+    A = psw.TridiagMatrix.symmetric(a, b)
+    part = psw.decompose(cfg.n, 64).induced_partition()
+    plan = psw.Plan(A, part)
+    F = cuda.empty((cfg.n, cfg.nrhs), dtype=cuda.float64, device="cuda")
+    psw.fill_uniform(F, 3, -1.0, 1.0)
+    full = plan.solve(F, cuda.empty_like(F), path=psw.PATH_RESWEEP)
+    for r in range(world):
+        k0, k1 = rhs_slice(cfg.nrhs, world, r)
+        Fs = F[:, k0:k1].contiguous()
+        Xs = plan.solve(Fs, cuda.empty_like(Fs), path=psw.PATH_RESWEEP)
+        cuda.cuda.synchronize()
+        assert bool((Xs == full[:, k0:k1]).all())

@@ -4,6 +4,6 @@ for e in "$@"; do
   python -c "
 import json
 d=json.loads(open('gpurun_out/e.json').read().strip().splitlines()[-1])
-print('$e |', d['config'].get('path'), round(d['ms_per_step'],4), round(d['roofline']['frac'],3), {n:round(x['ms'],4) for n,x in d.get('kernels',{}).items()})
+print('$e |', d['config'].get('path'), round(d['ms_per_step'],4), round(d['roofline']['frac'],3), {n:round(x['ms'],4) for n,x in d.get('kernels',{}).items()}, {k:round(v,4) for k,v in d.get('step_ms',{}).items()})
 " || tail -2 gpurun_out/e.err
 done
