@@ -1,0 +1,12 @@
+# round-2 evidence pass (one gpurun call): tests, smoke, default bench (C3),
+# reference arm, the other configs, ncu launch list + full captures
+mkdir -p gpurun_out/r02
+O=gpurun_out/r02
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
+timeout 900 python bench.py > $O/bench_default.json 2> $O/bench_default.err
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference.json 2> $O/bench_reference.err
+for c in C0 C1 C2 C4; do timeout 900 python bench.py --config $c --steps 20 --warmup 3 > $O/bench_$c.json 2> $O/bench_$c.err; done
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $O/ncu_launches_C3.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_launch.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"rs_part_tma|rs_solve_tma_st" -s 2 -c 2 -o $O/prof_C3 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_full_C3.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:cluster_kernel -s 2 -c 1 -o $O/prof_C1 python bench.py --config C1 --steps 1 --warmup 2 --no-cpu-baseline --no-e2e > $O/ncu_full_C1.log 2>&1
