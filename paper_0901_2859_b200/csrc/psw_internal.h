@@ -158,6 +158,7 @@ struct psw_plan {
 
     // RESWEEP tables over the plan's own segments (psw_resweep.cu)
     int rs_ngroups = 0, rs_nruns = 0, rs_maxruns = 0;  // maxruns: most runs in one group
+    int rs_minseg = 0;                                  // rows of the shortest own segment
     psw::RsGroup* d_rs_group = nullptr;
     psw::RsRun* d_rs_run = nullptr;
     psw::SegCoef* d_rs_runcoef = nullptr;  // composed affine map of every run

@@ -776,6 +776,10 @@ int build_rs_tables(psw_plan* pl, const std::vector<SegDesc>& desc,
         }
         g.r1 = int32_t(runs.size());
         pl->rs_maxruns = std::max(pl->rs_maxruns, int(g.r1 - g.r0));
+        for (int q = g0; q < g1; ++q) {
+            const int len = desc[size_t(q)].b - desc[size_t(q)].a;
+            pl->rs_minseg = pl->rs_minseg ? std::min(pl->rs_minseg, len) : len;
+        }
         groups.push_back(g);
     }
     static_assert(kRsSeg <= 8, "CarryW holds 8 slots");

@@ -605,14 +605,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rs_solve_tma_st(
     extern __shared__ __align__(1024) unsigned char dyn[];
     unsigned char* stage0 = dyn;
     unsigned char* cbuf0 = dyn + size_t(sch.stages) * stage_bytes;
-    double* xch = reinterpret_cast<double*>(cbuf0 + 2 * size_t(cbuf_bytes));  // s_d, s_l
-    uint64_t* full = reinterpret_cast<uint64_t*>(xch + 2 * kRsSeg * W);
+    uint64_t* full = reinterpret_cast<uint64_t*>(cbuf0 + 2 * size_t(cbuf_bytes));
     uint64_t* empty = full + sch.stages;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < sch.stages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], kTmaWarps);
         }
         fence_mbar_init();
     }
@@ -624,8 +623,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rs_solve_tma_st(
                                                cbuf_bytes, full, empty);
         return;
     }
-    double(*s_d)[W] = reinterpret_cast<double(*)[W]>(xch);
-    double(*s_l)[W] = s_d + kRsSeg;
     TileIt it;
     int i = 0, prev_st = -1;
     for (bool ok = it.start(sch); ok; ok = it.next(sch), ++i) {
@@ -677,17 +674,21 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rs_solve_tma_st(
                 fwd(std::true_type{});
             else
                 fwd(std::false_type{});
-        }
+            // the segment's own (now dead) first rows carry its exchange
+            // values: doubles [0, W) = d~ end, [W, 2W) = Lam~ (as doubles)
+            __syncwarp();
+            double* xw = reinterpret_cast<double*>(tile + a * W);
 #pragma unroll
-        for (int u = 0; u < VPL; ++u) {
-            s_d[warp][lane + 32 * u] = double(d[u]);
-            s_l[warp][lane + 32 * u] = double(lx[u]);
+            for (int u = 0; u < VPL; ++u) {
+                xw[lane + 32 * u] = double(d[u]);
+                xw[W + lane + 32 * u] = double(lx[u]);
+            }
         }
         consumers_sync();
+        T D[VPL], x[VPL], xl[VPL];
         if (sv) {
             // the segment's exact carries in closed form over its run (CarryW)
             const CarryW& q = cws[warp];
-            T D[VPL], x[VPL], xl[VPL];
 #pragma unroll
             for (int u = 0; u < VPL; ++u) {
                 const int l = lane + 32 * u;
@@ -698,14 +699,19 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rs_solve_tma_st(
 #pragma unroll
                 for (int k = 0; k < kRsSeg; ++k)
                     if (k < ns) {
-                        const double dd = s_d[k][l];
+                        const double* xk =
+                            reinterpret_cast<const double*>(tile + (mt->desc[k].a - G.ra) * W);
+                        const double dd = xk[l];
                         dc = fma(q.A[k], dd, dc);
-                        xc = fma(q.C[k], dd, fma(q.B[k], s_l[k][l], xc));
+                        xc = fma(q.C[k], dd, fma(q.B[k], xk[W + l], xc));
                     }
                 D[u] = T(dc);
                 x[u] = T(xc);
                 xl[u] = T(rL);
             }
+        }
+        consumers_sync();  // every warp has its carries: the exchange rows may be overwritten
+        if (sv) {
             auto bwd = [&](auto full_) {
                 constexpr bool FULL = decltype(full_)::value;
 #pragma unroll
@@ -726,15 +732,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rs_solve_tma_st(
             else
                 bwd(std::false_type{});
         }
-        fence_proxy_async_smem();  // x (generic proxy) before the TMA store reads it
-        consumers_sync();          // also: the exchange arrays are free for the next tile
-        if (threadIdx.x == 0) {
-            const int rows = G.rb - G.ra, n32 = rows >> 5, col = it.c * W, r0 = G.ra - row0;
-            for (int j = 0; j < n32; ++j)
-                tma_store_2d(&x32, col, r0 + 32 * j, tile + size_t(j) * 32 * W);
-            for (int r = n32 * 32; r < rows; ++r) tma_store_2d(&x1, col, r0 + r, tile + size_t(r) * W);
+        // each warp stores its own rows as soon as they are written
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            if (sv) {
+                const int col = it.c * W, r0 = sd.a - row0, n32 = len >> 5;
+                const T* src = tile + a * W;
+                for (int j = 0; j < n32; ++j) tma_store_2d(&x32, col, r0 + 32 * j, src + size_t(j) * 32 * W);
+                for (int r = n32 * 32; r < len; ++r) tma_store_2d(&x1, col, r0 + r, src + size_t(r) * W);
+            }
             bulk_commit();
-            // the previous tile's store has read its stage: release it
+            // this warp's previous store has read its stage
             if (prev_st >= 0) {
                 bulk_wait_read<1>();
                 mbar_arrive(&empty[prev_st]);
@@ -742,7 +751,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rs_solve_tma_st(
         }
         prev_st = st;
     }
-    if (threadIdx.x == 0) bulk_wait_all();
+    if (lane == 0) bulk_wait_all();
 }
 
 // ------------------------------------------------------------------ host side
@@ -790,7 +799,7 @@ bool tma_plan(const psw_plan* pl, int64_t N, TmaSched& sch, size_t& stage_bytes,
     sch.nchunks = int((N + W - 1) / W);
     stage_bytes = size_t(kTmaRows) * kTmaRowBytes + (AUX ? size_t(3) * sch.mr * W * 8 : 0);
     cbuf_bytes = size_t(AUX ? kMetaK3 : kMetaK1) + size_t(kTmaRows) * sizeof(Coef);
-    const size_t xch = size_t(AUX ? 2 : 4) * kRsSeg * W * 8;
+    const size_t xch = store ? 0 : size_t(AUX ? 2 : 4) * kRsSeg * W * 8;
     sch.stages = std::min(tma_env("PSW_TMA_STAGES", 3), kTmaMaxStages);
     while (sch.stages > 2 && tma_smem(sch.stages, stage_bytes, cbuf_bytes, xch) > size_t(maxs))
         --sch.stages;
@@ -807,7 +816,7 @@ bool tma_plan(const psw_plan* pl, int64_t N, TmaSched& sch, size_t& stage_bytes,
     // stage: >= S - 2 tiles, any unit for S <= 3 (and S >= 2, or the ring
     // would wait on itself).
     const int need = store ? std::max(1, sch.stages - 2) : (AUX ? sch.stages : sch.stages - 1);
-    int cs = std::max(tma_env("PSW_TMA_CS", 8), need);
+    int cs = std::max(tma_env("PSW_TMA_CS", 4), need);
     if (sch.nchunks < need) sch.stages = AUX ? std::max(1, sch.nchunks) : 2;
     if (store && sch.stages < 2) return false;
     if (sch.nchunks <= cs) {
@@ -871,7 +880,9 @@ bool launch_solve_tma(const psw_plan* pl, const T* F, int64_t ldf, T* X, int64_t
     if (!tma_enabled() || (ldv & 1) || ldv < (N + W - 1) / W * W) return false;
     CUtensorMap m32, m1;
     if (!tma_encode<T>(F, ldf, N, pl->row1 - pl->row0, &m32, &m1)) return false;
-    if (tma_env("PSW_K3_STORE", 1)) {
+    // the store variant lends each segment's first rows to the exchange
+    // (2 W doubles = W / 16 rows of 256 bytes)
+    if (tma_env("PSW_K3_STORE", 1) && pl->rs_minseg >= W / 16) {
         CUtensorMap x32, x1;
         if (tma_encode<T>(X, ldx, N, pl->row1 - pl->row0, &x32, &x1)) {
             TmaSched sch;
