@@ -233,13 +233,16 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rs_part_tma(
         const RsGroup G = mt->g;
         const bool sv = warp < G.s1 - G.s0;
         T d[VPL], lx[VPL];
-        double br[VPL], bl[VPL];
+        // segment beta partials in the solve precision (fp32: one FFMA per
+        // product instead of two conversions and a DFMA; the 32-row partials
+        // are summed in fp64 by the run fold), fp64 otherwise
+        T br[VPL], bl[VPL];
 #pragma unroll
         for (int v = 0; v < VPL; ++v) {
             d[v] = T(0);
             lx[v] = T(0);
-            br[v] = 0.0;
-            bl[v] = 0.0;
+            br[v] = T(0);
+            bl[v] = T(0);
         }
         if (sv) {
             const SegDesc sd = mt->desc[warp];
@@ -256,8 +259,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rs_part_tma(
                         for (int v = 0; v < VPL; ++v) {
                             const T fv = f[r * W + 32 * v];
                             d[v] = fma(q.ma, d[v], fv * q.rp);
-                            br[v] = fma(double(fv), double(q.gr), br[v]);
-                            bl[v] = fma(double(fv), double(q.gl), bl[v]);
+                            br[v] = fma(fv, q.gr, br[v]);
+                            bl[v] = fma(fv, q.gl, bl[v]);
                             lx[v] = fma(q.lam, d[v], lx[v]);
                         }
                     }
@@ -272,8 +275,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rs_part_tma(
         for (int v = 0; v < VPL; ++v) {
             s_d[warp][lane + 32 * v] = double(d[v]);
             s_l[warp][lane + 32 * v] = double(lx[v]);
-            s_r[warp][lane + 32 * v] = br[v];
-            s_b[warp][lane + 32 * v] = bl[v];
+            s_r[warp][lane + 32 * v] = double(br[v]);
+            s_b[warp][lane + 32 * v] = double(bl[v]);
         }
         consumers_sync();
         if (warp < G.r1 - G.r0) {  // one warp per run folds its segments (as rs_part_kernel)
