@@ -48,7 +48,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-PATHS = ["auto", "staged", "fused", "chunked", "resweep", "cluster"]
+PATHS = ["auto", "staged", "fused", "resweep", "cluster"]
 
 
 def _args():
@@ -394,7 +394,7 @@ def run(args, cfg, overridden):
     es = 8 if dt == psw.F64 else 4
     layout = psw.LAYOUT_R if cfg.layout == "R" else psw.LAYOUT_S
     path = {"auto": psw.PATH_AUTO, "staged": psw.PATH_STAGED, "fused": psw.PATH_FUSED,
-            "chunked": psw.PATH_CHUNKED, "resweep": psw.PATH_RESWEEP,
+            "resweep": psw.PATH_RESWEEP,
             "cluster": psw.PATH_CLUSTER}[args.path]
     sharded = args.mode == "rows" and world > 1
     if sharded and layout != psw.LAYOUT_R:

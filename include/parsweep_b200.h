@@ -63,8 +63,6 @@ typedef enum psw_layout { PSW_LAYOUT_R = 0, PSW_LAYOUT_S = 1 } psw_layout;
  * supports the plan/shape: CLUSTER and FUSED keep every RHS tile resident on
  * chip and read F once (layout R, uniform partitions whose blocks fit a
  * cluster; CLUSTER: one CTA per SM holding G blocks, FUSED: 16-CTA clusters);
- * CHUNKED runs the RESWEEP kernels over RHS chunks sized for L2, so the
- * second read of F hits L2 (layout R, narrow systems: the fp32 config);
  * RESWEEP reads F twice from HBM and writes X once, with a few aggregates per
  * 256 rows in between (either layout, e.g. the 2^20-row config); STAGED is
  * the general three-kernel path (and the only one returning betas/boundary
@@ -73,7 +71,7 @@ typedef enum psw_path {
     PSW_PATH_AUTO = 0,
     PSW_PATH_STAGED = 1,
     PSW_PATH_FUSED = 2,
-    /* 3, 4: retired paths (PSW_NOT_SUPPORTED) */
+    /* 3, 4, 5: retired paths (PSW_NOT_SUPPORTED) */
     PSW_PATH_CHUNKED = 5,
     PSW_PATH_RESWEEP = 6,
     PSW_PATH_CLUSTER = 7

@@ -200,10 +200,6 @@ int build_cluster_tables(psw_plan* pl, const std::vector<FusedFwd<double>>& ff,
 bool resweep_supported(const psw_plan* plan, int layout, int64_t N);
 int solve_resweep(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
                   int64_t N, int layout, cudaStream_t s, void** events, int nevents);
-// the same kernels over RHS chunks sized for L2, chunks on forked streams
-bool chunked_supported(const psw_plan* plan, int layout, int64_t N);
-int solve_chunked(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx,
-                  int64_t N, int layout, cudaStream_t s, void** events, int nevents);
 // RESWEEP tables (groups, runs, solve coefficients) over the plan's own blocks
 int build_rs_tables(psw_plan* pl, const std::vector<SegDesc>& desc,
                     const std::vector<SegCoef>& seg, const std::vector<FusedFwd<double>>& ff,

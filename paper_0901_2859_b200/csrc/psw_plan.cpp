@@ -901,9 +901,7 @@ int psw_solve_ex(const psw_plan* plan, const void* F, int64_t ldf, void* X, int6
     if (path != PSW_PATH_STAGED && path != PSW_PATH_AUTO && want_intermediates) {
         rc = unsupported("only the staged");
     } else if (path == PSW_PATH_CHUNKED) {
-        rc = psw::chunked_supported(plan, layout, nrhs)
-                 ? psw::solve_chunked(plan, F, ldf, X, ldx, nrhs, layout, s, ev, nev)
-                 : unsupported("chunked");
+        rc = unsupported("chunked (retired)");
     } else if (path == PSW_PATH_CLUSTER) {
         rc = psw::cluster_supported(plan, layout, nrhs, F, ldf)
                  ? psw::solve_cluster(plan, F, ldf, X, ldx, nrhs, layout, s, ev, nev)

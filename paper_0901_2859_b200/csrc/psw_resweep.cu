@@ -3,9 +3,6 @@
 // partition, both layouts. The same kernels serve three drivers:
 //   solve_resweep   all RHS at once (the 2^20-row config C3: one 16-RHS
 //                   column of F is 128 MB, no single-read scheme fits on chip)
-//   solve_chunked   RHS chunks sized for L2 on forked streams: K3's second
-//                   read of a chunk hits L2, so HBM sees F once (fp32 C2:
-//                   a 32-RHS column of F is 8 MB)
 //   shard_forward / shard_backward   a rank's own blocks of a row-sharded
 //                   solve (psw_shard.cpp), around one all-reduce
 //
@@ -704,37 +701,9 @@ int solve_all_dt(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_
                : solve_all<float>(pl, F, ldf, X, ldx, N, layout, w, stream_loads, s, ev, nev, launches);
 }
 
-// ---- chunked driver: internal streams, one set per device ----------------
-constexpr int kMaxChunkStreams = 4;
-struct ChunkStreams {
-    std::mutex mu;
-    bool ready = false;
-    cudaStream_t st[kMaxChunkStreams] = {};
-};
-ChunkStreams& chunk_streams(int dev) {
-    static std::mutex mu;
-    static std::vector<ChunkStreams*> v;
-    std::lock_guard<std::mutex> lk(mu);
-    if (size_t(dev) >= v.size()) v.resize(size_t(dev) + 1, nullptr);
-    if (!v[size_t(dev)]) v[size_t(dev)] = new ChunkStreams();  // lives for the process
-    return *v[size_t(dev)];
-}
-
 int env_int(const char* name, int dflt) {
     const char* e = std::getenv(name);
     return e ? std::atoi(e) : dflt;
-}
-
-// RHS per chunk: the chunk's F fits a quarter of L2 (the chunk in K1, its
-// re-read in K3 and the neighbouring streams' chunks share it)
-int64_t chunk_rhs(const psw_plan* pl, int64_t N) {
-    const int es = pl->dtype == PSW_F64 ? 8 : 4;
-    int l2 = 0;
-    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, pl->device);
-    const int64_t mb = env_int("PSW_CHUNK_MB", 0);
-    const int64_t budget = mb > 0 ? mb << 20 : int64_t(l2 > 0 ? l2 : (96 << 20)) / 4;
-    int64_t c = budget / (int64_t(pl->n) * es) / 32 * 32;
-    return std::min<int64_t>(std::max<int64_t>(c, 32), N);
 }
 
 }  // namespace
@@ -870,59 +839,6 @@ int solve_resweep(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64
     scratch_free(mem, s);
     if (rc != PSW_OK) return rc;
     if (e != cudaSuccess) return cuda_fail(e, "resweep kernels");
-    note_launches(launches);
-    return PSW_OK;
-}
-
-bool chunked_supported(const psw_plan* pl, int layout, int64_t N) {
-    return layout == PSW_LAYOUT_R && resweep_supported(pl, layout, N);
-}
-
-int solve_chunked(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_t ldx, int64_t N,
-                  int layout, cudaStream_t s, void** ev, int nev) {
-    const int es = pl->dtype == PSW_F64 ? 8 : 4;
-    const int64_t c = chunk_rhs(pl, N);
-    const int64_t nchunks = (N + c - 1) / c;
-    const int nst = int(std::min<int64_t>(std::max(1, std::min(env_int("PSW_CHUNK_STREAMS", 3),
-                                                               kMaxChunkStreams)),
-                                          nchunks));
-    const size_t wb = (work_bytes(pl, c, true) + 255) & ~size_t(255);
-    void* mem = nullptr;
-    PSW_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&mem), wb * size_t(nst), pl->device, s));
-    ChunkStreams& cs = chunk_streams(pl->device);
-    std::lock_guard<std::mutex> lk(cs.mu);
-    if (!cs.ready) {
-        for (int i = 0; i < kMaxChunkStreams; ++i)
-            PSW_CUDA_TRY(cudaStreamCreateWithFlags(&cs.st[i], cudaStreamNonBlocking));
-        cs.ready = true;
-    }
-    cudaEvent_t fork = nullptr, join[kMaxChunkStreams] = {};
-    PSW_CUDA_TRY(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-    for (int i = 0; i < nst; ++i) PSW_CUDA_TRY(cudaEventCreateWithFlags(&join[i], cudaEventDisableTiming));
-    mark(ev, nev, 0, s);
-    PSW_CUDA_TRY(cudaEventRecord(fork, s));
-    for (int i = 0; i < nst; ++i) PSW_CUDA_TRY(cudaStreamWaitEvent(cs.st[i], fork, 0));
-    int64_t launches = 0;
-    int rc = PSW_OK;
-    for (int64_t ci = 0; ci < nchunks && rc == PSW_OK; ++ci) {
-        const int si = int(ci % nst);
-        const int64_t k0 = ci * c, kc = std::min(c, N - k0);
-        const Work w = carve(pl, kc, static_cast<char*>(mem) + wb * size_t(si), true);
-        rc = solve_all_dt(pl, static_cast<const char*>(F) + k0 * es, ldf,
-                          static_cast<char*>(X) + k0 * es, ldx, kc, layout, w, false, cs.st[si],
-                          nullptr, 0, launches);
-    }
-    for (int i = 0; i < nst; ++i) {
-        cudaEventRecord(join[i], cs.st[i]);
-        cudaStreamWaitEvent(s, join[i], 0);
-    }
-    mark(ev, nev, 1, s);
-    cudaError_t e = cudaGetLastError();
-    scratch_free(mem, s);
-    cudaEventDestroy(fork);
-    for (int i = 0; i < nst; ++i) cudaEventDestroy(join[i]);
-    if (rc != PSW_OK) return rc;
-    if (e != cudaSuccess) return cuda_fail(e, "chunked kernels");
     note_launches(launches);
     return PSW_OK;
 }

@@ -179,7 +179,7 @@ def test_device_generator_matches_host(psw, cuda):
 
 
 # ------------------------------------------------------------------ full configs
-def _config_run(psw, torch, cfg, seed=0, check_rhs=None, P=None, layout=None):
+def _config_run(psw, torch, cfg, seed=0, check_rhs=None, P=None, layout=None, path=0):
     """Device-generated config input, GPU solve, oracle check on a subset."""
     from oracle.pyoracle import Oracle
     from paper_0901_2859_b200 import configs
@@ -203,7 +203,7 @@ def _config_run(psw, torch, cfg, seed=0, check_rhs=None, P=None, layout=None):
     idx = torch.from_numpy(ks).cuda()
     Fs = (F[:, idx].T if lay == psw.LAYOUT_R else F[idx]).double().cpu().numpy()
     X = torch.empty_like(F)
-    plan.solve(F, X, layout=lay)
+    plan.solve(F, X, layout=lay, path=path)
     torch.cuda.synchronize()
     Xs = (X[:, idx].T if lay == psw.LAYOUT_R else X[idx]).double().cpu().numpy()
     want = Oracle().solve_batch_threads(a, b, a, np.array(part.boundaries), Fs, 8)[0]

@@ -120,7 +120,7 @@ def test_randomized_against_oracle(psw, cuda, seed):
         F = F.astype(np.float32).astype(np.float64)
     want = Oracle().solve_batch(sub, diag, sub, np.array(bnd, np.int64), F)
     from test_parity_gpu import gpu_solve
-    paths = [psw.PATH_AUTO, psw.PATH_STAGED, psw.PATH_RESWEEP, psw.PATH_CHUNKED]
+    paths = [psw.PATH_AUTO, psw.PATH_STAGED, psw.PATH_RESWEEP, psw.PATH_CLUSTER, psw.PATH_FUSED]
     for path in paths:
         try:
             X = gpu_solve(psw, cuda, plan, F, layout, path=path)

@@ -64,38 +64,14 @@ def test_resweep_config_C1(psw, cuda):
     assert rel_l2(Xs, want) <= FP64_TOL
 
 
-@pytest.mark.parametrize("chunk_mb", ["1", "3"])
-@pytest.mark.parametrize("name", ["c1_n4096_P16", "c4_n4096_P16", "c0_n1024_P4", "decomp_n333_P9",
-                                  "rand_n200_p7"])
-def test_chunked_golden(psw, cuda, name, chunk_mb, monkeypatch):
-    """CHUNKED: the RESWEEP kernels over RHS chunks on forked streams (small
-    chunks forced through PSW_CHUNK_MB so every case has several)."""
-    monkeypatch.setenv("PSW_CHUNK_MB", chunk_mb)
-    g = load_golden(name)
-    plan = plan_for(psw, g)
-    F = np.concatenate([g["F"]] * 8, axis=0)  # >= 8 chunks' worth of RHS
-    want = np.concatenate([g["X"]] * 8, axis=0)
-    X = gpu_solve(psw, cuda, plan, F, 0, path=psw.PATH_CHUNKED)
-    X2 = gpu_solve(psw, cuda, plan, F, 0, path=psw.PATH_CHUNKED, inplace=False, pad=5)
-    assert rel_l2(X, want) <= FP64_TOL
-    assert np.array_equal(X, X2)
-
-
-@pytest.mark.parametrize("name", ["c2_n8192_P8", "c2_n8192_P64", "c2_n8192_P512"])
-def test_chunked_fp32(psw, cuda, name, monkeypatch):
-    monkeypatch.setenv("PSW_CHUNK_MB", "1")
-    g = load_golden(name)
-    plan = plan_for(psw, g, dtype=psw.F32)
-    F = np.concatenate([g["F"]] * 4, axis=0)
-    X = gpu_solve(psw, cuda, plan, F, 0, path=psw.PATH_CHUNKED)
-    assert rel_l2(X, np.concatenate([g["X"]] * 4, axis=0)) <= FP32_TOL
-
-
-def test_chunked_rejects_layout_s(psw, cuda):
+def test_retired_paths(psw, cuda):
+    """PIPE (3), TILE (4) and CHUNKED (5) were explicit-only paths that lost to
+    CLUSTER / RESWEEP; they are retired and answer NotSupported."""
     g = load_golden("c1_n4096_P16")
     plan = plan_for(psw, g)
-    with pytest.raises(psw.NotSupported):
-        gpu_solve(psw, cuda, plan, g["F"], 1, path=psw.PATH_CHUNKED)
+    for path in (3, 4, psw.PATH_CHUNKED):
+        with pytest.raises(psw.NotSupported):
+            gpu_solve(psw, cuda, plan, g["F"], 0, path=path)
 
 
 def test_resweep_c3_full(psw, cuda):
