@@ -105,6 +105,9 @@ CONFIGS = {
     "C2": Config("C2", "f32", 65536, 65536, 64, "R", "uniform", "dominant05"),
     "C3": Config("C3", "f64", 1 << 20, 1024, 64, "R", "uniform", "dominant01"),
     "C4": Config("C4", "f64", 4096, 4096, 16, "S", "grid", "adi"),
+    # C4's second direction: the same grid field and matrix solved along the
+    # columns (unknowns strided by the row pitch = layout R)
+    "C4c": Config("C4c", "f64", 4096, 4096, 16, "R", "grid", "adi"),
 }
 
 

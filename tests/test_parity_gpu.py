@@ -218,6 +218,13 @@ def test_config_C0_full(psw, cuda):
     assert err <= FP64_TOL, err
 
 
+def test_config_C4c_full(psw, cuda):
+    """C4's column direction on its own (layout R over the grid field)."""
+    from paper_0901_2859_b200.configs import CONFIGS
+    err, _, _ = _config_run(psw, cuda, CONFIGS["C4c"])
+    assert err <= FP64_TOL, err
+
+
 def test_config_C1_full(psw, cuda):
     from paper_0901_2859_b200.configs import CONFIGS
     err, _, _ = _config_run(psw, cuda, CONFIGS["C1"])
