@@ -266,6 +266,15 @@ int psw_fill_normal(void* dst, int dtype, int64_t count, uint64_t seed, uint64_t
  * %globaltimer at start/end (14, 15). NULL disables tracing (default). */
 int psw_debug_trace(void* device_buffer);
 
+/* DST-I of `rows` rows (Fourier consumer; replaces poisson/dst.hpp:85-164
+ * DstPlan::apply_raw / apply_raw_pair): out[r][l-1] = scale * sum_{j=1}^{N-1}
+ * in[r][j-1] sin(pi j l / N), l = 1..N-1, fp64 device rows of pitch ldin /
+ * ldout. Power-of-two N <= 4096: the reference's paired radix-2 FFT of the
+ * odd extension (one CTA per pair of rows, shared memory); other N: the
+ * direct sine sum (dst.hpp:120-128). Asynchronous on `stream`. */
+int psw_dst_rows(const double* in, int64_t ldin, double* out, int64_t ldout, int64_t rows,
+                 int64_t N, double scale, void* stream);
+
 /* Write `bytes` of zeros+index pattern over a scratch buffer (L2 flush). */
 int psw_l2_flush(void* scratch, int64_t bytes, void* stream);
 

@@ -127,6 +127,7 @@ def lib() -> C.CDLL:
         L.psw_solve_ex.argtypes = [vp, vp, C.c_int64, vp, C.c_int64, C.c_int64, C.c_int, vp, vp]
         L.psw_solve_host.argtypes = [vp, vp, C.c_int64, vp, C.c_int64, C.c_int64, C.c_int]
         L.psw_solve_multi.argtypes = [C.POINTER(vp), C.c_int64, vp, C.c_int64, vp, C.c_int64, vp]
+        L.psw_dst_rows.argtypes = [vp, C.c_int64, vp, C.c_int64, C.c_int64, C.c_int64, C.c_double, vp]
         L.psw_shard_partials_count.argtypes = [vp]
         L.psw_shard_partials_count.restype = C.c_int64
         L.psw_shard_row_offset.argtypes = [vp]

@@ -1,0 +1,178 @@
+// DST-I of many rows on the device: the Fourier consumer's transform
+// (reference poisson/dst.hpp:85-164).
+//
+// out[l-1] = scale * sum_{j=1}^{N-1} in[j-1] sin(pi j l / N), l = 1..N-1,
+// for `rows` rows of N-1 values (row pitch ldin / ldout, fp64).
+//
+// Power-of-two N (dst.hpp:96-118, 130-149): the reference's construction —
+// two rows packed into the real and imaginary parts of the odd extension
+// (length L = 2N), one radix-2 decimation-in-time FFT with the reference's
+// bit reversal and twiddle table w_k = (cos, sin)(-2 pi k / L) (computed on
+// the host with std::cos / std::sin exactly as Radix2Fft does), the two
+// spectra split by conjugate symmetry. One CTA per pair of rows; the whole
+// signal and the twiddles live in shared memory (L <= 8192: N <= 4096).
+// Other N (dst.hpp:120-128): the direct sine sum over the reference's
+// sines[m] table, one thread per output.
+#include <cmath>
+#include <mutex>
+
+
+#include <vector>
+
+#include "psw_internal.h"
+
+namespace psw {
+namespace {
+
+constexpr double kPi = 3.141592653589793238462643383279502884;  // std::numbers::pi
+constexpr int kDstThreads = 512;
+constexpr int kDstMaxL = 8192;
+
+__global__ void __launch_bounds__(kDstThreads) dst_pair_kernel(
+    const double* __restrict__ in, int64_t ldin, double* __restrict__ out, int64_t ldout,
+    int64_t rows, int N, int logL, const double2* __restrict__ gtw, double scale) {
+    extern __shared__ double2 sm[];
+    const int L = 2 * N;
+    double2* v = sm;        // [L]
+    double2* tw = sm + L;   // [L / 2]
+    const int64_t ra = 2 * int64_t(blockIdx.x), rb = ra + 1;
+    const bool hasb = rb < rows;
+    const double* a = in + ra * ldin;
+    const double* b = in + (hasb ? rb : ra) * ldin;
+    for (int k = threadIdx.x; k < L / 2; k += blockDim.x) tw[k] = gtw[k];
+    // the odd extension, stored bit-reversed (Radix2Fft::transform's swap pass)
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+        double re = 0.0, im = 0.0;
+        if (i > 0 && i < N) {
+            re = a[i - 1];
+            im = hasb ? b[i - 1] : 0.0;
+        } else if (i > N) {
+            re = -a[L - i - 1];
+            im = hasb ? -b[L - i - 1] : 0.0;
+        }
+        v[__brev(unsigned(i)) >> (32 - logL)] = make_double2(re, im);
+    }
+    __syncthreads();
+    for (int len = 2; len <= L; len <<= 1) {
+        const int half = len >> 1, step = L / len;
+        for (int bf = threadIdx.x; bf < L / 2; bf += blockDim.x) {
+            const int k = bf & (half - 1), i0 = (bf - k) * 2 + k;  // start + k, start = (bf / half) * len
+            const double2 w = tw[k * step];
+            const double2 x = v[i0], y = v[i0 + half];
+            const double tr = w.x * y.x - w.y * y.y, ti = w.x * y.y + w.y * y.x;  // w * b
+            v[i0 + half] = make_double2(x.x - tr, x.y - ti);
+            v[i0] = make_double2(x.x + tr, x.y + ti);
+        }
+        __syncthreads();
+    }
+    // split the packed spectra (dst.hpp:144-148)
+    double* oa = out + ra * ldout;
+    double* ob = out + rb * ldout;
+    for (int l = 1 + threadIdx.x; l < N; l += blockDim.x) {
+        const double2 x = v[l];
+        const double2 y = make_double2(v[L - l].x, -v[L - l].y);  // conj(v[2N - l])
+        oa[l - 1] = scale * (-0.25 * (x.y + y.y));
+        if (hasb) ob[l - 1] = scale * (0.25 * (x.x - y.x));
+    }
+}
+
+// dst.hpp:120-128: direct summation over sines[m] = sin(pi m / N)
+__global__ void dst_direct_kernel(const double* __restrict__ in, int64_t ldin,
+                                  double* __restrict__ out, int64_t ldout, int64_t rows, int N,
+                                  const double* __restrict__ sines, double scale) {
+    const int l = 1 + int(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (l >= N) return;
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+        const double* x = in + r * ldin;
+        double s = 0.0;
+        for (int j = 1; j < N; ++j) {
+            const int m = int((int64_t(j) * l) % (2 * N));  // sin has period 2N with sign flip
+            s += x[j - 1] * (m < N ? sines[m] : -sines[m - N]);
+        }
+        out[r * ldout + l - 1] = scale * s;
+    }
+}
+
+struct DstTables {
+    std::mutex mu;
+    std::vector<std::pair<std::pair<int, int>, void*>> tab;  // ((device, N), table)
+};
+DstTables& dst_tables() {
+    static DstTables* t = new DstTables();  // lives for the process
+    return *t;
+}
+
+bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+
+// twiddles (power-of-two N, Radix2Fft(2N)) or sines (other N), cached per device
+int dst_table(int device, int N, const void** out) {
+    DstTables& T = dst_tables();
+    std::lock_guard<std::mutex> lk(T.mu);
+    for (auto& e : T.tab)
+        if (e.first == std::make_pair(device, N)) {
+            *out = e.second;
+            return PSW_OK;
+        }
+    std::vector<double> h;
+    if (is_pow2(N)) {
+        const size_t L = 2 * size_t(N);
+        h.resize(L);  // L/2 complex
+        for (size_t k = 0; k < L / 2; ++k) {
+            const double angle = -2.0 * kPi * static_cast<double>(k) / double(L);
+            h[2 * k] = std::cos(angle);
+            h[2 * k + 1] = std::sin(angle);
+        }
+    } else {
+        h.resize(size_t(N));
+        for (int j = 0; j < N; ++j) h[size_t(j)] = std::sin(kPi * static_cast<double>(j) / N);
+    }
+    void* d = nullptr;
+    PSW_CUDA_TRY(cudaMalloc(&d, sizeof(double) * h.size()));
+    PSW_CUDA_TRY(cudaMemcpy(d, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+    T.tab.push_back({{device, N}, d});
+    *out = d;
+    return PSW_OK;
+}
+
+}  // namespace
+}  // namespace psw
+
+extern "C" int psw_dst_rows(const double* in, int64_t ldin, double* out, int64_t ldout,
+                            int64_t rows, int64_t N, double scale, void* stream) {
+    psw::clear_error();
+    if (N < 2 || rows < 0 || (rows > 0 && (!in || !out)) || ldin < N - 1 || ldout < N - 1 ||
+        N > (int64_t(1) << 30)) {
+        psw::set_error(PSW_INVALID_ARGUMENT, "psw_dst_rows: invalid arguments");
+        return PSW_INVALID_ARGUMENT;
+    }
+    if (rows == 0) return PSW_OK;
+    int dev = 0;
+    PSW_CUDA_TRY(cudaGetDevice(&dev));
+    const int n = int(N);
+    const void* tab = nullptr;
+    if (int rc = psw::dst_table(dev, n, &tab)) return rc;
+    auto s = static_cast<cudaStream_t>(stream);
+    const bool fft = psw::is_pow2(n) && 2 * n <= psw::kDstMaxL;
+    if (fft) {
+        const int L = 2 * n;
+        int logL = 0;
+        while ((1 << logL) < L) ++logL;
+        const size_t smem = sizeof(double2) * (size_t(L) + size_t(L) / 2);
+        static std::once_flag once;
+        cudaError_t e = cudaSuccess;
+        std::call_once(once, [&] {
+            e = cudaFuncSetAttribute(psw::dst_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(sizeof(double2) * (psw::kDstMaxL + psw::kDstMaxL / 2)));
+        });
+        PSW_CUDA_TRY(e);
+        psw::dst_pair_kernel<<<unsigned((rows + 1) / 2), psw::kDstThreads, smem, s>>>(
+            in, ldin, out, ldout, rows, n, logL, static_cast<const double2*>(tab), scale);
+    } else {
+        const dim3 grid(unsigned((n - 1 + 127) / 128), unsigned(rows < 65535 ? rows : 65535));
+        psw::dst_direct_kernel<<<grid, 128, 0, s>>>(in, ldin, out, ldout, rows, n,
+                                                    static_cast<const double*>(tab), scale);
+    }
+    PSW_CUDA_TRY(cudaGetLastError());
+    psw::note_launches(1);
+    return PSW_OK;
+}

@@ -11,17 +11,17 @@ boundary), as in the ADI driver (adi.py).
 
 Per Poisson right-hand side:
   1. the DST-I of every interior row along direction 2 (dst.hpp:13-20:
-     out_l = sum_j in_j sin(pi j l / N)), scaled by 2/N2 (fourier.hpp:130) —
-     one batched fp64 FFT of the odd extension, the reference's own
-     construction for power-of-two N (dst.hpp:107-118) and used for every N
-     here;
+     out_l = sum_j in_j sin(pi j l / N)), scaled by 2/N2 (fourier.hpp:130)
+     and by -h1^2 (fourier.hpp:159) in the same pass — psw_dst_rows, a
+     hand-written kernel restating the reference's paired radix-2 FFT of the
+     odd extension (dst.hpp:85-149; direct sum for other N);
   2. rhs = -h1^2 coeff (fourier.hpp:159) and ONE multi-matrix solve of all
      harmonics (psw_solve_multi: column l of the coefficient grid with the
      plan of B_l; the reference's per-harmonic solve_harmonic loop,
      fourier.hpp:157-164);
   3. the inverse DST-I of every row (fourier.hpp:167-186).
-The transforms round differently from the reference's radix-2 FFT (a few ulp
-of the field); the solves are the dichotomy path of the reference.
+The transforms follow the reference's FFT operation order (FMA contraction
+aside); the solves are the dichotomy path of the reference.
 """
 from __future__ import annotations
 
@@ -47,16 +47,24 @@ def harmonic_system(n1: int, n2: int, h1: float, h2: float, l: int) -> HarmonicS
     return HarmonicSystem(l, d_l, TridiagMatrix.constant(n1 - 1, 1.0, -(2.0 + d_l), 1.0))
 
 
-def dst_raw(x: torch.Tensor) -> torch.Tensor:
-    """out[..., l-1] = sum_{j=1}^{N-1} x[..., j-1] sin(pi j l / N) for rows of
-    length N-1 (dst.hpp:93-118): FFT of the odd extension of length 2N."""
-    m = x.shape[-1]
-    n = m + 1
-    v = torch.zeros(*x.shape[:-1], 2 * n, dtype=torch.float64, device=x.device)
-    v[..., 1:n] = x
-    v[..., n + 1:] = -torch.flip(x, dims=[-1])
-    V = torch.fft.fft(v, dim=-1)
-    return -0.5 * V[..., 1:n].imag
+def dst_raw(x: torch.Tensor, out: torch.Tensor | None = None, scale: float = 1.0,
+            stream=None) -> torch.Tensor:
+    """out[..., l-1] = scale * sum_{j=1}^{N-1} x[..., j-1] sin(pi j l / N) for
+    the rows of a CUDA fp64 matrix x of N-1 columns (psw_dst_rows: the
+    reference's paired radix-2 FFT of the odd extension for power-of-two N,
+    dst.hpp:93-149; the direct sum otherwise, :120-128)."""
+    from . import _check, _ptr, _stream_ptr, lib
+    if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float64 and x.dim() == 2
+            and x.stride(1) == 1):
+        raise ValueError("dst_raw: a CUDA fp64 matrix with contiguous rows")
+    if out is None:
+        out = torch.empty_like(x)
+    if out.shape != x.shape or out.stride(1) != 1 or not out.is_cuda or out.dtype != torch.float64:
+        raise ValueError("dst_raw: out must match x")
+    rows, m = x.shape
+    _check(lib().psw_dst_rows(_ptr(x), x.stride(0), _ptr(out), out.stride(0), rows, m + 1,
+                              float(scale), _stream_ptr(stream)))
+    return out
 
 
 class FourierWorkspace:
@@ -99,9 +107,9 @@ def fourier_solve(f: torch.Tensor, ws: FourierWorkspace | None = None, h1: float
     if (ws.n1, ws.n2) != (n1, n2):
         raise ValueError("fourier_solve: workspace mesh does not match the field")
     interior = f[1:n1, 1:n2].to(torch.float64)
-    coeff = (2.0 / float(n2)) * dst_raw(interior)          # fourier.hpp:129-149
-    rhs = (-ws.h1 * ws.h1) * coeff                          # fourier.hpp:159
-    sol = ws.solve_harmonics(rhs.contiguous())              # fourier.hpp:157-164
+    # fourier.hpp:129-149 and :159 in one pass: rhs = -h1^2 (2 / N2) S f
+    rhs = dst_raw(interior, scale=(-ws.h1 * ws.h1) * (2.0 / float(n2)))
+    sol = ws.solve_harmonics(rhs)                           # fourier.hpp:157-164
     u = torch.zeros_like(f, dtype=torch.float64)
-    u[1:n1, 1:n2] = dst_raw(sol)                            # fourier.hpp:167-186
+    dst_raw(sol, out=u[1:n1, 1:n2])                         # fourier.hpp:167-186
     return u

@@ -11,19 +11,29 @@ import pytest
 from conftest import load_golden
 
 
-def test_dst_raw_matches_the_sine_sum():
-    import torch
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [8, 13, 32, 1024, 4096, 6000])
+def test_dst_raw_matches_the_sine_sum(psw, cuda, n):
+    """psw_dst_rows against the dense sine sum (power-of-two N through the
+    paired FFT, others through the direct sum; odd and even row counts)."""
     from paper_0901_2859_b200.fourier import dst_raw
-    for n in (8, 13, 32):  # power of two and not (dst.hpp:96-118 / :120-128)
-        x = np.random.default_rng(n).standard_normal((3, n - 1))
+    for rows in (1, 3, 8):
+        x = np.random.default_rng(n + rows).standard_normal((rows, n - 1))
         j = np.arange(1, n)
         S = np.sin(np.pi * np.outer(j, j) / n)
         want = x @ S.T
-        got = dst_raw(torch.from_numpy(x)).numpy()
-        assert np.max(np.abs(got - want)) <= 1e-13 * np.max(np.abs(want))
+        got = dst_raw(cuda.from_numpy(x).cuda()).cpu().numpy()
+        assert np.max(np.abs(got - want)) <= 1e-12 * np.max(np.abs(want))
         # (2/N) S is the inverse of S (dst.hpp:13-17)
-        back = dst_raw(torch.from_numpy(got * 2.0 / n)).numpy()
-        assert np.max(np.abs(back - x)) <= 1e-13 * np.max(np.abs(x))
+        back = dst_raw(cuda.from_numpy(got).cuda(), scale=2.0 / n).cpu().numpy()
+        assert np.max(np.abs(back - x)) <= 1e-12 * np.max(np.abs(x))
+
+
+def test_dst_raw_needs_a_cuda_matrix(psw):
+    import torch
+    from paper_0901_2859_b200.fourier import dst_raw
+    with pytest.raises(ValueError):  # no CPU fallback
+        dst_raw(torch.zeros(2, 7, dtype=torch.float64))
 
 
 def test_harmonic_system_is_the_reference_matrix():
