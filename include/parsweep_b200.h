@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define PSW_ABI_VERSION 3
+#define PSW_ABI_VERSION 4
 
 /* Status codes. The C++ wrapper (parsweep_b200.hpp) maps them back onto the
  * reference exception types of core/errors.hpp:9-62. */
@@ -192,12 +192,14 @@ int64_t psw_last_launch_count(void);
  *          -> the direction-2 systems (along j) in layout S.
  * Same operation order as the reference. The driver (AdiWorkspace /
  * AdiIteration / adi_solve) is paper_0901_2859_b200/adi.py. */
-int psw_adi_rhs(int dir, const double* u, const double* f, double* rhs, int64_t ldr, int64_t n1,
-                int64_t n2, double h1, double h2, double tau, void* stream);
-/* out2[0] = max |a - b|, out2[1] = max |b| over `count` doubles (device
- * pointers; max_abs_diff / max_abs of poisson/grid2d.hpp:43-53). */
-int psw_grid_max_abs_diff(const double* a, const double* b, int64_t count, double* out2,
-                          void* stream);
+int psw_adi_rhs(int dir, const double* u, int64_t ldu, const double* f, int64_t ldf, double* rhs,
+                int64_t ldr, int64_t n1, int64_t n2, double h1, double h2, double tau,
+                void* stream);
+/* out2[0] = max |a - b|, out2[1] = max |b| over rows x cols doubles with row
+ * pitches lda / ldb (device pointers; max_abs_diff / max_abs of
+ * poisson/grid2d.hpp:43-53). */
+int psw_grid_max_abs_diff(const double* a, int64_t lda, const double* b, int64_t ldb,
+                          int64_t rows, int64_t cols, double* out2, void* stream);
 
 /* psw_path taken by the last psw_solve/psw_solve_ex on this thread (0 before any). */
 int psw_last_path(void);

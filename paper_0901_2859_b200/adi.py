@@ -103,22 +103,42 @@ class AdiWorkspace:
 
 def _adi_rhs(direction, u, f, rhs, ldr, n1, n2, h1, h2, tau, stream):
     L = lib()
-    L.psw_adi_rhs.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
-                              C.c_int64, C.c_double, C.c_double, C.c_double, C.c_void_p]
-    _check(L.psw_adi_rhs(direction, _ptr(u), _ptr(f), _ptr(rhs), ldr, n1, n2, h1, h2, tau,
-                         stream))
+    L.psw_adi_rhs.argtypes = [C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
+                              C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_double,
+                              C.c_void_p]
+    _check(L.psw_adi_rhs(direction, _ptr(u), u.stride(0), _ptr(f), f.stride(0), _ptr(rhs), ldr,
+                         n1, n2, h1, h2, tau, stream))
 
 
 def max_abs_diff_and_max(a, b, out=None, stream=None):
     """(max |a - b|, max |b|) of two fields on the device (grid2d.hpp:43-53)."""
     import torch
     L = lib()
-    L.psw_grid_max_abs_diff.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+    L.psw_grid_max_abs_diff.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int64,
+                                        C.c_int64, C.c_void_p, C.c_void_p]
+    if a.shape != b.shape or a.dim() != 2 or a.stride(1) != 1 or b.stride(1) != 1:
+        raise ValueError("max_abs_diff_and_max: two fields of one shape with contiguous rows")
     if out is None:
         out = torch.empty(2, dtype=torch.float64, device=a.device)
-    _check(L.psw_grid_max_abs_diff(_ptr(a), _ptr(b), a.numel(), _ptr(out), _stream_ptr(stream)))
+    _check(L.psw_grid_max_abs_diff(_ptr(a), a.stride(0), _ptr(b), b.stride(0), a.shape[0],
+                                   a.shape[1], _ptr(out), _stream_ptr(stream)))
     v = out.tolist()
     return v[0], v[1]
+
+
+def _is_padded(t) -> bool:
+    return t.stride(0) % 4 == 0 and (t.data_ptr() + 8 * (t.stride(0) + 1)) % 32 == 0
+
+
+def padded_field(n1: int, n2: int, device) -> "torch.Tensor":
+    """A zero (n1+1) x (n2+1) Grid2D field whose rows have a pitch of a
+    multiple of 4 doubles and whose interior node (1, 1) sits on 32 bytes:
+    the layout-S solve of direction 2 then writes whole 32-byte sectors of
+    every line (the CLUSTER kernel's 256-bit store variant)."""
+    import torch
+    ld = (n2 + 1 + 3) // 4 * 4
+    store = torch.zeros((n1 + 1) * ld + 4, dtype=torch.float64, device=device)
+    return store.as_strided((n1 + 1, n2 + 1), (ld, 1), 3)
 
 
 class AdiIteration:
@@ -135,7 +155,7 @@ class AdiIteration:
         self.ldr = (n2 - 1 + 1) // 2 * 2
         self.rhs = torch.empty((n1 - 1, self.ldr), dtype=torch.float64, device=f.device)
         self.half = torch.zeros_like(f)   # half-step field (boundary stays zero)
-        self.next = torch.zeros_like(f)
+        self.next = padded_field(n1, n2, f.device)
 
     def step(self, u, k: int) -> None:
         """Advances u (in place) by iteration k (parameter k mod n0)."""
@@ -146,12 +166,14 @@ class AdiIteration:
         # direction 1: lines j, unknowns along i -> layout R into the half field
         _adi_rhs(1, u, f, self.rhs, self.ldr, n1, n2, h1, h2, tau, self.stream)
         st.plan1.solve(self.rhs, self.half[1:, 1:], nrhs=n2 - 1, layout=LAYOUT_R,
-                       ldf=self.ldr, ldx=n2 + 1, stream=self.stream)
+                       ldf=self.ldr, ldx=self.half.stride(0), stream=self.stream)
         # direction 2: lines i, unknowns along j -> layout S into the next field
         _adi_rhs(2, self.half, f, self.rhs, self.ldr, n1, n2, h1, h2, tau, self.stream)
         st.plan2.solve(self.rhs, self.next[1:, 1:], nrhs=n1 - 1, layout=LAYOUT_S,
-                       ldf=self.ldr, ldx=n2 + 1, stream=self.stream)
+                       ldf=self.ldr, ldx=self.next.stride(0), stream=self.stream)
         u.data, self.next.data = self.next.data, u.data  # std::swap(u.values, next_.values)
+        if not _is_padded(self.next):  # the caller's first field: keep the buffer padded
+            self.next = padded_field(n1, n2, f.device)
 
 
 def adi_solve(f, eps: float, u0, ws: AdiWorkspace, exact=None, stream=None):

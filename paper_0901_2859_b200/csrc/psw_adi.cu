@@ -22,13 +22,14 @@
 namespace psw {
 namespace {
 
-__global__ void adi_rhs_kernel(const double* __restrict__ u, const double* __restrict__ f,
+__global__ void adi_rhs_kernel(const double* __restrict__ u, int64_t ldu,
+                               const double* __restrict__ f, int64_t ldf,
                                double* __restrict__ rhs, int64_t ldr, int64_t n1, int64_t n2,
                                double h1, double h2, double tau, int dir) {
     const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x + 1;
     const int64_t i = int64_t(blockIdx.y) + 1;
     if (j >= n2 || i >= n1) return;
-    const int64_t ld = n2 + 1;
+    const int64_t ld = ldu;
     const int64_t c = i * ld + j;
     const double uc = u[c];
     double lam, hs;
@@ -41,18 +42,22 @@ __global__ void adi_rhs_kernel(const double* __restrict__ u, const double* __res
                         __dmul_rn(h1, h1));
         hs = __dmul_rn(-h2, h2);
     }
-    rhs[(i - 1) * ldr + (j - 1)] = __dmul_rn(hs, __dadd_rn(__dadd_rn(__ddiv_rn(uc, tau), lam), f[c]));
+    rhs[(i - 1) * ldr + (j - 1)] =
+        __dmul_rn(hs, __dadd_rn(__dadd_rn(__ddiv_rn(uc, tau), lam), f[i * ldf + j]));
 }
 
 // out[0] = max |a - b|, out[1] = max |b| (non-negative doubles order like
 // their bit patterns, so an integer atomicMax reduces them exactly)
-__global__ void max_abs_diff_kernel(const double* __restrict__ a, const double* __restrict__ b,
-                                    int64_t count, unsigned long long* out) {
+__global__ void max_abs_diff_kernel(const double* __restrict__ a, int64_t lda,
+                                    const double* __restrict__ b, int64_t ldb, int64_t rows,
+                                    int64_t cols, unsigned long long* out) {
     double md = 0.0, mb = 0.0;
+    const int64_t count = rows * cols;
     for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < count;
          k += int64_t(gridDim.x) * blockDim.x) {
-        const double bv = b[k];
-        md = fmax(md, fabs(a[k] - bv));
+        const int64_t r = k / cols, c = k - r * cols;
+        const double bv = b[r * ldb + c];
+        md = fmax(md, fabs(a[r * lda + c] - bv));
         mb = fmax(mb, fabs(bv));
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -67,23 +72,24 @@ __global__ void max_abs_diff_kernel(const double* __restrict__ a, const double* 
 
 }  // namespace
 
-int adi_rhs(int dir, const double* u, const double* f, double* rhs, int64_t ldr, int64_t n1,
-            int64_t n2, double h1, double h2, double tau, cudaStream_t s) {
+int adi_rhs(int dir, const double* u, int64_t ldu, const double* f, int64_t ldf, double* rhs,
+            int64_t ldr, int64_t n1, int64_t n2, double h1, double h2, double tau, cudaStream_t s) {
     if (n1 < 2 || n2 < 2) return PSW_OK;
     const dim3 grid(unsigned((n2 - 1 + 127) / 128), unsigned(n1 - 1));
-    adi_rhs_kernel<<<grid, 128, 0, s>>>(u, f, rhs, ldr, n1, n2, h1, h2, tau, dir);
+    adi_rhs_kernel<<<grid, 128, 0, s>>>(u, ldu, f, ldf, rhs, ldr, n1, n2, h1, h2, tau, dir);
     PSW_CUDA_TRY(cudaGetLastError());
     note_launches(1);
     return PSW_OK;
 }
 
-int grid_max_abs_diff(const double* a, const double* b, int64_t count, double* out2,
-                      cudaStream_t s) {
+int grid_max_abs_diff(const double* a, int64_t lda, const double* b, int64_t ldb, int64_t rows,
+                      int64_t cols, double* out2, cudaStream_t s) {
     PSW_CUDA_TRY(cudaMemsetAsync(out2, 0, 2 * sizeof(double), s));
+    const int64_t count = rows * cols;
     if (count <= 0) return PSW_OK;
     const int64_t blocks = std::min<int64_t>((count + 255) / 256, 148 * 8);
     max_abs_diff_kernel<<<unsigned(blocks), 256, 0, s>>>(
-        a, b, count, reinterpret_cast<unsigned long long*>(out2));
+        a, lda, b, ldb, rows, cols, reinterpret_cast<unsigned long long*>(out2));
     PSW_CUDA_TRY(cudaGetLastError());
     note_launches(1);
     return PSW_OK;
@@ -93,26 +99,30 @@ int grid_max_abs_diff(const double* a, const double* b, int64_t count, double* o
 
 extern "C" {
 
-int psw_adi_rhs(int dir, const double* u, const double* f, double* rhs, int64_t ldr, int64_t n1,
-                int64_t n2, double h1, double h2, double tau, void* stream) {
+int psw_adi_rhs(int dir, const double* u, int64_t ldu, const double* f, int64_t ldf, double* rhs,
+                int64_t ldr, int64_t n1, int64_t n2, double h1, double h2, double tau,
+                void* stream) {
     psw::clear_error();
     psw::reset_launches();
-    if ((dir != 1 && dir != 2) || !u || !f || !rhs || ldr < n2 - 1 || !(tau > 0.0)) {
+    if ((dir != 1 && dir != 2) || !u || !f || !rhs || ldr < n2 - 1 || ldu < n2 + 1 ||
+        ldf < n2 + 1 || !(tau > 0.0)) {
         psw::set_error(PSW_INVALID_ARGUMENT, "psw_adi_rhs: invalid arguments");
         return PSW_INVALID_ARGUMENT;
     }
-    return psw::adi_rhs(dir, u, f, rhs, ldr, n1, n2, h1, h2, tau, static_cast<cudaStream_t>(stream));
+    return psw::adi_rhs(dir, u, ldu, f, ldf, rhs, ldr, n1, n2, h1, h2, tau,
+                        static_cast<cudaStream_t>(stream));
 }
 
-int psw_grid_max_abs_diff(const double* a, const double* b, int64_t count, double* out2,
-                          void* stream) {
+int psw_grid_max_abs_diff(const double* a, int64_t lda, const double* b, int64_t ldb,
+                          int64_t rows, int64_t cols, double* out2, void* stream) {
     psw::clear_error();
     psw::reset_launches();
-    if (!a || !b || !out2 || count < 0) {
+    if (!a || !b || !out2 || rows < 0 || cols < 0 || lda < cols || ldb < cols) {
         psw::set_error(PSW_INVALID_ARGUMENT, "psw_grid_max_abs_diff: invalid arguments");
         return PSW_INVALID_ARGUMENT;
     }
-    return psw::grid_max_abs_diff(a, b, count, out2, static_cast<cudaStream_t>(stream));
+    return psw::grid_max_abs_diff(a, lda, b, ldb, rows, cols, out2,
+                                  static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -39,7 +39,7 @@ def test_library_is_sm100a_cuda(psw):
 
 
 def test_abi_version(psw):
-    assert psw.lib().psw_abi_version() == 3
+    assert psw.lib().psw_abi_version() == 4
 
 
 def test_decompose_matches_reference(psw, orc):
