@@ -197,8 +197,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rs_part_tma(
     extern __shared__ __align__(1024) unsigned char dyn[];
     unsigned char* stage0 = dyn;
     unsigned char* cbuf0 = dyn + size_t(sch.stages) * stage_bytes;
-    double* xch = reinterpret_cast<double*>(cbuf0 + 2 * size_t(cbuf_bytes));  // [4][kRsSeg][W]
-    uint64_t* full = reinterpret_cast<uint64_t*>(xch + 4 * kRsSeg * W);
+    uint64_t* full = reinterpret_cast<uint64_t*>(cbuf0 + 2 * size_t(cbuf_bytes));
     uint64_t* empty = full + sch.stages;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     pdl_trigger();  // the fold kernel may be scheduled as K1's CTAs retire
@@ -217,10 +216,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rs_part_tma(
                                                cbuf_bytes, full, empty);
         return;
     }
-    double(*s_d)[W] = reinterpret_cast<double(*)[W]>(xch);
-    double(*s_l)[W] = s_d + kRsSeg;
-    double(*s_r)[W] = s_d + 2 * kRsSeg;
-    double(*s_b)[W] = s_d + 3 * kRsSeg;
     TileIt it;
     int i = 0;
     for (bool ok = it.start(sch); ok; ok = it.next(sch), ++i) {
@@ -271,12 +266,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rs_part_tma(
             else
                 sweep(std::false_type{});
         }
+        // the segment's own (dead) first rows carry its exchange values:
+        // doubles [0, W) d~ end, [W, 2W) Lam~, [2W, 3W) right, [3W, 4W) left
+        if (sv) {
+            __syncwarp();
+            double* xw = reinterpret_cast<double*>(const_cast<T*>(tile) + (mt->desc[warp].a - G.ra) * W);
 #pragma unroll
-        for (int v = 0; v < VPL; ++v) {
-            s_d[warp][lane + 32 * v] = double(d[v]);
-            s_l[warp][lane + 32 * v] = double(lx[v]);
-            s_r[warp][lane + 32 * v] = double(br[v]);
-            s_b[warp][lane + 32 * v] = double(bl[v]);
+            for (int v = 0; v < VPL; ++v) {
+                xw[0 * W + lane + 32 * v] = double(d[v]);
+                xw[1 * W + lane + 32 * v] = double(lx[v]);
+                xw[2 * W + lane + 32 * v] = double(br[v]);
+                xw[3 * W + lane + 32 * v] = double(bl[v]);
+            }
         }
         consumers_sync();
         if (warp < G.r1 - G.r0) {  // one warp per run folds its segments (as rs_part_kernel)
@@ -289,11 +290,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rs_part_tma(
                 for (int s = rr.s0; s < rr.s1; ++s) {
                     const int j = s - G.s0;
                     const SegCoef q = mt->seg[j];
-                    lam = fma(nupre, fma(D, q.k1, s_l[j][lane + 32 * v]), lam);
-                    D = fma(q.mu_end, D, s_d[j][lane + 32 * v]);
+                    const double* xk = reinterpret_cast<const double*>(tile + (mt->desc[j].a - G.ra) * W);
+                    const int l = lane + 32 * v;
+                    lam = fma(nupre, fma(D, q.k1, xk[W + l]), lam);
+                    D = fma(q.mu_end, D, xk[l]);
                     nupre *= q.nu;
-                    R += s_r[j][lane + 32 * v];
-                    L += s_b[j][lane + 32 * v];
+                    R += xk[2 * W + l];
+                    L += xk[3 * W + l];
                 }
                 if (k < N) {
                     const int64_t o = int64_t(run) * sc.ld + k;
@@ -304,7 +307,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rs_part_tma(
                 }
             }
         }
-        consumers_sync();  // exchange arrays and this unit's meta are free again
+        // no second barrier: the exchange lives in this tile's stage, which
+        // goes back only when every warp (the folding ones last) has arrived
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
     }
@@ -802,7 +806,7 @@ bool tma_plan(const psw_plan* pl, int64_t N, TmaSched& sch, size_t& stage_bytes,
     sch.nchunks = int((N + W - 1) / W);
     stage_bytes = size_t(kTmaRows) * kTmaRowBytes + (AUX ? size_t(3) * sch.mr * W * 8 : 0);
     cbuf_bytes = size_t(AUX ? kMetaK3 : kMetaK1) + size_t(kTmaRows) * sizeof(Coef);
-    const size_t xch = store ? 0 : size_t(AUX ? 2 : 4) * kRsSeg * W * 8;
+    const size_t xch = (store || !AUX) ? 0 : size_t(2) * kRsSeg * W * 8;
     sch.stages = std::min(tma_env("PSW_TMA_STAGES", 3), kTmaMaxStages);
     while (sch.stages > 2 && tma_smem(sch.stages, stage_bytes, cbuf_bytes, xch) > size_t(maxs))
         --sch.stages;
@@ -858,7 +862,8 @@ template <typename T>
 bool launch_part_tma(const psw_plan* pl, const T* F, int64_t ldf, int64_t N, const RsScratch& sc,
                      cudaStream_t s, int& rc) {
     rc = PSW_OK;
-    if (!tma_enabled()) return false;
+    // each segment lends its first W / 8 rows (4 W doubles) to the exchange
+    if (!tma_enabled() || pl->rs_minseg < (kTmaRowBytes / int(sizeof(T))) / 8) return false;
     CUtensorMap m32, m1;
     if (!tma_encode<T>(F, ldf, N, pl->row1 - pl->row0, &m32, &m1)) return false;
     TmaSched sch;
