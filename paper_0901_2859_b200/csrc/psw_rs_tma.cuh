@@ -847,13 +847,22 @@ inline unsigned tma_grid(const psw_plan* pl, const TmaSched& sch) {
 
 template <typename KernT>
 cudaError_t tma_smem_attr(KernT kern, size_t smem) {
+    // per kernel (several kernels share one signature)
     static std::mutex mu;
-    static size_t set = 0;
+    static std::vector<std::pair<const void*, size_t>> set;
     std::lock_guard<std::mutex> lk(mu);
-    if (smem <= set) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e == cudaSuccess) set = smem;
-    return e;
+    const void* key = reinterpret_cast<const void*>(kern);
+    for (auto& e : set)
+        if (e.first == key) {
+            if (smem <= e.second) return cudaSuccess;
+            const cudaError_t r =
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            if (r == cudaSuccess) e.second = smem;
+            return r;
+        }
+    const cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (r == cudaSuccess) set.push_back({key, smem});
+    return r;
 }
 
 // K1 through the TMA pipeline; returns false (nothing launched) when the
