@@ -35,6 +35,7 @@ struct TmaSched {
     int stages;
     int reverse;
     int mr;  // max runs per group (K3 aux slots per kind)
+    int early;  // K3 store variant: release the previous stage after the forward sweep
 };
 
 struct TileIt {
@@ -632,6 +633,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rs_solve_tma_st(
     }
     TileIt it;
     int i = 0, prev_st = -1;
+    const bool early = sch.early != 0;
     for (bool ok = it.start(sch); ok; ok = it.next(sch), ++i) {
         const int st = i % sch.stages;
         mbar_wait(&full[st], uint32_t((i / sch.stages) & 1));
@@ -691,6 +693,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rs_solve_tma_st(
                 xw[W + lane + 32 * u] = double(lx[u]);
             }
         }
+        // the previous tile's store has had a forward sweep's time to read
+        // its stage: release this warp's share now rather than at the end
+        if (lane == 0 && prev_st >= 0 && early) {
+            bulk_wait_read<0>();
+            mbar_arrive(&empty[prev_st]);
+        }
+        if (early) prev_st = -1;
         consumers_sync();
         T D[VPL], x[VPL], xl[VPL];
         if (sv) {
@@ -835,6 +844,7 @@ bool tma_plan(const psw_plan* pl, int64_t N, TmaSched& sch, size_t& stage_bytes,
     sch.cs = cs;
     sch.nunits = pl->rs_ngroups * sch.nsets;
     sch.reverse = AUX ? tma_env("PSW_TMA_REV", 1) : 0;
+    sch.early = tma_env("PSW_K3_EARLY", 0);  // measured: C3 K3 2.85 -> 3.02 ms with it
     (void)nsm;
     return true;
 }
