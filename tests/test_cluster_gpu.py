@@ -1,7 +1,8 @@
 """CLUSTER path (psw_cluster.cu): one persistent kernel, C-CTA clusters of
-G-block strips, F read once and X written once. Agreement with STAGED to
-rounding and the fp64 gate against the reference on every golden case it
-supports; ragged N, padded leading dimensions, fp32, the full C1 config."""
+G-block strips, F read once and X written once. The fp64 gate against the
+reference (golden fixtures, or the CPU oracle on the same inputs) on every
+case, plus agreement with STAGED to rounding; ragged N, padded leading
+dimensions, fp32, the full C1 config."""
 import numpy as np
 import pytest
 
@@ -9,6 +10,12 @@ from conftest import golden_cases, load_golden, rel_l2
 from test_parity_gpu import FP32_TOL, FP64_TOL, gpu_solve, plan_for
 
 pytestmark = pytest.mark.gpu
+
+
+def _oracle(sub, diag, sup, bnd, F):
+    from oracle.pyoracle import Oracle
+    return Oracle().solve_batch_threads(sub, diag, sup, np.asarray(bnd, np.int64),
+                                        np.ascontiguousarray(F), 8)[0]
 
 
 def _supported(psw, cuda, plan, F):
@@ -42,6 +49,7 @@ def test_cluster_ragged(psw, cuda, N):
     X2 = gpu_solve(psw, cuda, plan, F, 0, path=psw.PATH_CLUSTER, inplace=False, pad=2)
     assert rel_l2(X, ref) <= 1e-12
     assert np.array_equal(X, X2)
+    assert rel_l2(X, _oracle(g["sub"], g["diag"], g["super"], g["bnd"], F)) <= FP64_TOL
 
 
 def test_cluster_c0(psw, cuda):
@@ -92,10 +100,14 @@ def test_cluster_shapes(psw, cuda, n, P, dtype):
     plan = psw.Plan(psw.TridiagMatrix.symmetric(a, b), psw.decompose(n, P).induced_partition(),
                     dtype=psw.F64 if dtype == 0 else psw.F32)
     F = rng.uniform(-1, 1, (300, n))
+    if dtype == 1:
+        F = F.astype(np.float32).astype(np.float64)
     ref = gpu_solve(psw, cuda, plan, F, 0, path=psw.PATH_STAGED)
     X = gpu_solve(psw, cuda, plan, F, 0, path=psw.PATH_CLUSTER)
     tol = 1e-12 if dtype == 0 else 1e-5
     assert rel_l2(X, ref) <= tol, rel_l2(X, ref)
+    bnd = psw.decompose(n, P).induced_partition().boundaries
+    assert rel_l2(X, _oracle(a, b, a, bnd, F)) <= (FP64_TOL if dtype == 0 else FP32_TOL)
 
 
 @pytest.mark.parametrize("n,P", [(4096, 16), (2048, 4), (4096, 32), (1024, 4), (2048, 8),
@@ -117,6 +129,8 @@ def test_cluster_shapes_s(psw, cuda, n, P):
         return
     ref = gpu_solve(psw, cuda, plan, F, 1, path=psw.PATH_STAGED)
     assert rel_l2(X, ref) <= 1e-12, rel_l2(X, ref)
+    bnd = psw.decompose(n, P).induced_partition().boundaries
+    assert rel_l2(X, _oracle(a, b, a, bnd, F)) <= FP64_TOL
 
 
 @pytest.mark.parametrize("N", [2, 16, 18, 100, 1000])
@@ -130,6 +144,7 @@ def test_cluster_layout_s(psw, cuda, N):
     X2 = gpu_solve(psw, cuda, plan, F, 1, path=psw.PATH_CLUSTER, inplace=False, pad=2)
     assert rel_l2(X, ref) <= 1e-12, rel_l2(X, ref)
     assert np.array_equal(X, X2)
+    assert rel_l2(X, _oracle(g["sub"], g["diag"], g["super"], g["bnd"], F)) <= FP64_TOL
 
 
 @pytest.mark.parametrize("name", ["c0_n1024_P4", "c1_n4096_P16", "c4_n4096_P16"])
