@@ -53,15 +53,48 @@ __global__ void __launch_bounds__(kDstThreads) dst_pair_kernel(
         v[__brev(unsigned(i)) >> (32 - logL)] = make_double2(re, im);
     }
     __syncthreads();
-    for (int len = 2; len <= L; len <<= 1) {
+    // Radix2Fft::transform's stages len = 2, 4, ..., L, three at a time: the
+    // eight elements k + j q (j < 8) of an 8q block in registers go through
+    // the stages of half q, 2q, 4q with the same butterflies, twiddles and
+    // order as the radix-2 sweep (bitwise equal to it), a third of the
+    // shared-memory passes and barriers. The 1 or 2 leftover stages run first.
+    int len = 2;
+    const int rem = logL % 3;
+    for (int t = 0; t < rem; ++t, len <<= 1) {
         const int half = len >> 1, step = L / len;
         for (int bf = threadIdx.x; bf < L / 2; bf += blockDim.x) {
-            const int k = bf & (half - 1), i0 = (bf - k) * 2 + k;  // start + k, start = (bf / half) * len
+            const int k = bf & (half - 1), i0 = (bf - k) * 2 + k;
             const double2 w = tw[k * step];
             const double2 x = v[i0], y = v[i0 + half];
             const double tr = w.x * y.x - w.y * y.y, ti = w.x * y.y + w.y * y.x;  // w * b
             v[i0 + half] = make_double2(x.x - tr, x.y - ti);
             v[i0] = make_double2(x.x + tr, x.y + ti);
+        }
+        __syncthreads();
+    }
+    for (; len <= L / 4; len <<= 3) {
+        const int q = len >> 1;
+        for (int bf = threadIdx.x; bf < L / 8; bf += blockDim.x) {
+            const int k = bf & (q - 1), i0 = (bf - k) * 8 + k;
+            double2 e[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) e[j] = v[i0 + j * q];
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                const int h = 1 << t;                  // in units of q
+                const int step = L / (len << t);       // L / len_t
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (j & h) continue;
+                    const double2 w = tw[(k + (j & (h - 1)) * q) * step];
+                    const double2 y = e[j + h];
+                    const double tr = w.x * y.x - w.y * y.y, ti = w.x * y.y + w.y * y.x;
+                    e[j + h] = make_double2(e[j].x - tr, e[j].y - ti);
+                    e[j] = make_double2(e[j].x + tr, e[j].y + ti);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[i0 + j * q] = e[j];
         }
         __syncthreads();
     }

@@ -25,7 +25,19 @@
 
 constexpr int kTmaWarps = kRsSeg;                 // consumer warps (segment each)
 constexpr int kTmaThreads = (kTmaWarps + 1) * 32;  // + the producer warp
-constexpr int kTmaRowBytes = 256;                 // bytes of RHS per tile row
+#ifndef PSW_F32_ROW_BYTES
+#define PSW_F32_ROW_BYTES 256
+#endif
+// bytes of RHS per tile row: 32 fp64 RHS (one per lane); fp32 tiles take
+// PSW_F32_ROW_BYTES (256: two RHS per lane, 128: one)
+template <typename T>
+__host__ __device__ constexpr int tma_rb() {
+    return sizeof(T) == 8 ? 256 : PSW_F32_ROW_BYTES;
+}
+template <typename T>
+__host__ __device__ constexpr int tma_w() {
+    return tma_rb<T>() / int(sizeof(T));
+}
 
 struct TmaSched {
     int nchunks;  // ceil(N / W)
@@ -102,8 +114,8 @@ template <typename T>
 __device__ __forceinline__ void tma_aux(const RsGroup& G, int col, const TmaSched& sch,
                                         const RsScratch& sc, const double* __restrict__ V,
                                         int64_t ldv, unsigned char* stage, uint64_t* bar) {
-    constexpr int W = kTmaRowBytes / int(sizeof(T));
-    double* aux = reinterpret_cast<double*>(stage + size_t(kTmaRows) * kTmaRowBytes);
+    constexpr int W = tma_w<T>();
+    double* aux = reinterpret_cast<double*>(stage + size_t(kTmaRows) * tma_rb<T>());
     for (int j = 0; j < G.r1 - G.r0; ++j) {
         const int64_t o = int64_t(G.r0 + j) * sc.ld + col;
         bulk_load(aux + (0 * sch.mr + j) * W, sc.dt + o, W * 8, bar);
@@ -126,7 +138,7 @@ __device__ __forceinline__ void tma_produce(const CUtensorMap* m32, const CUtens
                                             unsigned char* stage0, size_t stage_bytes,
                                             unsigned char* cbuf0, size_t cbuf_bytes,
                                             uint64_t* full, uint64_t* empty) {
-    constexpr int W = kTmaRowBytes / int(sizeof(T));
+    constexpr int W = tma_w<T>();
     constexpr int kMeta = AUX ? kMetaK3 : kMetaK1;
     const uint64_t pol = AUX && sch.reverse ? policy_evict_first() : policy_evict_normal();
     TileIt it;
@@ -143,7 +155,7 @@ __device__ __forceinline__ void tma_produce(const CUtensorMap* m32, const CUtens
         unsigned char* cb = cbuf0 + size_t(it.ord & 1) * cbuf_bytes;
         const int rows = G.rb - G.ra, ns = G.s1 - G.s0, nr = G.r1 - G.r0;
         const int nvl = nr - (G.t0 == 0 ? 1 : 0);  // K3: runs whose block has a left boundary value
-        uint32_t bytes = uint32_t(rows) * kTmaRowBytes;
+        uint32_t bytes = uint32_t(rows) * tma_rb<T>();
         if (AUX) bytes += uint32_t(2 * nr + nvl) * W * 8;
         if (it.first)
             bytes += uint32_t(sizeof(RsGroup) + ns * (sizeof(SegDesc) + sizeof(SegCoef)) +
@@ -162,9 +174,9 @@ __device__ __forceinline__ void tma_produce(const CUtensorMap* m32, const CUtens
         const int col = it.c * W, r0 = G.ra - row0;
         const int n32 = rows >> 5;
         for (int j = 0; j < n32; ++j)
-            tma_load_2d_hint(stage + size_t(j) * 32 * kTmaRowBytes, m32, col, r0 + 32 * j, &full[st], pol);
+            tma_load_2d_hint(stage + size_t(j) * 32 * tma_rb<T>(), m32, col, r0 + 32 * j, &full[st], pol);
         for (int r = n32 * 32; r < rows; ++r)
-            tma_load_2d_hint(stage + size_t(r) * kTmaRowBytes, m1, col, r0 + r, &full[st], pol);
+            tma_load_2d_hint(stage + size_t(r) * tma_rb<T>(), m1, col, r0 + r, &full[st], pol);
         if (AUX) {
             // K3 is a programmatic dependent launch of the carry kernel: the
             // first S tiles' F rows go out before waiting for the carries
@@ -194,7 +206,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rs_part_tma(
     int32_t row0, TmaSched sch, const RsGroup* __restrict__ groups, const RsRun* __restrict__ runs,
     const SegDesc* __restrict__ desc, const SegCoef* __restrict__ segc,
     const FusedFwd<T>* __restrict__ ff, RsScratch sc, uint32_t stage_bytes, uint32_t cbuf_bytes) {
-    constexpr int VPL = 8 / int(sizeof(T)), W = 32 * VPL;
+    constexpr int W = tma_w<T>(), VPL = W / 32;
     extern __shared__ __align__(1024) unsigned char dyn[];
     unsigned char* stage0 = dyn;
     unsigned char* cbuf0 = dyn + size_t(sch.stages) * stage_bytes;
@@ -343,14 +355,14 @@ __device__ __forceinline__ void k3_issue(K3Issuer<T>& q, const TmaSched& sch,
                                          int64_t ldv, unsigned char* stage0, size_t stage_bytes,
                                          unsigned char* cbuf0, size_t cbuf_bytes, uint64_t* full,
                                          uint64_t pol) {
-    constexpr int W = kTmaRowBytes / int(sizeof(T));
+    constexpr int W = tma_w<T>();
     if (!q.ok) return;
     const int st = q.n % sch.stages;
     const RsGroup& G = q.G;
     unsigned char* stage = stage0 + size_t(st) * stage_bytes;
     const int rows = G.rb - G.ra, ns = G.s1 - G.s0, nr = G.r1 - G.r0;
     const int nvl = nr - (G.t0 == 0 ? 1 : 0);  // runs whose block has a left boundary value
-    uint32_t bytes = uint32_t(rows) * kTmaRowBytes + uint32_t(2 * nr + nvl) * W * 8;
+    uint32_t bytes = uint32_t(rows) * tma_rb<T>() + uint32_t(2 * nr + nvl) * W * 8;
     if (q.it.first)
         bytes += uint32_t(sizeof(RsGroup) + ns * (sizeof(SegDesc) + sizeof(SegCoef) + sizeof(CarryW)) +
                           nr * sizeof(RsRun) + rows * sizeof(SolveCoef<T>));
@@ -367,10 +379,10 @@ __device__ __forceinline__ void k3_issue(K3Issuer<T>& q, const TmaSched& sch,
     }
     const int col = q.it.c * W, r0 = G.ra - row0, n32 = rows >> 5;
     for (int j = 0; j < n32; ++j)
-        tma_load_2d_hint(stage + size_t(j) * 32 * kTmaRowBytes, m32, col, r0 + 32 * j, &full[st], pol);
+        tma_load_2d_hint(stage + size_t(j) * 32 * tma_rb<T>(), m32, col, r0 + 32 * j, &full[st], pol);
     for (int r = n32 * 32; r < rows; ++r)
-        tma_load_2d_hint(stage + size_t(r) * kTmaRowBytes, m1, col, r0 + r, &full[st], pol);
-    double* aux = reinterpret_cast<double*>(stage + size_t(kTmaRows) * kTmaRowBytes);
+        tma_load_2d_hint(stage + size_t(r) * tma_rb<T>(), m1, col, r0 + r, &full[st], pol);
+    double* aux = reinterpret_cast<double*>(stage + size_t(kTmaRows) * tma_rb<T>());
     for (int j = 0; j < nr; ++j) {  // [D_in | x_B | x_l] x runs, W doubles each
         const int64_t o = int64_t(G.r0 + j) * sc.ld + col;
         bulk_load(aux + (0 * sch.mr + j) * W, sc.dt + o, W * 8, &full[st]);
@@ -391,7 +403,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 1) rs_solve_tma(
     const SegCoef* __restrict__ segc, const SolveCoef<T>* __restrict__ sco,
     const CarryW* __restrict__ cw, RsScratch sc, const double* __restrict__ V, int64_t ldv,
     uint32_t stage_bytes, uint32_t cbuf_bytes) {
-    constexpr int VPL = 8 / int(sizeof(T)), W = 32 * VPL;
+    constexpr int W = tma_w<T>(), VPL = W / 32;
     extern __shared__ __align__(1024) unsigned char dyn[];
     unsigned char* stage0 = dyn;
     unsigned char* cbuf0 = dyn + size_t(sch.stages) * stage_bytes;
@@ -424,7 +436,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 1) rs_solve_tma(
         mbar_wait(&full[st], uint32_t((i / sch.stages) & 1));
         const T* tile = reinterpret_cast<const T*>(stage0 + size_t(st) * stage_bytes);
         const double* aux = reinterpret_cast<const double*>(stage0 + size_t(st) * stage_bytes +
-                                                            size_t(kTmaRows) * kTmaRowBytes);
+                                                            size_t(kTmaRows) * tma_rb<T>());
         const unsigned char* cb = cbuf0 + size_t(it.ord & 1) * cbuf_bytes;
         const TmaMeta* mt = reinterpret_cast<const TmaMeta*>(cb);
         const SolveCoef<T>* cf = reinterpret_cast<const SolveCoef<T>*>(cb + kMetaK3);
@@ -609,7 +621,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rs_solve_tma_st(
     const SegDesc* __restrict__ desc, const SegCoef* __restrict__ segc,
     const SolveCoef<T>* __restrict__ sco, const CarryW* __restrict__ cw, RsScratch sc,
     const double* __restrict__ V, int64_t ldv, uint32_t stage_bytes, uint32_t cbuf_bytes) {
-    constexpr int VPL = 8 / int(sizeof(T)), W = 32 * VPL;
+    constexpr int W = tma_w<T>(), VPL = W / 32;
     extern __shared__ __align__(1024) unsigned char dyn[];
     unsigned char* stage0 = dyn;
     unsigned char* cbuf0 = dyn + size_t(sch.stages) * stage_bytes;
@@ -639,7 +651,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rs_solve_tma_st(
         mbar_wait(&full[st], uint32_t((i / sch.stages) & 1));
         T* tile = reinterpret_cast<T*>(stage0 + size_t(st) * stage_bytes);
         const double* aux = reinterpret_cast<const double*>(stage0 + size_t(st) * stage_bytes +
-                                                            size_t(kTmaRows) * kTmaRowBytes);
+                                                            size_t(kTmaRows) * tma_rb<T>());
         const unsigned char* cb = cbuf0 + size_t(it.ord & 1) * cbuf_bytes;
         const TmaMeta* mt = reinterpret_cast<const TmaMeta*>(cb);
         const SolveCoef<T>* cf = reinterpret_cast<const SolveCoef<T>*>(cb + kMetaK3);
@@ -775,7 +787,7 @@ template <typename T>
 bool tma_encode(const void* F, int64_t ldf, int64_t N, int64_t rows, CUtensorMap* m32,
                 CUtensorMap* m1) {
     const auto enc = tensor_map_encoder();
-    constexpr int es = int(sizeof(T)), W = kTmaRowBytes / es;
+    constexpr int es = int(sizeof(T)), W = tma_w<T>();
     if (!enc || (reinterpret_cast<uintptr_t>(F) & 15) || (ldf * es) % 16 || N < W || rows < 1 ||
         ldf < N)
         return false;
@@ -807,13 +819,13 @@ inline size_t tma_smem(int stages, size_t stage_bytes, size_t cbuf_bytes, size_t
 template <typename T, typename Coef, bool AUX>
 bool tma_plan(const psw_plan* pl, int64_t N, TmaSched& sch, size_t& stage_bytes,
               size_t& cbuf_bytes, size_t& smem, bool store = false) {
-    constexpr int W = kTmaRowBytes / int(sizeof(T));
+    constexpr int W = tma_w<T>();
     int dev = pl->device, nsm = 0, maxs = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&maxs, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     sch.mr = std::max(1, pl->rs_maxruns);
     sch.nchunks = int((N + W - 1) / W);
-    stage_bytes = size_t(kTmaRows) * kTmaRowBytes + (AUX ? size_t(3) * sch.mr * W * 8 : 0);
+    stage_bytes = size_t(kTmaRows) * tma_rb<T>() + (AUX ? size_t(3) * sch.mr * W * 8 : 0);
     cbuf_bytes = size_t(AUX ? kMetaK3 : kMetaK1) + size_t(kTmaRows) * sizeof(Coef);
     const size_t xch = (store || !AUX) ? 0 : size_t(2) * kRsSeg * W * 8;
     sch.stages = std::min(tma_env("PSW_TMA_STAGES", 3), kTmaMaxStages);
@@ -882,7 +894,8 @@ bool launch_part_tma(const psw_plan* pl, const T* F, int64_t ldf, int64_t N, con
                      cudaStream_t s, int& rc) {
     rc = PSW_OK;
     // each segment lends its first W / 8 rows (4 W doubles) to the exchange
-    if (!tma_enabled() || pl->rs_minseg < (kTmaRowBytes / int(sizeof(T))) / 8) return false;
+    // each segment lends 4 W doubles of its first rows to the exchange
+    if (!tma_enabled() || pl->rs_minseg < 32 * tma_w<T>() / tma_rb<T>()) return false;
     CUtensorMap m32, m1;
     if (!tma_encode<T>(F, ldf, N, pl->row1 - pl->row0, &m32, &m1)) return false;
     TmaSched sch;
@@ -902,14 +915,14 @@ bool launch_part_tma(const psw_plan* pl, const T* F, int64_t ldf, int64_t N, con
 template <typename T>
 bool launch_solve_tma(const psw_plan* pl, const T* F, int64_t ldf, T* X, int64_t ldx, int64_t N,
                       const RsScratch& sc, const double* V, int64_t ldv, cudaStream_t s, int& rc) {
-    constexpr int W = kTmaRowBytes / int(sizeof(T));
+    constexpr int W = tma_w<T>();
     rc = PSW_OK;
     if (!tma_enabled() || (ldv & 1) || ldv < (N + W - 1) / W * W) return false;
     CUtensorMap m32, m1;
     if (!tma_encode<T>(F, ldf, N, pl->row1 - pl->row0, &m32, &m1)) return false;
     // the store variant lends each segment's first rows to the exchange
-    // (2 W doubles = W / 16 rows of 256 bytes)
-    if (tma_env("PSW_K3_STORE", 1) && pl->rs_minseg >= W / 16) {
+    // (2 W doubles of its first rows)
+    if (tma_env("PSW_K3_STORE", 1) && pl->rs_minseg >= 16 * W / tma_rb<T>()) {
         CUtensorMap x32, x1;
         if (tma_encode<T>(X, ldx, N, pl->row1 - pl->row0, &x32, &x1)) {
             TmaSched sch;
