@@ -144,6 +144,16 @@ int psw_plan_info(const psw_plan* plan, psw_plan_info_t* info);
  * must share the order, the partition, the dtype and the device. */
 int psw_solve_multi(const psw_plan* const* plans, int64_t nplans, const void* F, int64_t ldf,
                     void* X, int64_t ldx, void* stream);
+/* The same solve for repeated use (one FourierWorkspace, many right-hand
+ * sides): psw_multi_create gathers the plans' sweep tables once into
+ * RHS-interleaved device arrays (coalesced loads) and keeps the Z-sample
+ * table on the device; psw_multi_solve is then asynchronous on `stream`
+ * (no host copies). The plans must outlive the bundle. */
+typedef struct psw_multi psw_multi;
+int psw_multi_create(psw_multi** out, const psw_plan* const* plans, int64_t nplans);
+void psw_multi_destroy(psw_multi* multi);
+int psw_multi_solve(const psw_multi* multi, const void* F, int64_t ldf, void* X, int64_t ldx,
+                    void* stream);
 
 /* ---- batched solve ---------------------------------------------------- */
 /* Replaces the per-RHS loop of solve_batch (dichotomy/batch.hpp:67-73) over

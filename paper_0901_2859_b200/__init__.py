@@ -31,7 +31,7 @@ import numpy as np
 
 __all__ = [
     "TridiagMatrix", "Partition", "Decomposition", "decompose", "compute_preliminary", "Plan",
-    "solve_batch", "solve_multi", "SolverError", "PivotBreakdown", "TooManyPEs", "NotSupported", "NotSymmetrizable", "OracleFallbackRequired", "CudaError",
+    "solve_batch", "solve_multi", "MultiPlan", "SolverError", "PivotBreakdown", "TooManyPEs", "NotSupported", "NotSymmetrizable", "OracleFallbackRequired", "CudaError",
     "F64", "F32", "LAYOUT_R", "LAYOUT_S", "PATH_AUTO", "PATH_STAGED", "PATH_FUSED", "PATH_CHUNKED",
     "PATH_RESWEEP", "PATH_CLUSTER", "last_path", "lib", "library_path", "Comm", "NcclError",
 ]
@@ -128,6 +128,10 @@ def lib() -> C.CDLL:
         L.psw_solve_host.argtypes = [vp, vp, C.c_int64, vp, C.c_int64, C.c_int64, C.c_int]
         L.psw_solve_multi.argtypes = [C.POINTER(vp), C.c_int64, vp, C.c_int64, vp, C.c_int64, vp]
         L.psw_dst_rows.argtypes = [vp, C.c_int64, vp, C.c_int64, C.c_int64, C.c_int64, C.c_double, vp]
+        L.psw_multi_create.argtypes = [C.POINTER(vp), C.POINTER(vp), C.c_int64]
+        L.psw_multi_destroy.argtypes = [vp]
+        L.psw_multi_destroy.restype = None
+        L.psw_multi_solve.argtypes = [vp, vp, C.c_int64, vp, C.c_int64, vp]
         L.psw_shard_partials_count.argtypes = [vp]
         L.psw_shard_partials_count.restype = C.c_int64
         L.psw_shard_row_offset.argtypes = [vp]
@@ -582,6 +586,37 @@ def solve_multi(plans: Sequence["Plan"], F, X, stream=None):
     arr = (C.c_void_p * len(plans))(*[pl._h for pl in plans])
     _check(lib().psw_solve_multi(arr, len(plans), _ptr(F), F.stride(0), _ptr(X), X.stride(0),
                                  _stream_ptr(stream)))
+
+
+class MultiPlan:
+    """psw_multi: the plans' sweep tables gathered once (RHS-interleaved) for
+    repeated multi-matrix solves; keeps the plans alive."""
+
+    def __init__(self, plans: Sequence["Plan"]):
+        self.plans = list(plans)
+        arr = (C.c_void_p * len(self.plans))(*[pl._h for pl in self.plans])
+        h = C.c_void_p()
+        _check(lib().psw_multi_create(C.byref(h), arr, len(self.plans)))
+        self._h = h
+
+    def solve(self, F, X, stream=None):
+        for t, nm in ((F, "F"), (X, "X")):
+            if not getattr(t, "is_cuda", False) or t.dim() != 2 or t.stride(1) != 1:
+                raise ValueError(f"{nm}: a CUDA matrix with contiguous rows")
+            if t.shape[1] < len(self.plans) or t.shape[0] < self.plans[0].n:
+                raise ValueError(f"{nm}: too small for the bundle")
+        _check(lib().psw_multi_solve(self._h, _ptr(F), F.stride(0), _ptr(X), X.stride(0),
+                                     _stream_ptr(stream)))
+        return X
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                lib().psw_multi_destroy(h)
+            except Exception:  # noqa: BLE001
+                pass
+            self._h = None
 
 
 def fill_uniform(t, seed: int, lo: float, hi: float, offset: int = 0, stream=None):

@@ -12,6 +12,7 @@
 // therefore gets bitwise the betas, boundary values and solution of a
 // single-plan STAGED solve, i.e. the reference's betas and boundary values.
 // All plans share the partition (the workspace's, fourier.hpp:47-51).
+#include <algorithm>
 #include <vector>
 
 #include "psw_device.cuh"
@@ -120,6 +121,240 @@ int launch_multi(const psw_plan* const* plans, int64_t N, const void* Fv, int64_
 
 }  // namespace
 }  // namespace psw
+
+// ---------------------------------------------------------------- bundles
+// psw_multi_create gathers the plans' per-row sweep tables once into
+// interleaved arrays ([row][rhs]: a warp's 32 right-hand sides read one
+// contiguous 1 KB / 512 B piece per row) and keeps the Z-sample pointer
+// table on the device; psw_multi_solve then runs the same three kernels with
+// coalesced coefficient loads, rows in register batches, no host sync.
+namespace psw {
+namespace {
+
+constexpr int kMB = 16;  // rows per register batch
+
+template <typename T>
+__global__ void multi_gather_kernel(const FwdCoef<T>* const* __restrict__ cfs,
+                                    const BwdCoef<T>* const* __restrict__ cbs, int64_t n, int64_t N,
+                                    FwdCoef<T>* __restrict__ fo, BwdCoef<T>* __restrict__ bo) {
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= N) return;
+    for (int64_t q = blockIdx.y; q < n; q += gridDim.y) {
+        fo[q * N + k] = cfs[k][q];
+        bo[q * N + k] = cbs[k][q];
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) bundle_fwd_kernel(
+    const T* __restrict__ F, int64_t ldf, T* __restrict__ X, int64_t ldx, int64_t N,
+    const int32_t* __restrict__ blk, const FwdCoef<T>* __restrict__ cf, double* __restrict__ bl_out,
+    double* __restrict__ br_out, int p) {
+    const int t = blockIdx.y;
+    const int64_t k = int64_t(blockIdx.x) * kThreads + threadIdx.x;
+    if (k >= N) return;
+    const int s = blk[2 * t], e = blk[2 * t + 1];
+    T d = T(0);
+    double br = 0.0, bl = 0.0;
+    for (int q0 = s; q0 < e; q0 += kMB) {
+        T fv[kMB];
+        FwdCoef<T> c[kMB];
+#pragma unroll
+        for (int u = 0; u < kMB; ++u)
+            if (q0 + u < e) {
+                fv[u] = F[int64_t(q0 + u) * ldf + k];
+                c[u] = cf[int64_t(q0 + u) * N + k];
+            }
+#pragma unroll
+        for (int u = 0; u < kMB; ++u)
+            if (q0 + u < e) {
+                d = fma(c[u].ma, d, fv[u] * c[u].rp);
+                br = madd_rn(br, double(fv[u]), double(c[u].gr));
+                bl = madd_rn(bl, double(fv[u]), double(c[u].gl));
+                X[int64_t(q0 + u) * ldx + k] = d;
+            }
+    }
+    if (t < p) br_out[int64_t(t) * N + k] = br;
+    if (t > 0) bl_out[int64_t(t) * N + k] = bl;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) bundle_bwd_kernel(
+    T* __restrict__ X, int64_t ldx, int64_t N, const int32_t* __restrict__ blk,
+    const BwdCoef<T>* __restrict__ cb, const double* __restrict__ V, int p) {
+    const int t = blockIdx.y;
+    const int64_t k = int64_t(blockIdx.x) * kThreads + threadIdx.x;
+    if (k >= N) return;
+    const int s = blk[2 * t], e = blk[2 * t + 1];
+    const T xl = t > 0 ? T(V[int64_t(t - 1) * N + k]) : T(0);
+    T xn = t < p ? T(V[int64_t(t) * N + k]) : T(0);
+    for (int q1 = e - 1; q1 >= s; q1 -= kMB) {
+        T dv[kMB];
+        BwdCoef<T> c[kMB];
+#pragma unroll
+        for (int u = 0; u < kMB; ++u)
+            if (q1 - u >= s) {
+                dv[u] = X[int64_t(q1 - u) * ldx + k];
+                c[u] = cb[int64_t(q1 - u) * N + k];
+            }
+#pragma unroll
+        for (int u = 0; u < kMB; ++u)
+            if (q1 - u >= s) {
+                xn = fma(c[u].al, xn, fma(xl, c[u].w, dv[u]));
+                X[int64_t(q1 - u) * ldx + k] = xn;
+            }
+    }
+}
+
+}  // namespace
+}  // namespace psw
+
+struct psw_multi {
+    int64_t n = 0, N = 0, P = 1, p = 0;
+    int dtype = PSW_F64, device = 0;
+    const psw_plan* p0 = nullptr;  // partition, level items (shared by every plan)
+    void* fwd = nullptr;           // FwdCoef<T>[n][N]
+    void* bwd = nullptr;           // BwdCoef<T>[n][N]
+    void* zptr = nullptr;          // const double*[2][N]: every plan's ZR, ZL samples
+};
+
+extern "C" int psw_multi_create(psw_multi** out, const psw_plan* const* plans, int64_t nplans) {
+    psw::clear_error();
+    if (!out || nplans <= 0 || !plans) {
+        psw::set_error(PSW_INVALID_ARGUMENT, "psw_multi_create: invalid arguments");
+        return PSW_INVALID_ARGUMENT;
+    }
+    *out = nullptr;
+    const psw_plan* p0 = plans[0];
+    for (int64_t k = 0; k < nplans; ++k) {
+        const psw_plan* q = plans[k];
+        if (!q || q->world != 1 || q->n != p0->n || q->P != p0->P || q->dtype != p0->dtype ||
+            q->device != p0->device || q->bnd != p0->bnd) {
+            psw::set_error(PSW_INVALID_ARGUMENT,
+                           "psw_multi_create: plans must share order, partition, dtype and device");
+            return PSW_INVALID_ARGUMENT;
+        }
+    }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    PSW_CUDA_TRY(cudaSetDevice(p0->device));
+    auto* m = new psw_multi();
+    m->n = p0->n;
+    m->N = nplans;
+    m->P = p0->P;
+    m->p = p0->p;
+    m->dtype = p0->dtype;
+    m->device = p0->device;
+    m->p0 = p0;
+    const size_t es = p0->dtype == PSW_F64 ? 8 : 4;
+    const size_t fb = sizeof(double) * 4 * size_t(m->n) * size_t(nplans) / (8 / es);
+    const size_t bb = 16 * size_t(m->n) * size_t(nplans);
+    std::vector<const void*> tab(size_t(4) * nplans);
+    for (int64_t k = 0; k < nplans; ++k) {
+        tab[size_t(k)] = plans[k]->d_fwd;
+        tab[size_t(nplans + k)] = plans[k]->d_bwd;
+        tab[size_t(2 * nplans + k)] = plans[k]->d_zr;
+        tab[size_t(3 * nplans + k)] = plans[k]->d_zl;
+    }
+    void* dtab = nullptr;
+    cudaError_t e = cudaMalloc(&m->fwd, fb);
+    if (e == cudaSuccess) e = cudaMalloc(&m->bwd, bb);
+    if (e == cudaSuccess) e = cudaMalloc(&m->zptr, sizeof(void*) * 2 * size_t(nplans));
+    if (e == cudaSuccess) e = cudaMalloc(&dtab, sizeof(void*) * tab.size());
+    if (e == cudaSuccess)
+        e = cudaMemcpy(dtab, tab.data(), sizeof(void*) * tab.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(m->zptr, tab.data() + 2 * nplans, sizeof(void*) * 2 * size_t(nplans),
+                       cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        const dim3 grid(unsigned((nplans + 127) / 128), unsigned(std::min<int64_t>(m->n, 4096)));
+        auto** dt = static_cast<const void**>(dtab);
+        if (p0->dtype == PSW_F64)
+            psw::multi_gather_kernel<double><<<grid, 128>>>(
+                reinterpret_cast<const psw::FwdCoef<double>* const*>(dt),
+                reinterpret_cast<const psw::BwdCoef<double>* const*>(dt + nplans), m->n, nplans,
+                static_cast<psw::FwdCoef<double>*>(m->fwd), static_cast<psw::BwdCoef<double>*>(m->bwd));
+        else
+            psw::multi_gather_kernel<float><<<grid, 128>>>(
+                reinterpret_cast<const psw::FwdCoef<float>* const*>(dt),
+                reinterpret_cast<const psw::BwdCoef<float>* const*>(dt + nplans), m->n, nplans,
+                static_cast<psw::FwdCoef<float>*>(m->fwd), static_cast<psw::BwdCoef<float>*>(m->bwd));
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    }
+    if (dtab) cudaFree(dtab);
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) {
+        psw_multi_destroy(m);
+        return psw::cuda_fail(e, "psw_multi_create");
+    }
+    *out = m;
+    return PSW_OK;
+}
+
+extern "C" void psw_multi_destroy(psw_multi* m) {
+    if (!m) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(m->device);
+    for (void* q : {m->fwd, m->bwd, m->zptr})
+        if (q) cudaFree(q);
+    cudaSetDevice(prev);
+    delete m;
+}
+
+namespace psw {
+namespace {
+template <typename T>
+int bundle_solve(const psw_multi* m, const void* Fv, int64_t ldf, void* Xv, int64_t ldx,
+                 cudaStream_t s) {
+    const int64_t N = m->N;
+    const int P = int(m->P), p = int(m->p);
+    void* scratch = nullptr;
+    const size_t need = sizeof(double) * size_t(N) * (2 * size_t(P) + size_t(p > 0 ? p : 1));
+    PSW_CUDA_TRY(scratch_alloc(&scratch, need, m->device, s));
+    double* bl = static_cast<double*>(scratch);
+    double* br = bl + size_t(P) * N;
+    double* V = br + size_t(P) * N;
+    const dim3 grid(unsigned((N + kThreads - 1) / kThreads), unsigned(P));
+    bundle_fwd_kernel<T><<<grid, kThreads, 0, s>>>(static_cast<const T*>(Fv), ldf,
+                                                   static_cast<T*>(Xv), ldx, N, m->p0->d_blk,
+                                                   static_cast<const FwdCoef<T>*>(m->fwd), bl, br, p);
+    int64_t launches = 1;
+    if (p > 0) {
+        const double* const* zp = static_cast<const double* const*>(m->zptr);
+        multi_combine_kernel<<<grid.x, kThreads, 0, s>>>(bl, br, N, p, m->p0->d_items, zp, zp + N, V);
+        ++launches;
+    }
+    bundle_bwd_kernel<T><<<grid, kThreads, 0, s>>>(static_cast<T*>(Xv), ldx, N, m->p0->d_blk,
+                                                   static_cast<const BwdCoef<T>*>(m->bwd), V, p);
+    ++launches;
+    cudaError_t e = cudaGetLastError();
+    scratch_free(scratch, s);
+    if (e != cudaSuccess) return cuda_fail(e, "multi-plan bundle kernels");
+    note_launches(launches);
+    return PSW_OK;
+}
+}  // namespace
+}  // namespace psw
+
+extern "C" int psw_multi_solve(const psw_multi* m, const void* F, int64_t ldf, void* X, int64_t ldx,
+                               void* stream) {
+    psw::clear_error();
+    psw::reset_launches();
+    if (!m || !F || !X || ldf < m->N || ldx < m->N) {
+        psw::set_error(PSW_INVALID_ARGUMENT, "invalid arguments to psw_multi_solve");
+        return PSW_INVALID_ARGUMENT;
+    }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != m->device) PSW_CUDA_TRY(cudaSetDevice(m->device));
+    auto s = static_cast<cudaStream_t>(stream);
+    const int rc = m->dtype == PSW_F64 ? psw::bundle_solve<double>(m, F, ldf, X, ldx, s)
+                                       : psw::bundle_solve<float>(m, F, ldf, X, ldx, s);
+    if (prev != m->device) cudaSetDevice(prev);
+    return rc;
+}
 
 extern "C" int psw_solve_multi(const psw_plan* const* plans, int64_t nplans, const void* F,
                                int64_t ldf, void* X, int64_t ldx, void* stream) {

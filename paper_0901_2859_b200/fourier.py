@@ -15,8 +15,8 @@ Per Poisson right-hand side:
      and by -h1^2 (fourier.hpp:159) in the same pass — psw_dst_rows, a
      hand-written kernel restating the reference's paired radix-2 FFT of the
      odd extension (dst.hpp:85-149; direct sum for other N);
-  2. rhs = -h1^2 coeff (fourier.hpp:159) and ONE multi-matrix solve of all
-     harmonics (psw_solve_multi: column l of the coefficient grid with the
+  2. ONE multi-matrix solve of all harmonics (psw_multi_solve on the
+     workspace's MultiPlan bundle: column l of the coefficient grid with the
      plan of B_l; the reference's per-harmonic solve_harmonic loop,
      fourier.hpp:157-164);
   3. the inverse DST-I of every row (fourier.hpp:167-186).
@@ -29,7 +29,7 @@ import math
 
 import torch
 
-from . import F64, Plan, TridiagMatrix, solve_multi
+from . import F64, MultiPlan, Plan, TridiagMatrix
 from .adi import _make_partition
 
 
@@ -82,6 +82,7 @@ class FourierWorkspace:
         self.part = _make_partition(order, dichotomy_pes)
         self.harmonics = [harmonic_system(n1, n2, h1, h2, l) for l in range(1, n2)]
         self.plans = [Plan(hs.matrix, self.part, dtype=F64, device=device) for hs in self.harmonics]
+        self._multi = None  # the plans' tables gathered for psw_multi_solve (first use)
 
     def partition(self):
         return self.part
@@ -91,7 +92,9 @@ class FourierWorkspace:
         row i-1 = direction-1 node i) is the right-hand side of B_l."""
         if out is None:
             out = torch.empty_like(coeff)
-        solve_multi(self.plans, coeff, out, stream=stream)
+        if self._multi is None:
+            self._multi = MultiPlan(self.plans)
+        self._multi.solve(coeff, out, stream=stream)
         return out
 
 

@@ -144,3 +144,19 @@ def test_solve_multi_equals_single_plan_staged(psw, cuda):
     with pytest.raises(ValueError):  # plans must share the partition
         other = psw.Plan(psw.TridiagMatrix.symmetric(*As[0]), psw.decompose(n, 5).induced_partition())
         psw.solve_multi(plans[:2] + [other], F, X)
+
+
+@pytest.mark.gpu
+def test_multi_bundle_equals_solve_multi(psw, cuda):
+    """psw_multi_solve (interleaved tables, one gather at creation) is bitwise
+    psw_solve_multi (per-plan tables) on every column."""
+    from paper_0901_2859_b200.fourier import FourierWorkspace
+    n1, n2 = 300, 97
+    ws = FourierWorkspace(n1, n2, 1.0 / n1, 1.0 / n2, 4)
+    rhs = cuda.randn(n1 - 1, n2 - 1, dtype=cuda.float64, device="cuda")
+    a = cuda.empty_like(rhs)
+    psw.solve_multi(ws.plans, rhs, a)
+    b = ws.solve_harmonics(rhs)
+    b2 = psw.MultiPlan(ws.plans).solve(rhs, cuda.empty_like(rhs))
+    cuda.cuda.synchronize()
+    assert bool((a == b).all()) and bool((a == b2).all())
