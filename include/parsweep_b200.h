@@ -132,6 +132,13 @@ int psw_plan_create(psw_plan** out, int64_t n, const double* sub, const double* 
 int psw_plan_create_ex(psw_plan** out, int64_t n, const double* sub, const double* diag,
                        const double* sup, int64_t p, const int64_t* boundaries, int dtype,
                        int device, int strategy);
+/* psw_plan_create_ex with flags: PSW_PLAN_STAGED_ONLY builds only what the
+ * STAGED path and the multi-matrix solve read (no segment tables): plan setup
+ * for many small systems, e.g. one plan per Fourier harmonic. */
+#define PSW_PLAN_STAGED_ONLY 1
+int psw_plan_create_flags(psw_plan** out, int64_t n, const double* sub, const double* diag,
+                          const double* sup, int64_t p, const int64_t* boundaries, int dtype,
+                          int device, int strategy, int flags);
 int psw_plan_destroy(psw_plan* plan);
 int psw_plan_info(const psw_plan* plan, psw_plan_info_t* info);
 

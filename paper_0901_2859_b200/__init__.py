@@ -117,6 +117,8 @@ def lib() -> C.CDLL:
         L.psw_decompose.argtypes = [C.c_int64, C.c_int64, i64]
         L.psw_partition_validate.argtypes = [C.c_int64, C.c_int64, i64]
         L.psw_plan_create.argtypes = [C.POINTER(vp), C.c_int64, d, d, d, C.c_int64, i64, C.c_int, C.c_int]
+        L.psw_plan_create_flags.argtypes = [C.POINTER(vp), C.c_int64, d, d, d, C.c_int64, i64,
+                                            C.c_int, C.c_int, C.c_int, C.c_int]
         L.psw_plan_create_ex.argtypes = [C.POINTER(vp), C.c_int64, d, d, d, C.c_int64, i64, C.c_int,
                                          C.c_int, C.c_int]
         L.psw_shard_plan_create.argtypes = [C.POINTER(vp), C.c_int64, d, d, d, C.c_int64, i64,
@@ -341,7 +343,7 @@ class Plan:
 
     def __init__(self, A: TridiagMatrix, part: Partition, dtype: int = F64, device: int = 0,
                  rank: int | None = None, world: int | None = None,
-                 strategy: int = GROW_AUTO):
+                 strategy: int = GROW_AUTO, staged_only: bool = False):
         L = lib()
         A.validate() if A.n() >= 2 else None
         self.n = A.n()
@@ -359,7 +361,9 @@ class Plan:
         args = (C.byref(h), self.n, A.sub.ctypes.data_as(dp), A.diag.ctypes.data_as(dp),
                 A.super.ctypes.data_as(dp), len(part.boundaries),
                 b.ctypes.data_as(C.POINTER(C.c_int64)), dtype, device)
-        if not shard:
+        if not shard and staged_only:  # STAGED / multi-matrix solves only (cheap setup)
+            _check(L.psw_plan_create_flags(*args, strategy, 1))
+        elif not shard:
             _check(L.psw_plan_create_ex(*args, strategy))
         else:  # row shard of a multi-GPU solve (psw_shard_*)
             _check(L.psw_shard_plan_create(*args, self.rank, self.world))

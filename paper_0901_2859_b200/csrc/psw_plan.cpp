@@ -368,7 +368,7 @@ int validate_inputs(int64_t n, const double* sub, const double* diag, const doub
 int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
                const double* sup, int64_t p, const int64_t* bnd, int dtype, int device,
                int rank, int world, std::vector<double>* cmat_host = nullptr, bool shard = false,
-               int strategy = PSW_GROW_AUTO);
+               int strategy = PSW_GROW_AUTO, int flags = 0);
 
 int device_preliminary(int64_t n, const double* sub, const double* diag, const double* sup,
                        int64_t p, const int64_t* bnd, const std::vector<int32_t>& blk,
@@ -387,7 +387,8 @@ static bool want_device_setup(int64_t n, int64_t p) {
 
 int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
                const double* sup, int64_t p, const int64_t* bnd, int dtype, int device,
-               int rank, int world, std::vector<double>* cmat_host, bool shard, int strategy) {
+               int rank, int world, std::vector<double>* cmat_host, bool shard, int strategy,
+               int flags) {
     clear_error();
     if (!out) {
         set_error(PSW_INVALID_ARGUMENT, "null plan output");
@@ -634,7 +635,10 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
     }
     int rc = (dtype == PSW_F64) ? upload<double>(pl, rp, ma, gr, gl, w, alv, zr, zl)
                                 : upload<float>(pl, rp, ma, gr, gl, w, alv, zr, zl);
-    if (rc == PSW_OK)
+    // PSW_PLAN_STAGED_ONLY: no segment tables (FUSED / CLUSTER / RESWEEP
+    // unsupported, STAGED and the multi-matrix solve only) — a cheap plan for
+    // the many one-RHS systems of the Fourier consumer
+    if (rc == PSW_OK && !(flags & PSW_PLAN_STAGED_ONLY))
         rc = build_fused_tables(pl, rp, ma, gr, gl, w, alv,
                                 pl->P <= 1024 || shard ? combine_matrix(pl, zr, zl)
                                                        : std::vector<double>());
@@ -828,6 +832,13 @@ int psw_plan_create_ex(psw_plan** out, int64_t n, const double* sub, const doubl
                        int device, int strategy) {
     return psw::build_plan(out, n, sub, diag, sup, p, boundaries, dtype, device, 0, 1, nullptr,
                            false, strategy);
+}
+
+int psw_plan_create_flags(psw_plan** out, int64_t n, const double* sub, const double* diag,
+                          const double* sup, int64_t p, const int64_t* boundaries, int dtype,
+                          int device, int strategy, int flags) {
+    return psw::build_plan(out, n, sub, diag, sup, p, boundaries, dtype, device, 0, 1, nullptr,
+                           false, strategy, flags);
 }
 
 int psw_plan_destroy(psw_plan* plan) {

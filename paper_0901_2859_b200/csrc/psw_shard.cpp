@@ -105,7 +105,8 @@ int on_device(int dev, Fn&& body) {
 namespace psw {
 int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
                const double* sup, int64_t p, const int64_t* bnd, int dtype, int device,
-               int rank, int world, std::vector<double>* cmat_host, bool shard, int strategy);
+               int rank, int world, std::vector<double>* cmat_host, bool shard, int strategy,
+               int flags);
 }  // namespace psw
 
 extern "C" {
@@ -113,7 +114,7 @@ int psw_shard_plan_create(psw_plan** out, int64_t n, const double* sub, const do
                           const double* sup, int64_t p, const int64_t* boundaries, int dtype,
                           int device, int rank, int world) {
     return psw::build_plan(out, n, sub, diag, sup, p, boundaries, dtype, device, rank, world,
-                           nullptr, true, PSW_GROW_AUTO);
+                           nullptr, true, PSW_GROW_AUTO, 0);
 }
 int64_t psw_shard_partials_count(const psw_plan* plan) { return plan ? plan->p : -1; }
 int64_t psw_shard_row_offset(const psw_plan* plan) { return plan ? plan->row0 : -1; }

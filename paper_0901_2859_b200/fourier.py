@@ -81,7 +81,9 @@ class FourierWorkspace:
         order = n1 - 1
         self.part = _make_partition(order, dichotomy_pes)
         self.harmonics = [harmonic_system(n1, n2, h1, h2, l) for l in range(1, n2)]
-        self.plans = [Plan(hs.matrix, self.part, dtype=F64, device=device) for hs in self.harmonics]
+        # one plan per harmonic, only what the multi-matrix solve reads
+        self.plans = [Plan(hs.matrix, self.part, dtype=F64, device=device, staged_only=True)
+                      for hs in self.harmonics]
         self._multi = None  # the plans' tables gathered for psw_multi_solve (first use)
 
     def partition(self):

@@ -160,3 +160,21 @@ def test_multi_bundle_equals_solve_multi(psw, cuda):
     b2 = psw.MultiPlan(ws.plans).solve(rhs, cuda.empty_like(rhs))
     cuda.cuda.synchronize()
     assert bool((a == b).all()) and bool((a == b2).all())
+
+
+@pytest.mark.gpu
+def test_staged_only_plan(psw, cuda):
+    """PSW_PLAN_STAGED_ONLY: the same STAGED result as a full plan; the
+    segment-table paths answer NotSupported and AUTO falls back to STAGED."""
+    from test_parity_gpu import gpu_solve
+    g = load_golden("c1_n4096_P16")
+    A = psw.TridiagMatrix(g["sub"], g["diag"], g["super"])
+    part = psw.Partition(A.n(), g["bnd"].tolist())
+    full, lean = psw.Plan(A, part), psw.Plan(A, part, staged_only=True)
+    assert lean.info["device_bytes"] < full.info["device_bytes"]
+    a = gpu_solve(psw, cuda, full, g["F"], 0, path=psw.PATH_STAGED)
+    b = gpu_solve(psw, cuda, lean, g["F"], 0, path=psw.PATH_AUTO)
+    assert np.array_equal(a, b)
+    for path in (psw.PATH_CLUSTER, psw.PATH_RESWEEP, psw.PATH_FUSED):
+        with pytest.raises(psw.NotSupported):
+            gpu_solve(psw, cuda, lean, g["F"], 0, path=path)
