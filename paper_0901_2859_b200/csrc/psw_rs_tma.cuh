@@ -48,6 +48,7 @@ struct TmaSched {
     int reverse;
     int mr;  // max runs per group (K3 aux slots per kind)
     int early;  // K3 store variant: release the previous stage after the forward sweep
+    int xhint;  // K3 store variant: X stores with an evict-first L2 policy
 };
 
 struct TileIt {
@@ -606,6 +607,14 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int
                  "r"(c0), "r"(c1), "r"(smem_u32(src))
                  : "memory");
 }
+__device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, int c0, int c1,
+                                                  const void* src, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(c0), "r"(c1), "r"(smem_u32(src)), "l"(pol)
+        : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -767,8 +776,16 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rs_solve_tma_st(
             if (sv) {
                 const int col = it.c * W, r0 = sd.a - row0, n32 = len >> 5;
                 const T* src = tile + a * W;
-                for (int j = 0; j < n32; ++j) tma_store_2d(&x32, col, r0 + 32 * j, src + size_t(j) * 32 * W);
-                for (int r = n32 * 32; r < len; ++r) tma_store_2d(&x1, col, r0 + r, src + size_t(r) * W);
+                if (sch.xhint) {  // X is not read again here: first to go from L2
+                    const uint64_t pol = policy_evict_first();
+                    for (int j = 0; j < n32; ++j)
+                        tma_store_2d_hint(&x32, col, r0 + 32 * j, src + size_t(j) * 32 * W, pol);
+                    for (int r = n32 * 32; r < len; ++r)
+                        tma_store_2d_hint(&x1, col, r0 + r, src + size_t(r) * W, pol);
+                } else {
+                    for (int j = 0; j < n32; ++j) tma_store_2d(&x32, col, r0 + 32 * j, src + size_t(j) * 32 * W);
+                    for (int r = n32 * 32; r < len; ++r) tma_store_2d(&x1, col, r0 + r, src + size_t(r) * W);
+                }
             }
             bulk_commit();
             // this warp's previous store has read its stage
@@ -856,7 +873,8 @@ bool tma_plan(const psw_plan* pl, int64_t N, TmaSched& sch, size_t& stage_bytes,
     sch.cs = cs;
     sch.nunits = pl->rs_ngroups * sch.nsets;
     sch.reverse = AUX ? tma_env("PSW_TMA_REV", 1) : 0;
-    sch.early = tma_env("PSW_K3_EARLY", 0);  // measured: C3 K3 2.85 -> 3.02 ms with it
+    sch.early = tma_env("PSW_K3_EARLY", 0);
+    sch.xhint = tma_env("PSW_K3_XHINT", 0);  // measured: no difference  // measured: C3 K3 2.85 -> 3.02 ms with it
     (void)nsm;
     return true;
 }
