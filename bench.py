@@ -192,9 +192,15 @@ def _sample_rows(cfg, nr: int) -> np.ndarray:
     the reference's std::vector-per-system layout (nr x n, fp64; fp32
     configs rounded): a bounded sample of the same workload."""
     from paper_0901_2859_b200 import configs
-    full = configs.host_rhs(cfg.with_(nrhs=nr))
-    F = full.T if cfg.layout == "R" else full
-    return np.ascontiguousarray(F, dtype=np.float64)
+    if cfg.rhs == "grid" and cfg.layout == "R":
+        # C4's column sweep: system k is column k of the whole grid field
+        F = configs.grid_rhs(cfg.n, cfg.n)[:, :nr].T
+    else:
+        full = configs.host_rhs(cfg.with_(nrhs=nr))
+        F = full.T if cfg.layout == "R" else full
+    F = np.ascontiguousarray(F, dtype=np.float64)
+    assert F.shape == (nr, cfg.n), (F.shape, nr, cfg.n)
+    return F
 
 
 def cpu_reference(cfg, budget_s: float):

@@ -327,20 +327,22 @@ __global__ void __launch_bounds__(128) rs_carry_kernel(int64_t N, int p, int t0,
 }
 
 // Whole-system boundary values V = MR right + ML left (P <= kCombMaxP): CTA
-// (x, y) forms rows 8y .. 8y + 7 of V for 32 RHS; the CTA's betas and its
-// eight combination-matrix rows are staged in shared memory first (all
-// loads in flight), warp w then forms row 8y + w.
+// (x, y) forms rows 32y .. 32y + 31 of V for 32 RHS; the CTA's betas and its
+// 32 combination-matrix rows are staged in shared memory first (all loads in
+// flight), warp w then forms rows 32y + w + 8i (i < 4). Few row blocks: the
+// betas (2P x N) are read once per 32 rows of V.
+constexpr int kVmatRows = 32;
 __global__ void __launch_bounds__(256) rs_vmat_kernel(int64_t N, int64_t ld, int P, int p,
                                                       const double* __restrict__ gcmat,
                                                       const double* __restrict__ bl,
                                                       const double* __restrict__ br,
                                                       double* __restrict__ V, int64_t ldv) {
-    extern __shared__ double sbv[];  // [2P][32] betas: right_u, then left_u; [8][2P] rows
+    extern __shared__ double sbv[];  // [2P][32] betas: right_u, then left_u; [kVmatRows][2P] rows
     double* sm = sbv + 2 * P * 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t k0 = int64_t(blockIdx.x) * 32;
-    const int j0 = int(blockIdx.y) * 8;
-    const int nj = min(8, p - j0);
+    const int j0 = int(blockIdx.y) * kVmatRows;
+    const int nj = min(kVmatRows, p - j0);
     for (int i = threadIdx.x; i < nj * 2 * P; i += blockDim.x) sm[i] = gcmat[int64_t(j0) * 2 * P + i];
     pdl_trigger();
     pdl_wait();  // the folds' block betas
@@ -358,9 +360,10 @@ __global__ void __launch_bounds__(256) rs_vmat_kernel(int64_t N, int64_t ld, int
     }
     __syncthreads();
     const int64_t k = k0 + lane;
-    if (k >= N || warp >= nj) return;
+    if (k >= N) return;
     const double(*sb)[32] = reinterpret_cast<const double(*)[32]>(sbv);
-    V[int64_t(j0 + warp) * ldv + k] = cmat_row(sm + warp * 2 * P, sb, 2 * P, lane);
+    for (int jj = warp; jj < nj; jj += 8)
+        V[int64_t(j0 + jj) * ldv + k] = cmat_row(sm + jj * 2 * P, sb, 2 * P, lane);
 }
 
 // Row shards: the rank's share of every boundary value, one thread per
@@ -655,9 +658,18 @@ int launch_comb(const psw_plan* pl, int64_t N, const Work& w, cudaStream_t s, in
     ++launches;
     if (p > 0) {
         if (pl->d_cmat && P <= kCombMaxP) {
-            PSW_CUDA_TRY(launch_pdl(rs_vmat_kernel, dim3(unsigned((N + 31) / 32), unsigned((p + 7) / 8)),
-                                    dim3(256), sizeof(double) * 2 * P * 40, s, N, w.sc.ld, P, p,
-                                    pl->d_cmat, w.bl, w.br, w.V, w.ldv));
+            const size_t vsm = sizeof(double) * 2 * P * (32 + kVmatRows);
+            static std::once_flag once;
+            cudaError_t ea = cudaSuccess;
+            std::call_once(once, [&] {
+                ea = cudaFuncSetAttribute(rs_vmat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(sizeof(double) * 2 * kCombMaxP * (32 + kVmatRows)));
+            });
+            PSW_CUDA_TRY(ea);
+            PSW_CUDA_TRY(launch_pdl(rs_vmat_kernel,
+                                    dim3(unsigned((N + 31) / 32), unsigned((p + kVmatRows - 1) / kVmatRows)),
+                                    dim3(256), vsm, s, N, w.sc.ld, P, p, pl->d_cmat, w.bl, w.br, w.V,
+                                    w.ldv));
         } else {
             // the combination runs over the padded pitch (columns >= N unused)
             if (int rc = launch_combine(pl, w.bl, w.br, w.sc.ld, w.V, s)) return rc;

@@ -16,6 +16,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 rnd = sys.argv[1]
 src = os.path.join(ROOT, "gpurun_out", rnd)
+rnd = sys.argv[2] if len(sys.argv) > 2 else rnd  # output prefix
 dst = os.path.join(ROOT, "profiles")
 
 
@@ -34,8 +35,9 @@ def launches(path):
     return out
 
 
-for f in glob.glob(os.path.join(src, "bench_*.json")):
-    shutil.copy(f, os.path.join(dst, f"{rnd}_" + os.path.basename(f)))
+for f in glob.glob(os.path.join(src, "bench_*.json")) + glob.glob(os.path.join(src, "*.json")):
+    if os.path.getsize(f):
+        shutil.copy(f, os.path.join(dst, f"{rnd}_" + os.path.basename(f)))
 
 traffic_path = os.path.join(dst, "ncu_traffic.json")
 traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
@@ -57,7 +59,9 @@ for f in glob.glob(os.path.join(src, "ncu_launches_*.csv")):
     per = [{"kernel": k[1].split("(")[0][-60:], "ms": L[k].get("gpu__time_duration.sum", 0) * 1e3,
             "dram_read": L[k].get("dram__bytes_read.sum", 0),
             "dram_write": L[k].get("dram__bytes_write.sum", 0)} for k in one]
-    path = "resweep" if any("rs_part" in k[1] for k in one) else ("cluster" if any("cluster" in k[1] for k in one) else "other")
+    path = ("resweep" if any("rs_part" in k[1] for k in one) else
+            "cluster" if any("cluster" in k[1] for k in one) else
+            "fused" if any("fused" in k[1] for k in one) else "other")
     traffic[f"{cfg}:{path}"] = {"dram_bytes_per_solve": rd + wr, "dram_read": rd, "dram_write": wr,
                                 "kernels": per, "source": f"profiles/{rnd}_ncu_launches_{cfg}.csv"}
 json.dump(traffic, open(traffic_path, "w"), indent=1)
