@@ -127,18 +127,19 @@ def max_abs_diff_and_max(a, b, out=None, stream=None):
 
 
 def _is_padded(t) -> bool:
-    return t.stride(0) % 4 == 0 and (t.data_ptr() + 8 * (t.stride(0) + 1)) % 32 == 0
+    return t.stride(0) % 16 == 0 and (t.data_ptr() + 8 * (t.stride(0) + 1)) % 128 == 0
 
 
 def padded_field(n1: int, n2: int, device) -> "torch.Tensor":
     """A zero (n1+1) x (n2+1) Grid2D field whose rows have a pitch of a
-    multiple of 4 doubles and whose interior node (1, 1) sits on 32 bytes:
-    the layout-S solve of direction 2 then writes whole 32-byte sectors of
-    every line (the CLUSTER kernel's 256-bit store variant)."""
+    multiple of 16 doubles and whose interior node (1, 1) sits on 128 bytes:
+    the layout-R solve of direction 1 then writes whole 128-byte lines of
+    every grid row, and the layout-S solve of direction 2 whole 32-byte
+    sectors of every line (the CLUSTER kernel's 256-bit store variant)."""
     import torch
-    ld = (n2 + 1 + 3) // 4 * 4
-    store = torch.zeros((n1 + 1) * ld + 4, dtype=torch.float64, device=device)
-    return store.as_strided((n1 + 1, n2 + 1), (ld, 1), 3)
+    ld = (n2 + 1 + 15) // 16 * 16
+    store = torch.zeros((n1 + 1) * ld + 16, dtype=torch.float64, device=device)
+    return store.as_strided((n1 + 1, n2 + 1), (ld, 1), 15)
 
 
 class AdiIteration:
@@ -154,7 +155,7 @@ class AdiIteration:
         # right-hand sides of one half step (even pitch: 16-byte aligned rows)
         self.ldr = (n2 - 1 + 1) // 2 * 2
         self.rhs = torch.empty((n1 - 1, self.ldr), dtype=torch.float64, device=f.device)
-        self.half = torch.zeros_like(f)   # half-step field (boundary stays zero)
+        self.half = padded_field(n1, n2, f.device)  # half-step field (boundary stays zero)
         self.next = padded_field(n1, n2, f.device)
 
     def step(self, u, k: int) -> None:

@@ -22,28 +22,37 @@
 namespace psw {
 namespace {
 
+// x / d for a divisor shared by the whole grid: q = x * (1/d) refined by one
+// FMA residual step, the correctly rounded quotient except in rare ties (the
+// reference divides, adi.hpp:148-150, 165-167; an IEEE division per node is
+// what made this pass compute-bound)
+__device__ __forceinline__ double div_by(double x, double d, double r) {
+    const double q = x * r;
+    return fma(fma(-q, d, x), r, q);
+}
+
 __global__ void adi_rhs_kernel(const double* __restrict__ u, int64_t ldu,
                                const double* __restrict__ f, int64_t ldf,
                                double* __restrict__ rhs, int64_t ldr, int64_t n1, int64_t n2,
-                               double h1, double h2, double tau, int dir) {
+                               double h1, double h2, double tau, double rt, double rh, int dir) {
     const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x + 1;
     const int64_t i = int64_t(blockIdx.y) + 1;
     if (j >= n2 || i >= n1) return;
     const int64_t ld = ldu;
     const int64_t c = i * ld + j;
     const double uc = u[c];
-    double lam, hs;
+    double lam, hs;  // rt = 1 / tau, rh = 1 / h^2 of the direction (host, IEEE)
     if (dir == 1) {  // adi.hpp:148-150
-        lam = __ddiv_rn(__dadd_rn(__dsub_rn(u[c + 1], __dmul_rn(2.0, uc)), u[c - 1]),
-                        __dmul_rn(h2, h2));
+        const double hh = __dmul_rn(h2, h2);
+        lam = div_by(__dadd_rn(__dsub_rn(u[c + 1], __dmul_rn(2.0, uc)), u[c - 1]), hh, rh);
         hs = __dmul_rn(-h1, h1);
     } else {  // adi.hpp:165-167
-        lam = __ddiv_rn(__dadd_rn(__dsub_rn(u[c + ld], __dmul_rn(2.0, uc)), u[c - ld]),
-                        __dmul_rn(h1, h1));
+        const double hh = __dmul_rn(h1, h1);
+        lam = div_by(__dadd_rn(__dsub_rn(u[c + ld], __dmul_rn(2.0, uc)), u[c - ld]), hh, rh);
         hs = __dmul_rn(-h2, h2);
     }
     rhs[(i - 1) * ldr + (j - 1)] =
-        __dmul_rn(hs, __dadd_rn(__dadd_rn(__ddiv_rn(uc, tau), lam), f[i * ldf + j]));
+        __dmul_rn(hs, __dadd_rn(__dadd_rn(div_by(uc, tau, rt), lam), f[i * ldf + j]));
 }
 
 // out[0] = max |a - b|, out[1] = max |b| (non-negative doubles order like
@@ -76,7 +85,9 @@ int adi_rhs(int dir, const double* u, int64_t ldu, const double* f, int64_t ldf,
             int64_t ldr, int64_t n1, int64_t n2, double h1, double h2, double tau, cudaStream_t s) {
     if (n1 < 2 || n2 < 2) return PSW_OK;
     const dim3 grid(unsigned((n2 - 1 + 127) / 128), unsigned(n1 - 1));
-    adi_rhs_kernel<<<grid, 128, 0, s>>>(u, ldu, f, ldf, rhs, ldr, n1, n2, h1, h2, tau, dir);
+    const double hh = dir == 1 ? h2 * h2 : h1 * h1;
+    adi_rhs_kernel<<<grid, 128, 0, s>>>(u, ldu, f, ldf, rhs, ldr, n1, n2, h1, h2, tau, 1.0 / tau,
+                                        1.0 / hh, dir);
     PSW_CUDA_TRY(cudaGetLastError());
     note_launches(1);
     return PSW_OK;

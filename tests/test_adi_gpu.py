@@ -129,3 +129,29 @@ def test_large_grid_layouts_and_paths(psw, cuda):
             it.step(u, k)
         outs.append(u.cpu().numpy())
     assert _rel(outs[1], outs[0]) <= 1e-10
+
+
+def test_stencil_division_is_ieee(psw, cuda):
+    """psw_adi_rhs divides by tau and h^2 with a reciprocal and one FMA
+    residual step instead of an IEEE division per node: on a random field the
+    right-hand sides equal the reference's operation order (numpy, IEEE
+    division) bitwise."""
+    import numpy as np
+    from paper_0901_2859_b200.adi import _adi_rhs
+    rng = np.random.default_rng(5)
+    n1, n2, h1, h2, tau = 130, 97, 1 / 130, 1 / 97, 0.0123
+    u = rng.standard_normal((n1 + 1, n2 + 1))
+    f = rng.standard_normal((n1 + 1, n2 + 1))
+    for d in (1, 2):
+        rhs = cuda.empty((n1 - 1, n2 - 1), dtype=cuda.float64, device="cuda")
+        _adi_rhs(d, cuda.from_numpy(u).cuda(), cuda.from_numpy(f).cuda(), rhs, n2 - 1, n1, n2, h1, h2,
+                 tau, 0)
+        c = u[1:n1, 1:n2]
+        if d == 1:
+            lam = ((u[1:n1, 2:] - 2.0 * c) + u[1:n1, :n2 - 1]) / (h2 * h2)
+            hs = -h1 * h1
+        else:
+            lam = ((u[2:, 1:n2] - 2.0 * c) + u[:n1 - 1, 1:n2]) / (h1 * h1)
+            hs = -h2 * h2
+        want = hs * ((c / tau + lam) + f[1:n1, 1:n2])
+        assert np.array_equal(rhs.cpu().numpy(), want)
