@@ -104,3 +104,34 @@ def test_resweep_c3_full(psw, cuda):
     R[:-1] += ad[:, None] * X[1:]
     res = ((R - F).norm(dim=0) / F.norm(dim=0)).max()
     assert float(res) <= 1e-13
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_resweep_tma_random_partitions(psw, cuda, seed):
+    """The TMA-pipelined RESWEEP kernels (layout R, N >= one 256-byte chunk,
+    16-byte row pitch) on random partitions: groups straddling several blocks
+    (several runs per group, closed-form carries per run), short segments
+    (the register fallback when a segment cannot lend its exchange rows),
+    ragged last chunks and padded pitches; fp64 and fp32 against the oracle."""
+    from oracle.pyoracle import Oracle
+    rng = np.random.default_rng(7000 + seed)
+    n = int(rng.integers(300, 6000))
+    P = int(rng.integers(2, min(120, n // 3)))
+    if seed % 3 == 0:
+        bnd = psw.decompose(n, P).induced_partition().boundaries
+    else:
+        bnd = sorted(rng.choice(np.arange(2, n), size=P - 1, replace=False).tolist())
+    sub = -rng.uniform(0.2, 1.0, n - 1)
+    diag = np.r_[0, np.abs(sub)] + np.r_[np.abs(sub), 0] + rng.uniform(0.1, 1.0, n)
+    f32 = seed % 4 == 3
+    plan = psw.Plan(psw.TridiagMatrix(sub, diag, sub), psw.Partition(n, bnd),
+                    dtype=psw.F32 if f32 else psw.F64)
+    N = int(rng.integers(64, 400))
+    F = rng.uniform(-1, 1, (N, n))
+    if f32:
+        F = F.astype(np.float32).astype(np.float64)
+    want = Oracle().solve_batch_threads(sub, diag, sub, np.array(bnd, np.int64), F, 8)[0]
+    pad = int(rng.integers(0, 3)) * (4 if f32 else 2)  # keeps 16-byte row pitches
+    X = gpu_solve(psw, cuda, plan, F, 0, path=psw.PATH_RESWEEP, inplace=bool(seed % 2), pad=pad)
+    tol = FP32_TOL if f32 else FP64_TOL
+    assert rel_l2(X, want) <= tol, (seed, n, P, N, f32, rel_l2(X, want))
