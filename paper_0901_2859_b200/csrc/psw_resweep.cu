@@ -327,27 +327,34 @@ __global__ void __launch_bounds__(128) rs_carry_kernel(int64_t N, int p, int t0,
 }
 
 // Whole-system boundary values V = MR right + ML left (P <= kCombMaxP): CTA
-// (x, y) forms rows 32y .. 32y + 31 of V for 32 RHS; the CTA's betas and its
+// (x, y) forms rows 32y .. 32y + 31 of V for 64 RHS. The CTA's betas and its
 // 32 combination-matrix rows are staged in shared memory first (all loads in
-// flight), warp w then forms rows 32y + w + 8i (i < 4). Few row blocks: the
-// betas (2P x N) are read once per 32 rows of V.
+// flight); warp w then forms rows 32y + 4w .. 32y + 4w + 3 for RHS k0 + lane
+// and k0 + 32 + lane, each beta loaded once for the warp's four rows and each
+// matrix quadruple (one broadcast 32-byte load) once for its two RHS: 16
+// shared loads per 32 FMAs (cmat_row's one per FMA made the kernel
+// shared-load bound, 266 us on C2). Every V entry is summed exactly as
+// cmat_row sums it (four interleaved partial sums over u, (a0 + a1) + (a2 + a3)).
 constexpr int kVmatRows = 32;
+constexpr int kVmatRhs = 64;
 __global__ void __launch_bounds__(256) rs_vmat_kernel(int64_t N, int64_t ld, int P, int p,
                                                       const double* __restrict__ gcmat,
                                                       const double* __restrict__ bl,
                                                       const double* __restrict__ br,
                                                       double* __restrict__ V, int64_t ldv) {
-    extern __shared__ double sbv[];  // [2P][32] betas: right_u, then left_u; [kVmatRows][2P] rows
-    double* sm = sbv + 2 * P * 32;
+    extern __shared__ __align__(16) double sbv[];  // [2P][64] betas: right_u, left_u; [32][2P] rows
+    double* sm = sbv + 2 * P * kVmatRhs;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t k0 = int64_t(blockIdx.x) * 32;
+    const int64_t k0 = int64_t(blockIdx.x) * kVmatRhs;
     const int j0 = int(blockIdx.y) * kVmatRows;
     const int nj = min(kVmatRows, p - j0);
-    for (int i = threadIdx.x; i < nj * 2 * P; i += blockDim.x) sm[i] = gcmat[int64_t(j0) * 2 * P + i];
+    const int len = 2 * P;
+    for (int i = threadIdx.x; i < kVmatRows * len; i += blockDim.x)
+        sm[i] = i < nj * len ? gcmat[int64_t(j0) * len + i] : 0.0;
     pdl_trigger();
     pdl_wait();  // the folds' block betas
-    for (int i = threadIdx.x; i < 2 * P * 32; i += blockDim.x) {
-        const int u = i >> 5, l = i & 31;
+    for (int i = threadIdx.x; i < len * kVmatRhs; i += blockDim.x) {
+        const int u = i / kVmatRhs, l = i % kVmatRhs;
         const int64_t k = k0 + l;
         double v = 0.0;
         if (k < N) {
@@ -359,11 +366,52 @@ __global__ void __launch_bounds__(256) rs_vmat_kernel(int64_t N, int64_t ld, int
         sbv[i] = v;
     }
     __syncthreads();
-    const int64_t k = k0 + lane;
-    if (k >= N) return;
-    const double(*sb)[32] = reinterpret_cast<const double(*)[32]>(sbv);
-    for (int jj = warp; jj < nj; jj += 8)
-        V[int64_t(j0 + jj) * ldv + k] = cmat_row(sm + jj * 2 * P, sb, 2 * P, lane);
+    double acc[4][2][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[r][c][q] = 0.0;
+    const double* mrow = sm + (4 * warp) * len;
+    int u = 0;
+    for (; u + 4 <= len; u += 4) {
+        double b[2][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            b[0][q] = sbv[(u + q) * kVmatRhs + lane];
+            b[1][q] = sbv[(u + q) * kVmatRhs + 32 + lane];
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const double2 m01 = *reinterpret_cast<const double2*>(mrow + r * len + u);
+            const double2 m23 = *reinterpret_cast<const double2*>(mrow + r * len + u + 2);
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                acc[r][c][0] = fma(m01.x, b[c][0], acc[r][c][0]);
+                acc[r][c][1] = fma(m01.y, b[c][1], acc[r][c][1]);
+                acc[r][c][2] = fma(m23.x, b[c][2], acc[r][c][2]);
+                acc[r][c][3] = fma(m23.y, b[c][3], acc[r][c][3]);
+            }
+        }
+    }
+    for (; u < len; ++u)  // len % 4 == 2 (odd P): the tail into the first partial sum
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+                acc[r][c][0] = fma(mrow[r * len + u], sbv[u * kVmatRhs + 32 * c + lane], acc[r][c][0]);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int jj = 4 * warp + r;
+        if (jj >= nj) break;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const int64_t k = k0 + 32 * c + lane;
+            if (k < N)
+                V[int64_t(j0 + jj) * ldv + k] = (acc[r][c][0] + acc[r][c][1]) + (acc[r][c][2] + acc[r][c][3]);
+        }
+    }
 }
 
 // Row shards: the rank's share of every boundary value, one thread per
@@ -658,16 +706,17 @@ int launch_comb(const psw_plan* pl, int64_t N, const Work& w, cudaStream_t s, in
     ++launches;
     if (p > 0) {
         if (pl->d_cmat && P <= kCombMaxP) {
-            const size_t vsm = sizeof(double) * 2 * P * (32 + kVmatRows);
+            const size_t vsm = sizeof(double) * 2 * P * (kVmatRhs + kVmatRows);
             static std::once_flag once;
             cudaError_t ea = cudaSuccess;
             std::call_once(once, [&] {
                 ea = cudaFuncSetAttribute(rs_vmat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          int(sizeof(double) * 2 * kCombMaxP * (32 + kVmatRows)));
+                                          int(sizeof(double) * 2 * kCombMaxP * (kVmatRhs + kVmatRows)));
             });
             PSW_CUDA_TRY(ea);
             PSW_CUDA_TRY(launch_pdl(rs_vmat_kernel,
-                                    dim3(unsigned((N + 31) / 32), unsigned((p + kVmatRows - 1) / kVmatRows)),
+                                    dim3(unsigned((N + kVmatRhs - 1) / kVmatRhs),
+                                         unsigned((p + kVmatRows - 1) / kVmatRows)),
                                     dim3(256), vsm, s, N, w.sc.ld, P, p, pl->d_cmat, w.bl, w.br, w.V,
                                     w.ldv));
         } else {
