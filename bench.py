@@ -654,9 +654,45 @@ def _e2e(psw, plan, solver, cfg, F, layout, dt, args, dist, dev):
         t = torch.tensor([el], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         el = float(t.item())
-    return {"value": cfg.nrhs * cfg.n * steps / el, "unit": "unknowns/s",
-            "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": steps,
-            "ms_per_step": 1e3 * el / steps, "api": api}
+    out = {"value": cfg.nrhs * cfg.n * steps / el, "unit": "unknowns/s",
+           "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": steps,
+           "ms_per_step": 1e3 * el / steps, "api": api}
+    if solver is None:
+        out["link"] = _link_floor(Fh, Xh, 1e3 * el / steps)
+    return out
+
+
+def _link_floor(Fh, Xh, e2e_ms):
+    """The host link's own bound for the step's traffic: the same bytes as
+    one contiguous H2D and one contiguous D2H, on two streams at once (the
+    most a pipelined solve can overlap); e2e is at `frac` of it."""
+    import torch
+    dev_a = torch.empty(Fh.shape, dtype=Fh.dtype, device="cuda")
+    dev_b = torch.empty_like(dev_a)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def both():
+        with torch.cuda.stream(s1):
+            dev_a.copy_(Fh, non_blocking=True)
+        with torch.cuda.stream(s2):
+            Xh.copy_(dev_b, non_blocking=True)
+
+    best = None
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        both()
+        torch.cuda.synchronize()
+        el = (time.perf_counter() - t) * 1e3
+        best = el if best is None else min(best, el)
+    del dev_a, dev_b
+    torch.cuda.empty_cache()
+    nb = Fh.numel() * Fh.element_size()
+    return {"both_directions_ms": best, "aggregate_gbs": 2 * nb / best / 1e6,
+            "frac": best / e2e_ms,
+            "note": "F's bytes H2D and X's bytes D2H as two concurrent contiguous copies "
+                    "(pinned); the solve itself adds the first chunk's upload and the last "
+                    "chunk's download, which cannot overlap anything"}
 
 
 if __name__ == "__main__":

@@ -99,7 +99,11 @@ extern "C" int psw_solve_host(const psw_plan* plan, const void* F, int64_t ldf, 
         // a layout-R chunk is a pitched copy of c * es bytes per row: keep
         // rows >= 2 KB (narrower DMA rows crawl: 16-256 B rows ran at 2-16
         // GB/s on the 2^20-row and fp32 configs), even if chunks get large
-        c = std::max<int64_t>(c, int64_t(2048 / es));
+        static const int64_t min_row = [] {  // PSW_HOST_MIN_ROW: tuning override (bytes)
+            const char* e = std::getenv("PSW_HOST_MIN_ROW");
+            return e && std::atoll(e) > 0 ? int64_t(std::atoll(e)) : int64_t(2048);
+        }();
+        c = std::max<int64_t>(c, min_row / int64_t(es));
         if (c >= 32) c = c / 32 * 32;
     }
     c = std::min(c, nrhs);
