@@ -33,7 +33,7 @@ __all__ = [
     "TridiagMatrix", "Partition", "Decomposition", "decompose", "compute_preliminary", "Plan",
     "solve_batch", "solve_multi", "MultiPlan", "SolverError", "PivotBreakdown", "TooManyPEs", "NotSupported", "NotSymmetrizable", "OracleFallbackRequired", "CudaError",
     "F64", "F32", "LAYOUT_R", "LAYOUT_S", "PATH_AUTO", "PATH_STAGED", "PATH_FUSED", "PATH_CHUNKED",
-    "PATH_RESWEEP", "PATH_CLUSTER", "last_path", "lib", "library_path", "Comm", "NcclError",
+    "PATH_RESWEEP", "PATH_CLUSTER", "PATH_HOLD", "last_path", "lib", "library_path", "Comm", "NcclError",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -44,6 +44,7 @@ if os.environ.get("PSW_LIB_VARIANT"):  # experiments: _lib/<variant>/ built with
 F64, F32 = 0, 1
 LAYOUT_R, LAYOUT_S = 0, 1
 PATH_AUTO, PATH_STAGED, PATH_FUSED, PATH_CHUNKED, PATH_RESWEEP, PATH_CLUSTER = 0, 1, 2, 5, 6, 7
+PATH_HOLD = 8
 OK, INVALID_ARGUMENT, PIVOT_BREAKDOWN, TOO_MANY_PES, NOT_SUPPORTED, CUDA_ERROR, NCCL_ERROR, OOM = range(8)
 NOT_SYMMETRIZABLE, ORACLE_FALLBACK_REQUIRED = 8, 9
 # GRowStrategy (dichotomy/preliminary.hpp:18-24)
@@ -189,7 +190,7 @@ def last_launch_count() -> int:
 
 
 PATH_NAMES = {PATH_STAGED: "staged", PATH_FUSED: "fused", PATH_CHUNKED: "chunked",
-              PATH_RESWEEP: "resweep", PATH_CLUSTER: "cluster"}
+              PATH_RESWEEP: "resweep", PATH_CLUSTER: "cluster", PATH_HOLD: "hold"}
 
 
 def last_path() -> str:

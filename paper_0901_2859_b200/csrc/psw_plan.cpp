@@ -11,6 +11,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -325,7 +326,8 @@ void free_plan(psw_plan* pl) {
                     pl->d_lvl_off, pl->d_ffwd, pl->d_fbwd, pl->d_seg, pl->d_cmat,
                     pl->d_segdesc, pl->d_segoff, pl->d_ctab[0], pl->d_ctab[1],
                     pl->d_rs_group, pl->d_rs_run, pl->d_rs_runcoef, pl->d_rs_runoff,
-                    pl->d_scoef, pl->d_rs_cw};
+                    pl->d_scoef, pl->d_rs_cw, pl->d_hd_cta, pl->d_hd_run, pl->d_hd_runcoef,
+                    pl->d_hd_runoff, pl->d_hd_coef};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     cudaSetDevice(prev);
@@ -755,14 +757,19 @@ cudaError_t scratch_free(void* p, cudaStream_t s) { return cudaFreeAsync(p, s); 
 
 int auto_path(const psw_plan* pl, const void* F, int64_t ldf, const void* X, int64_t ldx,
               int64_t N, int layout) {
-    (void)X;
-    (void)ldx;
     const int64_t es = pl->dtype == PSW_F64 ? 8 : 4;
     if (N * es >= 128 * 128 && cluster_supported(pl, layout, N, F, ldf)) return PSW_PATH_CLUSTER;
     if (fused_supported(pl, layout, N, F, ldf)) return PSW_PATH_FUSED;
     // CHUNKED (RESWEEP over L2-sized RHS chunks) is explicit only: on the fp32
     // config its per-chunk launches cost more than the re-read they save
     // (27 vs 10.2 ms, round 2)
+    // HOLD: one RHS tile of all rows held by the whole grid (fp32, F read once)
+    static const int hold_min = [] {
+        const char* e = std::getenv("PSW_HOLD_MIN_ROWS");
+        return e ? std::atoi(e) : 16384;
+    }();
+    if (pl->n >= hold_min && N >= 256 && hold_supported(pl, layout, N, F, ldf, X, ldx))
+        return PSW_PATH_HOLD;
     if (resweep_supported(pl, layout, N)) return PSW_PATH_RESWEEP;
     return PSW_PATH_STAGED;
 }
@@ -921,6 +928,10 @@ int psw_solve_ex(const psw_plan* plan, const void* F, int64_t ldf, void* X, int6
         rc = psw::resweep_supported(plan, layout, nrhs)
                  ? psw::solve_resweep(plan, F, ldf, X, ldx, nrhs, layout, s, ev, nev)
                  : unsupported("resweep");
+    } else if (path == PSW_PATH_HOLD) {
+        rc = psw::hold_supported(plan, layout, nrhs, F, ldf, X, ldx)
+                 ? psw::solve_hold(plan, F, ldf, X, ldx, nrhs, layout, s, ev, nev)
+                 : unsupported("hold");
     } else if (path == PSW_PATH_FUSED) {
         rc = psw::fused_supported(plan, layout, nrhs, F, ldf)
                  ? psw::solve_fused(plan, F, ldf, X, ldx, nrhs, layout, s, ev, nev)
