@@ -763,12 +763,18 @@ int auto_path(const psw_plan* pl, const void* F, int64_t ldf, const void* X, int
     // CHUNKED (RESWEEP over L2-sized RHS chunks) is explicit only: on the fp32
     // config its per-chunk launches cost more than the re-read they save
     // (27 vs 10.2 ms, round 2)
-    // HOLD: one RHS tile of all rows held by the whole grid (fp32, F read once)
+    // HOLD (one RHS tile of all rows held by the whole grid, fp32, F read once)
+    // is explicit only: 26.9 ms on C2 against RESWEEP's 9.4 ms (its in-order
+    // exchange warps bound the tile rate). PSW_HOLD_AUTO=1
+    // lets AUTO take it for systems of at least PSW_HOLD_MIN_ROWS rows.
     static const int hold_min = [] {
+        const char* a = std::getenv("PSW_HOLD_AUTO");
+        if (!a || std::atoi(a) == 0) return -1;
         const char* e = std::getenv("PSW_HOLD_MIN_ROWS");
         return e ? std::atoi(e) : 16384;
     }();
-    if (pl->n >= hold_min && N >= 256 && hold_supported(pl, layout, N, F, ldf, X, ldx))
+    if (hold_min >= 0 && pl->n >= hold_min && N >= 256 &&
+        hold_supported(pl, layout, N, F, ldf, X, ldx))
         return PSW_PATH_HOLD;
     if (resweep_supported(pl, layout, N)) return PSW_PATH_RESWEEP;
     return PSW_PATH_STAGED;

@@ -87,8 +87,8 @@ def test_hold_random_partitions(psw, cuda, seed):
 
 def test_hold_c2_shape(psw, cuda):
     """The fp32 config's system (n = 65536, P = 64, 14 segments per CTA, three
-    tiles in flight) with 4096 RHS: AUTO takes HOLD; a seeded RHS subset
-    against the oracle, every RHS through the device residual, two runs
+    tiles in flight) with 4096 RHS: HOLD is explicit only (AUTO keeps RESWEEP,
+    which is faster there); a seeded RHS subset against the oracle, every RHS through the device residual, two runs
     bitwise equal."""
     from oracle.pyoracle import Oracle
     from paper_0901_2859_b200.configs import CONFIGS
@@ -102,6 +102,8 @@ def test_hold_c2_shape(psw, cuda):
     psw.fill_uniform(F, 5, -1.0, 1.0)
     X = cuda.empty_like(F)
     plan.solve(F, X)
+    assert psw.last_path() == "resweep"
+    plan.solve(F, X, path=psw.PATH_HOLD)
     assert psw.last_path() == "hold"
     cuda.cuda.synchronize()
     X2 = cuda.empty_like(F)
