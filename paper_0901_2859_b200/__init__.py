@@ -572,6 +572,33 @@ def compute_preliminary(A: TridiagMatrix, part: Partition, dtype: int = F64, dev
     return Plan(A, part, dtype=dtype, device=device)
 
 
+def debug_preliminary(A: TridiagMatrix, part: Partition) -> dict:
+    """Test hook (psw_debug_preliminary): the raw tables of the preliminary as
+    plan creation produced them (host sweeps or the device kernels of
+    psw_prelim.cu, by PSW_DEVICE_SETUP): gr / gl (g_j on blocks j / j+1),
+    zr / zl (p x p samples), max_z, device_setup."""
+    n, p = A.n(), part.p()
+    dp = C.POINTER(C.c_double)
+    L = lib()
+    L.psw_debug_preliminary.restype = C.c_int
+    L.psw_debug_preliminary.argtypes = [C.c_int64, dp, dp, dp, C.c_int64, C.POINTER(C.c_int64),
+                                        dp, dp, dp, dp, dp, C.POINTER(C.c_int32)]
+    sub = np.ascontiguousarray(A.sub, dtype=np.float64)
+    diag = np.ascontiguousarray(A.diag, dtype=np.float64)
+    sup = np.ascontiguousarray(A.super, dtype=np.float64)
+    bnd = np.ascontiguousarray(part.boundaries, dtype=np.int64)
+    gr, gl = np.zeros(n), np.zeros(n)
+    zr, zl = np.zeros((max(p, 1), max(p, 1))), np.zeros((max(p, 1), max(p, 1)))
+    mz, ds = C.c_double(0.0), C.c_int32(0)
+    _check(L.psw_debug_preliminary(n, sub.ctypes.data_as(dp), diag.ctypes.data_as(dp),
+                                   sup.ctypes.data_as(dp), p, bnd.ctypes.data_as(C.POINTER(C.c_int64)),
+                                   gr.ctypes.data_as(dp), gl.ctypes.data_as(dp),
+                                   zr.ctypes.data_as(dp), zl.ctypes.data_as(dp), C.byref(mz),
+                                   C.byref(ds)))
+    return {"gr": gr, "gl": gl, "zr": zr[:p, :p] if p else zr[:0, :0],
+            "zl": zl[:p, :p] if p else zl[:0, :0], "max_z": mz.value, "device_setup": ds.value}
+
+
 def solve_batch(A: TridiagMatrix, part: Partition, rhs_series: Sequence[Sequence[float]],
                 dtype: int = F64, device: int = 0) -> list[np.ndarray]:
     """dichotomy/batch.hpp:57-75 on host data: validate, preliminary once,

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -375,16 +376,35 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
 int device_preliminary(int64_t n, const double* sub, const double* diag, const double* sup,
                        int64_t p, const int64_t* bnd, const std::vector<int32_t>& blk,
                        std::vector<double>& gr, std::vector<double>& gl, std::vector<double>& zr,
-                       std::vector<double>& zl, double& max_z, int64_t& bad_row);  // psw_prelim.cu
+                       std::vector<double>& zl, double& max_z, int64_t& bad_row, int* serial);
 
-// Where the DirectSymmetric preliminary runs: PSW_DEVICE_SETUP=1 moves the
-// 3p boundary sweeps to the GPU (psw_prelim.cu, bitwise the host setup). The
-// default is the host: the sweeps are single-thread recurrences through an
-// IEEE division per row, and on B200 they run slower than the host's worker
-// threads (C3: 3.3 s vs 0.3 s; tests/test_prelim_gpu.py).
-static bool want_device_setup(int64_t n, int64_t p) {
+// Where the DirectSymmetric preliminary runs: on the GPU (psw_prelim.cu,
+// bitwise the host setup) whenever a device is there and the 3p sweeps are
+// long enough to pay for its allocation, copies and launches (about 2 ms;
+// PSW_DEVICE_SETUP_MIN, default 3 p n >= 2^21 row steps: C2 8.5 -> 1.9 ms, C3
+// 202 -> 12 ms, while a 4096-row system takes 0.4 ms on the host against 2 ms;
+// tools/setup_bench.py); PSW_DEVICE_SETUP=0 keeps the host's worker
+// threads, =1 forces the device. Without a device the host path runs, so that
+// validation and PivotBreakdown are still reported before the missing device.
+// test hook (psw_debug_preliminary): the raw tables of the preliminary
+struct PrelimCapture {
+    std::vector<double> gr, gl, zr, zl;
+};
+static thread_local PrelimCapture* t_capture = nullptr;
+
+static bool want_device_setup(int64_t n, int64_t p, int device) {
+    if (p <= 0 || n <= 0) return false;
     const char* e = std::getenv("PSW_DEVICE_SETUP");
-    return p > 0 && n > 0 && e && std::atoi(e) != 0;
+    if (e && *e && std::atoi(e) == 0) return false;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return false;
+    }
+    if (e && *e) return true;
+    const char* m = std::getenv("PSW_DEVICE_SETUP_MIN");
+    const int64_t min_steps = m && *m ? std::atoll(m) : (int64_t{1} << 21);
+    return 3 * p * n >= min_steps;
 }
 
 int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
@@ -468,20 +488,18 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
             delete pl;
             return PSW_PIVOT_BREAKDOWN;
         }
-    } else if (grow.strategy == PSW_GROW_DIRECT_SYMMETRIC && want_device_setup(n, p)) {
+    }
+    bool host_sweeps = p > 0;
+    if (p > 0 && !cmat_host && grow.strategy == PSW_GROW_DIRECT_SYMMETRIC &&
+        want_device_setup(n, p, device)) {
         // the 3p sweeps on the GPU, bitwise the host restatement (psw_prelim.cu)
-        int ndev = 0;
-        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0 || device < 0 || device >= ndev) {
-            set_error(PSW_CUDA_ERROR, "no CUDA device for the device preliminary (no CPU fallback)");
-            delete pl;
-            return PSW_CUDA_ERROR;
-        }
         int prev_dev = 0;
         cudaGetDevice(&prev_dev);
         cudaSetDevice(device);
         int64_t bad = -1;
+        int serial = 0;
         const int rc = device_preliminary(n, sub, diag, sup, p, bnd, pl->blk, gr, gl, zr, zl, max_z,
-                                          bad);
+                                          bad, &serial);
         cudaSetDevice(prev_dev);
         if (rc == PSW_PIVOT_BREAKDOWN) {
             set_error(PSW_PIVOT_BREAKDOWN,
@@ -490,12 +508,21 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
             delete pl;
             return PSW_PIVOT_BREAKDOWN;
         }
-        if (rc != PSW_OK) {
-            delete pl;
+        if (rc == PSW_OK) {
+            pl->info.device_setup = serial ? 2 : 1;
+            host_sweeps = false;
+        } else if (rc != PSW_NOT_SUPPORTED) {  // NOT_SUPPORTED: a chain outgrew the device
+            delete pl;                         // scratch window, the host does the sweeps
             return rc;
+        } else {
+            clear_error();
+            gr.assign(n, 0.0);
+            gl.assign(n, 0.0);
+            zr.assign(p * p, 0.0);
+            zl.assign(p * p, 0.0);
         }
-        pl->info.device_setup = 1;
-    } else {
+    }
+    if (host_sweeps) {
         // boundaries are independent items (preliminary.hpp:182-195); errors
         // are reported in the serial executor's order (boundary, then g,
         // z_left, z_right).
@@ -576,6 +603,13 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
         }
     }
 
+    const auto t_prelim = std::chrono::steady_clock::now();
+    if (t_capture) {
+        t_capture->gr = gr;
+        t_capture->gl = gl;
+        t_capture->zr = zr;
+        t_capture->zl = zl;
+    }
     // ---- per-row sweep coefficients of every block (local_solve.hpp:25-50)
     std::vector<double> rp(n, 0.0), ma(n, 0.0), w(n, 0.0), alv(n, 0.0);
     for (int64_t t = 0; t <= p; ++t) {
@@ -607,6 +641,7 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
             alpha_prev = a;
         }
     }
+    const auto t_coef = std::chrono::steady_clock::now();
     int64_t terms = 0;
     pl->items = build_items(p, &terms, &pl->lvl_off);
     if (cmat_host) {
@@ -637,6 +672,7 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
     }
     int rc = (dtype == PSW_F64) ? upload<double>(pl, rp, ma, gr, gl, w, alv, zr, zl)
                                 : upload<float>(pl, rp, ma, gr, gl, w, alv, zr, zl);
+    const auto t_upload = std::chrono::steady_clock::now();
     // PSW_PLAN_STAGED_ONLY: no segment tables (FUSED / CLUSTER / RESWEEP
     // unsupported, STAGED and the multi-matrix solve only) — a cheap plan for
     // the many one-RHS systems of the Fourier consumer
@@ -650,6 +686,16 @@ int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag,
         return rc;
     }
     const auto t1 = std::chrono::steady_clock::now();
+    if (const char* v = std::getenv("PSW_SETUP_VERBOSE"); v && std::atoi(v)) {
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        std::fprintf(stderr,
+                     "psw setup n=%lld p=%lld: preliminary %.3f ms (%s), block coefficients %.3f ms, "
+                     "upload %.3f ms, tables %.3f ms, total %.3f ms\n",
+                     (long long)n, (long long)p, ms(t0, t_prelim),
+                     pl->info.device_setup ? (pl->info.device_setup == 2 ? "device, serial chain" : "device")
+                                           : "host",
+                     ms(t_prelim, t_coef), ms(t_coef, t_upload), ms(t_upload, t1), ms(t0, t1));
+    }
     auto& in = pl->info;
     in.n = n;
     in.p = p;
@@ -992,6 +1038,31 @@ extern "C" int psw_combine_matrix(int64_t n, const double* sub, const double* di
     const int rc = psw::build_plan(&dummy, n, sub, diag, sup, p, boundaries, PSW_F64, 0, 0, 1, &M);
     if (rc == PSW_OK && out) std::copy(M.begin(), M.end(), out);
     return rc;
+}
+
+// Test hook: the preliminary's tables as build_plan produced them (host
+// sweeps or psw_prelim.cu, by PSW_DEVICE_SETUP), so that tests can compare
+// bit patterns: gr/gl (n each: g_j on blocks j / j+1), zr/zl (p x p), max |z|
+// and the plan's device_setup flag.
+extern "C" int psw_debug_preliminary(int64_t n, const double* sub, const double* diag,
+                                     const double* sup, int64_t p, const int64_t* boundaries,
+                                     double* gr, double* gl, double* zr, double* zl,
+                                     double* max_z, int32_t* device_setup) {
+    psw::PrelimCapture cap;
+    psw::t_capture = &cap;
+    psw_plan* pl = nullptr;
+    const int rc = psw::build_plan(&pl, n, sub, diag, sup, p, boundaries, PSW_F64, 0, 0, 1, nullptr,
+                                   false, PSW_GROW_AUTO, PSW_PLAN_STAGED_ONLY);
+    psw::t_capture = nullptr;
+    if (rc != PSW_OK) return rc;
+    std::copy(cap.gr.begin(), cap.gr.end(), gr);
+    std::copy(cap.gl.begin(), cap.gl.end(), gl);
+    std::copy(cap.zr.begin(), cap.zr.end(), zr);
+    std::copy(cap.zl.begin(), cap.zl.end(), zl);
+    if (max_z) *max_z = pl->info.max_z_norm;
+    if (device_setup) *device_setup = pl->info.device_setup;
+    psw::destroy_plan(pl);
+    return PSW_OK;
 }
 
 extern "C" int psw_debug_trace(void* device_buffer) {
