@@ -192,6 +192,87 @@ __device__ __forceinline__ void bwd_v4(const unsigned char* co, int a, int len,
     }
 }
 
+// 4 x 4 transpose of 32-byte chunks among the four lanes 4g .. 4g+3: lane a
+// enters with chunks c[0..3] (16 consecutive rows) of its own right-hand
+// side and leaves with chunk a of the right-hand sides of lanes 4g + s in
+// c[s] (two butterfly stages, selects with compile-time register indices).
+__device__ __forceinline__ void chunk_transpose4(double (&c)[4][4], int lane) {
+    const bool a1 = lane & 2, a0 = lane & 1;
+#pragma unroll
+    for (int s0 = 0; s0 < 2; ++s0)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const double send = a1 ? c[s0][e] : c[s0 + 2][e];
+            const double recv = __shfl_xor_sync(0xffffffffu, send, 2);
+            if (a1) c[s0][e] = recv; else c[s0 + 2][e] = recv;
+        }
+#pragma unroll
+    for (int s0 = 0; s0 < 4; s0 += 2)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const double send = a0 ? c[s0][e] : c[s0 + 1][e];
+            const double recv = __shfl_xor_sync(0xffffffffu, send, 1);
+            if (a0) c[s0][e] = recv; else c[s0 + 1][e] = recv;
+        }
+}
+
+// Layout S backward with whole-line stores (fp64): as bwd_v4, but the four
+// lanes of a group exchange their 32-byte chunks first, so that a group's
+// store instruction writes 128 contiguous bytes (16 rows) of ONE right-hand
+// side instead of four separate sectors: a warp store touches 8 lines, not
+// 32. The arithmetic and the values are bwd_v4's. Every lane of the warp
+// runs it (shuffles); `kk0` = the group's first right-hand side, stores to
+// right-hand sides >= N are dropped. ga = the segment's first global row.
+template <int AL>
+__device__ __forceinline__ void bwd_v4t(const unsigned char* co, int a, int len,
+                                        double (&dr)[kSegMax], double D, double xl, double xn,
+                                        double* X, int64_t ldx, int64_t kk, int64_t N, int ga,
+                                        int lane) {
+    const unsigned char* cb = co + coff<double>(a);
+#pragma unroll
+    for (int r = kSegMax - 1; r >= 0; --r) {
+        if (r < kSegLen - 1 || r < len) {
+            const Quad<double> c1 = reinterpret_cast<const Quad<double>*>(crow<double, AL == 0 ? 1 : 0>(co, cb, a, r))[1];
+            xn = fma(c1.w, xn, fma(xl, c1.z, fma(c1.y, D, dr[r])));
+            dr[r] = xn;
+        } else {
+            dr[r] = 0.0;
+        }
+    }
+    constexpr int o0 = AL == 0 ? 0 : 1;  // first row of the first whole line
+    const int aa = lane & 3;
+    const int64_t k0 = kk - aa;
+    if constexpr (AL == 3)
+        if (kk < N) __stcs(X + kk * ldx + ga, dr[0]);
+    if constexpr (o0 + 32 < kSegMax)
+        if (kk < N && len > o0 + 32) __stcs(X + kk * ldx + ga + o0 + 32, dr[o0 + 32]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        double c[4][4];
+#pragma unroll
+        for (int s = 0; s < 4; ++s)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) c[s][e] = dr[o0 + 16 * h + 4 * s + e];
+        chunk_transpose4(c, lane);
+        // rows of this lane's chunk that exist (the segment may end inside it)
+        const int nt = len - (o0 + 16 * h + 4 * aa);
+        double* xp = X + k0 * ldx + ga + o0 + 16 * h + 4 * aa;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            double* q = xp + int64_t(s) * ldx;
+            if (k0 + s < N) {
+                if (nt >= 4) {
+                    st_v4(q, c[s][0], c[s][1], c[s][2], c[s][3]);
+                } else {
+                    if (nt >= 2) st_v2(q, c[s][0], c[s][1]);
+                    if (nt == 1) __stcs(q, c[s][0]);
+                    if (nt == 3) __stcs(q + 2, c[s][2]);
+                }
+            }
+        }
+    }
+}
+
 template <typename T, int W, int NMAX, bool EXACT = (NMAX <= kSegLen), bool LS = false, int DL = 0,
           int AC = -1>
 __device__ __forceinline__ void fwd(const T* slab, const unsigned char* co, int a, int lane,
@@ -272,7 +353,7 @@ __device__ __forceinline__ void bwd(const unsigned char* co, int a, int len,
     }
 }
 
-template <typename T, int W, int NSLAB, bool LS = false, bool V4 = false>
+template <typename T, int W, int NSLAB, bool LS = false, int V4 = 0>
 __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
     const __grid_constant__ CUtensorMap tmF, const __grid_constant__ CUtensorMap tmF1,
     const __grid_constant__ CUtensorMap tmF2, const T* F, int64_t ldf, T* X, CGeom g, const FusedFwd<T>* __restrict__ gff, const FusedBwd<T>* __restrict__ gfb,
@@ -540,8 +621,14 @@ __global__ void __launch_bounds__(kMaxThreads / NSLAB) cluster_kernel(
             // mod 4, choose_t). One store variant per instantiation: a third
             // one drives ptxas to 64 registers and 0.8 KB of spills (171 vs
             // 110 us on C4).
-            if (kk < g.N) {
-                if constexpr (V4) {
+            if constexpr (V4 == 2) {  // whole-line stores: the warp's lanes exchange chunks
+                double* xb = reinterpret_cast<double*>(X);
+                if ((sgd.a & 3) == 0)
+                    bwd_v4t<0>(co, a, len, dr, D, xlt, xn, xb, g.ldx, kk, g.N, sgd.a, lane);
+                else
+                    bwd_v4t<3>(co, a, len, dr, D, xlt, xn, xb, g.ldx, kk, g.N, sgd.a, lane);
+            } else if (kk < g.N) {
+                if constexpr (V4 == 1) {
                     double* xp = reinterpret_cast<double*>(X) + kk * g.ldx + sgd.a;
                     if ((sgd.a & 3) == 0)
                         bwd_v4<0>(co, a, len, dr, D, xlt, xn, xp);
@@ -719,7 +806,7 @@ int cluster_tables(psw_plan* pl, const CChoice& ch, int layout,
     return PSW_OK;
 }
 
-template <typename T, int W, int NSLAB, bool LS = false, bool V4 = false>
+template <typename T, int W, int NSLAB, bool LS = false, int V4 = 0>
 int launch(const psw_plan* pl, const CChoice& ch, const void* F, int64_t ldf, void* X, int64_t ldx,
            int64_t N, cudaStream_t s, void** ev, int nev) {
     const int lay = LS ? PSW_LAYOUT_S : PSW_LAYOUT_R;
@@ -924,10 +1011,17 @@ int solve_cluster(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64
         return PSW_NOT_SUPPORTED;
     }
     const CChoice ch = choose(pl, layout);
-    if (layout == PSW_LAYOUT_S)
-        return (reinterpret_cast<uintptr_t>(X) & 31) || ((size_t(ldx) * sizeof(double)) & 31)
-                   ? launch<double, 16, 1, true, false>(pl, ch, F, ldf, X, ldx, N, s, ev, nev)
-                   : launch<double, 16, 1, true, true>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
+    if (layout == PSW_LAYOUT_S) {
+        if ((reinterpret_cast<uintptr_t>(X) & 31) || ((size_t(ldx) * sizeof(double)) & 31))
+            return launch<double, 16, 1, true, 0>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
+        // PSW_CLUSTER_ST=1: per-lane 32-byte stores instead of the whole-line stores
+        static const int st = [] {
+            const char* e = std::getenv("PSW_CLUSTER_ST");
+            return e && *e ? std::atoi(e) : 2;
+        }();
+        return st == 1 ? launch<double, 16, 1, true, 1>(pl, ch, F, ldf, X, ldx, N, s, ev, nev)
+                       : launch<double, 16, 1, true, 2>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
+    }
     return pl->dtype == PSW_F64 ? launch<double, 16, 1>(pl, ch, F, ldf, X, ldx, N, s, ev, nev)
                                 : launch<float, 32, 1>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
 }
