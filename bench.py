@@ -48,7 +48,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-PATHS = ["auto", "staged", "fused", "resweep", "cluster", "hold"]
+PATHS = ["auto", "staged", "fused", "resweep", "cluster"]
 
 
 def _args():
@@ -403,7 +403,7 @@ def run(args, cfg, overridden):
     layout = psw.LAYOUT_R if cfg.layout == "R" else psw.LAYOUT_S
     path = {"auto": psw.PATH_AUTO, "staged": psw.PATH_STAGED, "fused": psw.PATH_FUSED,
             "resweep": psw.PATH_RESWEEP,
-            "cluster": psw.PATH_CLUSTER, "hold": psw.PATH_HOLD}[args.path]
+            "cluster": psw.PATH_CLUSTER}[args.path]
     sharded = args.mode == "rows" and world > 1
     if sharded and layout != psw.LAYOUT_R:
         raise SystemExit("row sharding runs layout R")

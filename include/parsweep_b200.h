@@ -64,17 +64,14 @@ typedef enum psw_layout { PSW_LAYOUT_R = 0, PSW_LAYOUT_S = 1 } psw_layout;
  * chip and read F once (layout R, uniform partitions whose blocks fit a
  * cluster; CLUSTER: one CTA per SM holding G blocks, FUSED: 16-CTA clusters);
  * RESWEEP reads F twice from HBM and writes X once, with a few aggregates per
- * 256 rows in between (either layout, e.g. the 2^20-row config); HOLD keeps
- * one 32-RHS tile of all n rows in the shared memory of the whole grid (one
- * persistent cooperative launch, fp32, layout R, P <= 64: the 65536-row fp32
- * config) and reads F once; STAGED is
+ * 256 rows in between (either layout, e.g. the 2^20-row config); STAGED is
  * the general three-kernel path (and the only one returning betas/boundary
  * values). */
 typedef enum psw_path {
     PSW_PATH_AUTO = 0,
     PSW_PATH_STAGED = 1,
     PSW_PATH_FUSED = 2,
-    /* 3, 4, 5: retired paths (PSW_NOT_SUPPORTED) */
+    /* 3, 4, 5, 8: retired paths (PSW_NOT_SUPPORTED) */
     PSW_PATH_CHUNKED = 5,
     PSW_PATH_RESWEEP = 6,
     PSW_PATH_CLUSTER = 7,

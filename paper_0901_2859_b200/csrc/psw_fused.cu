@@ -853,7 +853,6 @@ int build_fused_tables(psw_plan* pl, const std::vector<double>& rp, const std::v
                                         : upload_fused<float>(pl, ff, fb, seg);
     if (rc != PSW_OK) return rc;
     if (int r = build_rs_tables(pl, desc, seg, ff, fb)) return r;
-    if (int r = build_hold_tables(pl, desc, seg, ff, fb)) return r;
     return pl->world == 1 ? build_cluster_tables(pl, ff, fb) : PSW_OK;
 }
 

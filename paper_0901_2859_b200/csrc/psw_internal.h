@@ -166,14 +166,6 @@ struct psw_plan {
     void* d_scoef = nullptr;               // SolveCoef<T>[n]
     psw::CarryW* d_rs_cw = nullptr;        // [group][kRsSeg] closed-form carry weights
 
-    // HOLD tables (psw_hold.cu): one CTA per SM keeps its rows of every RHS tile
-    int hd_ncta = 0, hd_nruns = 0, hd_maxrows = 0;
-    psw::RsGroup* d_hd_cta = nullptr;      // per CTA: segments, runs, rows
-    psw::RsRun* d_hd_run = nullptr;
-    psw::SegCoef* d_hd_runcoef = nullptr;
-    int32_t* d_hd_runoff = nullptr;        // [P + 1] first run of every block
-    void* d_hd_coef = nullptr;             // HoldCoef<float>[n]
-
     // multi-GPU row shard (psw_shard_*); world == 1 for a full plan
     int rank = 0, world = 1;
     int64_t blk0 = 0, blk1 = 0;   // owned blocks [blk0, blk1)
@@ -212,14 +204,6 @@ int solve_resweep(const psw_plan* plan, const void* F, int64_t ldf, void* X, int
 int build_rs_tables(psw_plan* pl, const std::vector<SegDesc>& desc,
                     const std::vector<SegCoef>& seg, const std::vector<FusedFwd<double>>& ff,
                     const std::vector<FusedBwd<double>>& fb);
-// HOLD (psw_hold.cu): one persistent grid keeps a whole RHS tile on chip (fp32)
-int build_hold_tables(psw_plan* pl, const std::vector<SegDesc>& desc,
-                      const std::vector<SegCoef>& seg, const std::vector<FusedFwd<double>>& ff,
-                      const std::vector<FusedBwd<double>>& fb);
-bool hold_supported(const psw_plan* plan, int layout, int64_t N, const void* F, int64_t ldf,
-                    const void* X, int64_t ldx);
-int solve_hold(const psw_plan* plan, const void* F, int64_t ldf, void* X, int64_t ldx, int64_t N,
-               int layout, cudaStream_t s, void** events, int nevents);
 // row shards (psw_shard.cpp): forward = K1 + fold + the rank's share of the
 // boundary values; backward = carries from the reduced values + K3
 int64_t shard_workspace_bytes(const psw_plan* pl, int64_t N);

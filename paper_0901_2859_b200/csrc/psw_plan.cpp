@@ -327,8 +327,7 @@ void free_plan(psw_plan* pl) {
                     pl->d_lvl_off, pl->d_ffwd, pl->d_fbwd, pl->d_seg, pl->d_cmat,
                     pl->d_segdesc, pl->d_segoff, pl->d_ctab[0], pl->d_ctab[1],
                     pl->d_rs_group, pl->d_rs_run, pl->d_rs_runcoef, pl->d_rs_runoff,
-                    pl->d_scoef, pl->d_rs_cw, pl->d_hd_cta, pl->d_hd_run, pl->d_hd_runcoef,
-                    pl->d_hd_runoff, pl->d_hd_coef};
+                    pl->d_scoef, pl->d_rs_cw};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     cudaSetDevice(prev);
@@ -809,19 +808,11 @@ int auto_path(const psw_plan* pl, const void* F, int64_t ldf, const void* X, int
     // CHUNKED (RESWEEP over L2-sized RHS chunks) is explicit only: on the fp32
     // config its per-chunk launches cost more than the re-read they save
     // (27 vs 10.2 ms, round 2)
-    // HOLD (one RHS tile of all rows held by the whole grid, fp32, F read once)
-    // is explicit only: 26.9 ms on C2 against RESWEEP's 9.4 ms (its in-order
-    // exchange warps bound the tile rate). PSW_HOLD_AUTO=1
-    // lets AUTO take it for systems of at least PSW_HOLD_MIN_ROWS rows.
-    static const int hold_min = [] {
-        const char* a = std::getenv("PSW_HOLD_AUTO");
-        if (!a || std::atoi(a) == 0) return -1;
-        const char* e = std::getenv("PSW_HOLD_MIN_ROWS");
-        return e ? std::atoi(e) : 16384;
-    }();
-    if (hold_min >= 0 && pl->n >= hold_min && N >= 256 &&
-        hold_supported(pl, layout, N, F, ldf, X, ldx))
-        return PSW_PATH_HOLD;
+    // HOLD (one RHS tile of all rows held by the whole grid through one
+    // persistent launch, fp32, F read once) is retired: 26.9 ms on the fp32
+    // config against RESWEEP's 9.4 ms, and bound at about 8 ms by design (three
+    // tiles fit the grid's shared memory against an exchange chain of three L2
+    // hops)
     if (resweep_supported(pl, layout, N)) return PSW_PATH_RESWEEP;
     return PSW_PATH_STAGED;
 }
@@ -981,9 +972,7 @@ int psw_solve_ex(const psw_plan* plan, const void* F, int64_t ldf, void* X, int6
                  ? psw::solve_resweep(plan, F, ldf, X, ldx, nrhs, layout, s, ev, nev)
                  : unsupported("resweep");
     } else if (path == PSW_PATH_HOLD) {
-        rc = psw::hold_supported(plan, layout, nrhs, F, ldf, X, ldx)
-                 ? psw::solve_hold(plan, F, ldf, X, ldx, nrhs, layout, s, ev, nev)
-                 : unsupported("hold");
+        rc = unsupported("hold (retired)");
     } else if (path == PSW_PATH_FUSED) {
         rc = psw::fused_supported(plan, layout, nrhs, F, ldf)
                  ? psw::solve_fused(plan, F, ldf, X, ldx, nrhs, layout, s, ev, nev)

@@ -65,11 +65,11 @@ def test_resweep_config_C1(psw, cuda):
 
 
 def test_retired_paths(psw, cuda):
-    """PIPE (3), TILE (4) and CHUNKED (5) were explicit-only paths that lost to
-    CLUSTER / RESWEEP; they are retired and answer NotSupported."""
+    """PIPE (3), TILE (4), CHUNKED (5) and HOLD (8) were explicit-only paths
+    that lost to CLUSTER / RESWEEP; they are retired and answer NotSupported."""
     g = load_golden("c1_n4096_P16")
     plan = plan_for(psw, g)
-    for path in (3, 4, psw.PATH_CHUNKED):
+    for path in (3, 4, psw.PATH_CHUNKED, psw.PATH_HOLD):
         with pytest.raises(psw.NotSupported):
             gpu_solve(psw, cuda, plan, g["F"], 0, path=path)
 
