@@ -159,6 +159,17 @@ int psw_solve_multi(const psw_plan* const* plans, int64_t nplans, const void* F,
  * (no host copies). The plans must outlive the bundle. */
 typedef struct psw_multi psw_multi;
 int psw_multi_create(psw_multi** out, const psw_plan* const* plans, int64_t nplans);
+/* The same bundle for nsys symmetric systems (sub == super) sharing one
+ * partition, set up on the device in one pass (every system's preliminary,
+ * dichotomy/preliminary.hpp:171-199, and block sweep coefficients) instead of
+ * one plan per system: FourierWorkspace's per-harmonic plan list
+ * (poisson/fourier.hpp:41-105). Host arrays sub[nsys][n-1], diag[nsys][n],
+ * super[nsys][n-1]. Tables bitwise those of psw_multi_create over per-system
+ * plans. PSW_NOT_SUPPORTED for non-symmetric input or batches beyond 32 GB of
+ * device scratch (create plans one by one then). */
+int psw_multi_create_systems(psw_multi** out, int64_t n, int64_t nsys, const double* sub,
+                             const double* diag, const double* super, int64_t p,
+                             const int64_t* boundaries, int dtype, int device);
 void psw_multi_destroy(psw_multi* multi);
 int psw_multi_solve(const psw_multi* multi, const void* F, int64_t ldf, void* X, int64_t ldx,
                     void* stream);

@@ -626,16 +626,49 @@ class MultiPlan:
 
     def __init__(self, plans: Sequence["Plan"]):
         self.plans = list(plans)
+        self.nsys, self.n = len(self.plans), self.plans[0].n
         arr = (C.c_void_p * len(self.plans))(*[pl._h for pl in self.plans])
         h = C.c_void_p()
         _check(lib().psw_multi_create(C.byref(h), arr, len(self.plans)))
         self._h = h
 
+    @classmethod
+    def from_systems(cls, sub: np.ndarray, diag: np.ndarray, sup: np.ndarray, part: Partition,
+                     dtype: int = F64, device: int = 0) -> "MultiPlan":
+        """psw_multi_create_systems: the bundle of the symmetric systems
+        (sub[k], diag[k], sup[k]), k = 0..nsys-1 (rows of 2-D arrays), sharing
+        `part`, set up on the device in one pass (no per-system plans).
+        Raises NotSupported for non-symmetric systems."""
+        part.validate()
+        sub = np.ascontiguousarray(sub, dtype=np.float64)
+        diag = np.ascontiguousarray(diag, dtype=np.float64)
+        sup = np.ascontiguousarray(sup, dtype=np.float64)
+        if diag.ndim != 2 or sub.shape != (diag.shape[0], diag.shape[1] - 1) or sup.shape != sub.shape:
+            raise ValueError("from_systems: diag (nsys, n), sub and super (nsys, n - 1)")
+        nsys, n = diag.shape
+        if part.n != n:
+            raise ValueError("from_systems: partition order does not match the systems")
+        dp = C.POINTER(C.c_double)
+        L = lib()
+        L.psw_multi_create_systems.restype = C.c_int
+        L.psw_multi_create_systems.argtypes = [C.POINTER(C.c_void_p), C.c_int64, C.c_int64, dp, dp,
+                                               dp, C.c_int64, C.POINTER(C.c_int64), C.c_int, C.c_int]
+        bnd = np.ascontiguousarray(part.boundaries, dtype=np.int64)
+        h = C.c_void_p()
+        _check(L.psw_multi_create_systems(C.byref(h), n, nsys, sub.ctypes.data_as(dp),
+                                          diag.ctypes.data_as(dp), sup.ctypes.data_as(dp), part.p(),
+                                          bnd.ctypes.data_as(C.POINTER(C.c_int64)), dtype, device))
+        self = cls.__new__(cls)
+        self.plans = []
+        self.nsys, self.n = nsys, n
+        self._h = h
+        return self
+
     def solve(self, F, X, stream=None):
         for t, nm in ((F, "F"), (X, "X")):
             if not getattr(t, "is_cuda", False) or t.dim() != 2 or t.stride(1) != 1:
                 raise ValueError(f"{nm}: a CUDA matrix with contiguous rows")
-            if t.shape[1] < len(self.plans) or t.shape[0] < self.plans[0].n:
+            if t.shape[1] < self.nsys or t.shape[0] < self.n:
                 raise ValueError(f"{nm}: too small for the bundle")
         _check(lib().psw_multi_solve(self._h, _ptr(F), F.stride(0), _ptr(X), X.stride(0),
                                      _stream_ptr(stream)))

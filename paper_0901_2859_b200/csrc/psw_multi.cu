@@ -13,6 +13,7 @@
 // single-plan STAGED solve, i.e. the reference's betas and boundary values.
 // All plans share the partition (the workspace's, fourier.hpp:47-51).
 #include <algorithm>
+#include <string>
 #include <vector>
 
 #include "psw_device.cuh"
@@ -213,10 +214,109 @@ struct psw_multi {
     int64_t n = 0, N = 0, P = 1, p = 0;
     int dtype = PSW_F64, device = 0;
     const psw_plan* p0 = nullptr;  // partition, level items (shared by every plan)
+    psw_plan* own_p0 = nullptr;    // psw_multi_create_systems: the bundle's own copy of p0
     void* fwd = nullptr;           // FwdCoef<T>[n][N]
     void* bwd = nullptr;           // BwdCoef<T>[n][N]
     void* zptr = nullptr;          // const double*[2][N]: every plan's ZR, ZL samples
+    double* zall = nullptr;        // psw_multi_create_systems: [2][N][p p + 2] samples
 };
+
+namespace psw {
+int build_plan(psw_plan** out, int64_t n, const double* sub, const double* diag, const double* sup,
+               int64_t p, const int64_t* bnd, int dtype, int device, int rank, int world,
+               std::vector<double>* cmat_host, bool shard, int strategy, int flags);
+void destroy_plan(psw_plan* pl);
+size_t device_setup_batch_bytes(int64_t n, int64_t N, int64_t p);
+int device_setup_batch(int64_t n, int64_t N, const double* sub, const double* diag,
+                       const double* sup, int64_t p, const int64_t* bnd,
+                       const std::vector<int32_t>& blk, int dtype, void* fwd, void* bwd, double* zr,
+                       double* zl, int64_t& bad_sys, int64_t& bad_row);
+}  // namespace psw
+
+// The bundle of nsys symmetric systems sharing one partition, built directly
+// on the device (psw_prelim.cu device_setup_batch: preliminary sweeps and
+// block sweep coefficients of all systems in [row][system] layout) instead of
+// one plan per system gathered afterwards: the once-per-mesh phase of the
+// Fourier consumer (fourier.hpp:41-105). sub / diag / sup are host arrays
+// [nsys][n-1] / [nsys][n] / [nsys][n-1] with sub == sup (the DirectSymmetric
+// route, preliminary.hpp:111-112; anything else answers PSW_NOT_SUPPORTED and
+// the caller creates plans one by one). The tables are bitwise those of
+// psw_multi_create over per-system plans.
+extern "C" int psw_multi_create_systems(psw_multi** out, int64_t n, int64_t nsys, const double* sub,
+                                        const double* diag, const double* sup, int64_t p,
+                                        const int64_t* boundaries, int dtype, int device) {
+    psw::clear_error();
+    if (!out || n < 2 || nsys <= 0 || !sub || !diag || !sup || p < 0 || (p > 0 && !boundaries) ||
+        (dtype != PSW_F64 && dtype != PSW_F32)) {
+        psw::set_error(PSW_INVALID_ARGUMENT, "psw_multi_create_systems: invalid arguments");
+        return PSW_INVALID_ARGUMENT;
+    }
+    *out = nullptr;
+    if (int rc = psw_partition_validate(n, p, boundaries)) return rc;
+    for (int64_t k = 0; k < nsys; ++k)
+        for (int64_t i = 0; i + 1 < n; ++i)
+            if (!(sub[k * (n - 1) + i] == sup[k * (n - 1) + i])) {
+                psw::set_error(PSW_NOT_SUPPORTED,
+                               "psw_multi_create_systems takes symmetric systems (sub == super) only");
+                return PSW_NOT_SUPPORTED;
+            }
+    const size_t scratch = psw::device_setup_batch_bytes(n, nsys, p);
+    if (scratch > (size_t(32) << 30)) {
+        psw::set_error(PSW_NOT_SUPPORTED, "psw_multi_create_systems: batch too large for one pass");
+        return PSW_NOT_SUPPORTED;
+    }
+    // system 0 as an ordinary (lean) plan: validation of the matrix layout,
+    // the partition's block table and the level-ordered combination items
+    psw_plan* p0 = nullptr;
+    if (int rc = psw::build_plan(&p0, n, sub, diag, sup, p, boundaries, dtype, device, 0, 1, nullptr,
+                                 false, PSW_GROW_DIRECT_SYMMETRIC, PSW_PLAN_STAGED_ONLY))
+        return rc;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    auto* m = new psw_multi();
+    m->n = n;
+    m->N = nsys;
+    m->P = p + 1;
+    m->p = p;
+    m->dtype = dtype;
+    m->device = device;
+    m->p0 = m->own_p0 = p0;
+    const size_t es = dtype == PSW_F64 ? 8 : 4;
+    const size_t fb = 4 * es * size_t(n) * size_t(nsys), bb = 16 * size_t(n) * size_t(nsys);
+    const size_t zs = size_t(p) * size_t(p) + 2;
+    cudaError_t e = cudaMalloc(&m->fwd, fb);
+    if (e == cudaSuccess) e = cudaMalloc(&m->bwd, bb);
+    if (e == cudaSuccess) e = cudaMalloc(&m->zptr, sizeof(void*) * 2 * size_t(nsys));
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&m->zall), 8 * 2 * zs * size_t(nsys));
+    int rc = PSW_OK;
+    int64_t bad_sys = -1, bad_row = -1;
+    if (e == cudaSuccess) {
+        std::vector<const double*> zp(2 * size_t(nsys));
+        for (int64_t k = 0; k < nsys; ++k) {
+            zp[size_t(k)] = m->zall + size_t(k) * zs;
+            zp[size_t(nsys + k)] = m->zall + (size_t(nsys) + size_t(k)) * zs;
+        }
+        e = cudaMemcpy(m->zptr, zp.data(), sizeof(void*) * zp.size(), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess)
+            rc = psw::device_setup_batch(n, nsys, sub, diag, sup, p, boundaries, p0->blk, dtype,
+                                         m->fwd, m->bwd, m->zall, m->zall + size_t(nsys) * zs,
+                                         bad_sys, bad_row);
+    }
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) rc = psw::cuda_fail(e, "psw_multi_create_systems");
+    if (rc == PSW_PIVOT_BREAKDOWN)
+        psw::set_error(PSW_PIVOT_BREAKDOWN,
+                       "pivot breakdown during forward elimination at row " +
+                           std::to_string(bad_row) + " (system " + std::to_string(bad_sys) + ")",
+                       bad_row);
+    if (rc != PSW_OK) {
+        psw_multi_destroy(m);
+        return rc;
+    }
+    *out = m;
+    return PSW_OK;
+}
 
 extern "C" int psw_multi_create(psw_multi** out, const psw_plan* const* plans, int64_t nplans) {
     psw::clear_error();
@@ -297,9 +397,10 @@ extern "C" void psw_multi_destroy(psw_multi* m) {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(m->device);
-    for (void* q : {m->fwd, m->bwd, m->zptr})
+    for (void* q : {m->fwd, m->bwd, m->zptr, static_cast<void*>(m->zall)})
         if (q) cudaFree(q);
     cudaSetDevice(prev);
+    if (m->own_p0) psw::destroy_plan(m->own_p0);
     delete m;
 }
 

@@ -188,9 +188,43 @@ __global__ void pivot_accept_kernel(PrelimArgs a) {
 }
 
 // ---- the 3p boundary sweeps -------------------------------------------------
+// Row-indexed arrays are reached through views so that the same sweeps run
+// on one system (Lin: contiguous rows) and on a batch of systems laid out
+// [row][system] (Str: thread k strides by the number of systems, a warp's 32
+// systems read one contiguous piece per row).
+template <typename T>
+struct Lin {
+    T* p;
+    __device__ __forceinline__ T& operator[](int64_t i) const { return p[i]; }
+    __device__ __forceinline__ Lin at(int64_t i) const { return Lin{p + i}; }
+};
+template <typename T>
+struct Str {
+    T* p;
+    int64_t s;
+    __device__ __forceinline__ T& operator[](int64_t i) const { return p[i * s]; }
+    __device__ __forceinline__ Str at(int64_t i) const { return Str{p + i * s, s}; }
+};
+
+template <template <typename> class V>
+struct SweepView {
+    int64_t n, p, L, win;
+    V<const double> sub, diag, sup, al, pv;  // A and its global chain
+    V<const int32_t> neg;                    // per chunk of L rows: some pivot is not > 0
+    V<double> gr, gl;                        // g_j on blocks j / j+1
+    V<double> bg, az, bz;                    // windows of all p chains (chain j at j * win)
+    const int64_t* bnd;                      // 1-based boundaries
+    const int32_t* blk;                      // [2t] = s_t, [2t+1] = e_t
+    double *zr, *zl;                         // p x p samples
+    double* zmax;                            // [2][p]
+    int64_t* fail;                           // per j: z_right breakdown (local row) or -1
+    int64_t* overflow;                       // set to 1 when a chain outgrows its window
+};
+
 // first row k >= q of a zero region whose value is known without looking
 // further: a positive pivot ((+0) + (+-0) = +0) or the region's last row
-__device__ __forceinline__ int64_t anchor(const double* pv, int64_t q, int64_t last) {
+template <typename PV>
+__device__ __forceinline__ int64_t anchor(const PV& pv, int64_t q, int64_t last) {
     int64_t k = q;
     while (k < last && !(pv[k] > 0.0)) ++k;
     return k;
@@ -220,8 +254,8 @@ __device__ __forceinline__ void back_chain(int64_t hi, int64_t lo, double& x, Be
 // Rows b-1 .. lo of a zero region (betas (+0)/pv, x_b = x a signed zero): a
 // chunk whose pivots are all positive holds +0 everywhere, which the tables
 // were initialised to, and hands +0 on; other chunks are walked row by row.
-template <typename Keep>
-__device__ __forceinline__ void zero_walk(const PrelimArgs& a, int64_t lo, int64_t b, double& x,
+template <template <typename> class V, typename Keep>
+__device__ __forceinline__ void zero_walk(const SweepView<V>& a, int64_t lo, int64_t b, double& x,
                                           Keep keep) {
     int64_t i = b - 1;
     while (i >= lo) {
@@ -236,24 +270,24 @@ __device__ __forceinline__ void zero_walk(const PrelimArgs& a, int64_t lo, int64
     }
 }
 
-__global__ void sweeps_kernel(PrelimArgs a) {
-    const int64_t j = blockIdx.x;
-    const int task = blockIdx.y;  // 0: g row, 1: z_left, 2: z_right
-    if (threadIdx.x != 0 || a.status[0] >= 0) return;
+template <template <typename> class V>
+__device__ __forceinline__ void sweep_task(const SweepView<V>& a, int64_t j, int task) {
     const int64_t n = a.n, p = a.p, r = a.bnd[j], win = a.win;
-    const double *al = a.al, *pv = a.pv, *sub = a.sub;
+    const auto &al = a.al, &pv = a.pv, &sub = a.sub;
+    auto zal = [&](int64_t i) { return al[i]; };
+    auto zbe = [&](int64_t i) { return zero_like(pv[i]); };
     if (task == 0) {
         // g_j = inv(A) e_{r-1}: betas are (+0)/pv before row r-1, 1/pv_{r-1}
         // there, then the decaying chain; rows of blocks j and j+1 are kept
         // (betas.hpp:46-55)
         const int64_t lo = a.blk[2 * j], mid = a.blk[2 * j + 1], hi = a.blk[2 * (j + 1) + 1];
-        double* bg = a.bg + size_t(j) * size_t(win);
+        const auto bg = a.bg.at(j * win);
         double be = __ddiv_rn(1.0, pv[r - 1]);
         bg[0] = be;
         int64_t fend = r - 1;
         for (int64_t i = r; i < n && be != 0.0; ++i) {
             if (i - (r - 1) >= win) {
-                a.status[2] = 1;
+                *a.overflow = 1;
                 return;
             }
             be = __ddiv_rn(__dsub_rn(0.0, __dmul_rn(sub[i - 1], be)), pv[i]);
@@ -264,14 +298,12 @@ __global__ void sweeps_kernel(PrelimArgs a) {
             if (i >= lo && i < mid) a.gr[i] = x;
             else if (i >= mid && i < hi) a.gl[i] = x;
         };
-        auto zal = [&](int64_t i) { return al[i]; };
-        auto zbe = [&](int64_t i) { return zero_like(pv[i]); };
         // x belongs to row cur; rows above fend hold signed zeros
         const int64_t s0 = max(fend, hi - 1);
         int64_t cur;
         double x;
         if (s0 == n - 1) {
-            x = fend == n - 1 ? bg[fend - (r - 1)] : zero_like(pv[n - 1]);
+            x = fend == n - 1 ? double(bg[fend - (r - 1)]) : zero_like(pv[n - 1]);
             cur = n - 1;
             keep(cur, x);
         } else {
@@ -284,7 +316,7 @@ __global__ void sweeps_kernel(PrelimArgs a) {
             zero_walk(a, fend + 1, cur, x, keep);
             cur = fend + 1;
         }
-        back_chain(cur, r - 1, x, [&](int64_t i) { return bg[i - (r - 1)]; }, zal, keep);
+        back_chain(cur, r - 1, x, [&](int64_t i) { return double(bg[i - (r - 1)]); }, zal, keep);
         cur = r - 1;
         // below the unit entry the betas are (+0)/pv again: x decays to an exact zero
         while (cur > lo && x != 0.0) {
@@ -337,8 +369,7 @@ __global__ void sweeps_kernel(PrelimArgs a) {
             const int64_t q = a.bnd[next] - 1;  // q < row
             const int64_t k = anchor(pv, q, row);
             double v = k == row ? x : zero_like(pv[k]);
-            back_chain(k, q, v, [&](int64_t i) { return zero_like(pv[i]); },
-                       [&](int64_t i) { return al[i]; }, [&](int64_t, double) {});
+            back_chain(k, q, v, zbe, zal, [&](int64_t, double) {});
             a.zl[j * p + next] = v;
             // the next sample lies below q, whose value is now known
             row = q;
@@ -350,8 +381,7 @@ __global__ void sweeps_kernel(PrelimArgs a) {
         // z_right: rows r-1..n-1 of A with a unit first row and rhs e_first;
         // local row i is global row r-1+i
         const int64_t m = n - r + 1, g0 = r - 1;
-        double* az = a.az + size_t(j) * size_t(win);
-        double* bz = a.bz + size_t(j) * size_t(win);
+        const auto az = a.az.at(j * win), bz = a.bz.at(j * win);
         double alp = m > 1 ? __ddiv_rn(-0.0, 1.0) : 0.0;
         double be = __ddiv_rn(1.0, 1.0);
         az[0] = alp;
@@ -360,7 +390,7 @@ __global__ void sweeps_kernel(PrelimArgs a) {
         int64_t fend = 0;
         for (int64_t i = 1; i < m && !(merged && be == 0.0); ++i) {
             if (i >= win) {
-                a.status[2] = 1;
+                *a.overflow = 1;
                 return;
             }
             const int64_t g = g0 + i;
@@ -389,8 +419,7 @@ __global__ void sweeps_kernel(PrelimArgs a) {
             const int64_t q = g0 + (a.bnd[nq] - r);
             const int64_t k = anchor(pv, q, n - 1);
             double v = zero_like(pv[k]);
-            back_chain(k, q, v, [&](int64_t i) { return zero_like(pv[i]); },
-                       [&](int64_t i) { return al[i]; }, [&](int64_t, double) {});
+            back_chain(k, q, v, zbe, zal, [&](int64_t, double) {});
             a.zr[j * p + nq] = v;
             --nq;
         }
@@ -408,15 +437,22 @@ __global__ void sweeps_kernel(PrelimArgs a) {
             const int64_t q = g0 + fend + 1;
             const int64_t k = anchor(pv, q, n - 1);
             double v = zero_like(pv[k]);
-            back_chain(k, q, v, [&](int64_t i) { return zero_like(pv[i]); },
-                       [&](int64_t i) { return al[i]; }, [&](int64_t, double) {});
+            back_chain(k, q, v, zbe, zal, [&](int64_t, double) {});
             x = __dadd_rn(bz[fend], __dmul_rn(az[fend], v));
         }
         visit(fend, x);
-        back_chain(fend, 0, x, [&](int64_t i) { return bz[i]; }, [&](int64_t i) { return az[i]; },
-                   visit);
+        back_chain(fend, 0, x, [&](int64_t i) { return double(bz[i]); },
+                   [&](int64_t i) { return double(az[i]); }, visit);
         a.zmax[p + j] = mz;
     }
+}
+
+__global__ void sweeps_kernel(PrelimArgs a) {
+    if (threadIdx.x != 0 || a.status[0] >= 0) return;
+    SweepView<Lin> v{a.n, a.p, a.L, a.win, {a.sub}, {a.diag}, {a.sup}, {a.al}, {a.pv}, {a.neg},
+                     {a.gr}, {a.gl}, {a.bg}, {a.az}, {a.bz}, a.bnd, a.blk, a.zr, a.zl, a.zmax,
+                     a.fail, a.status + 2};
+    sweep_task(v, blockIdx.x, blockIdx.y);
 }
 
 int64_t env_i64(const char* name, int64_t dflt) {
@@ -549,6 +585,287 @@ int device_preliminary(int64_t n, const double* sub, const double* diag, const d
     max_z = 0.0;
     for (size_t j = 0; j < 2 * pp; ++j) max_z = std::max(max_z, zmax[j]);
     return PSW_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Batched setup: N systems that share one partition (the Fourier consumer's
+// harmonics, fourier.hpp:41-105: one matrix B_l per harmonic), every table of
+// the multi-matrix bundle (psw_multi.cu) built on the device in [row][system]
+// layout, one thread per system / (system, block) / (system, boundary, sweep).
+// The arithmetic is the single-system setup's, operation for operation: the
+// global pivot chain (serial per system here: the systems are the parallel
+// axis), sweep_task for the 3p boundary sweeps, and build_plan's per-block
+// sweep coefficients (local_solve.hpp:25-50 hoisted out of the RHS loop).
+namespace {
+
+struct BatchArgs {
+    int64_t n, N, p, L, nchunk, win;
+    const double *sub, *diag, *sup;  // [row][sys]
+    double *al, *pv;                 // global chain [row][sys]
+    int32_t* neg;                    // [chunk][sys]
+    int64_t* brk;                    // [sys] first pivot breakdown of the global chain or -1
+    double *rp, *ma, *w, *alb;       // block sweep coefficients [row][sys]
+    double *gr, *gl;                 // [row][sys]
+    double *bg, *az, *bz;            // [p * win][sys]
+    const int64_t* bnd;
+    const int32_t* blk;
+    double *zr, *zl;                 // [sys][p * p + 2]
+    double* zmax;                    // [sys][2 p]
+    int64_t* fail;                   // [sys][p]
+    int64_t* overflow;
+};
+
+// in[sys][len] -> out[len][sys]
+__global__ void interleave_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                  int64_t N, int64_t len) {
+    __shared__ double tile[32][33];
+    const int64_t k0 = int64_t(blockIdx.x) * 32, i0 = int64_t(blockIdx.y) * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t k = k0 + r, i = i0 + threadIdx.x;
+        if (k < N && i < len) tile[r][threadIdx.x] = in[k * len + i];
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t i = i0 + r, k = k0 + threadIdx.x;
+        if (k < N && i < len) out[i * N + k] = tile[threadIdx.x][r];
+    }
+}
+
+__global__ void batch_chain_kernel(BatchArgs a) {
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= a.N) return;
+    const int64_t n = a.n, N = a.N;
+    double piv = a.diag[k];
+    int64_t brk = fabs(piv) < kFloor ? 0 : -1;
+    double alp = n > 1 ? __ddiv_rn(-a.sup[k], piv) : 0.0;
+    a.al[k] = alp;
+    a.pv[k] = piv;
+    bool anyneg = !(piv > 0.0);
+    for (int64_t i0 = 1; i0 < n && brk < 0; i0 += kB) {
+        double vs[kB], vd[kB], vu[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+            const int64_t i = i0 + u;
+            if (i < n) {
+                vs[u] = a.sub[(i - 1) * N + k];
+                vd[u] = a.diag[i * N + k];
+                vu[u] = i + 1 < n ? a.sup[i * N + k] : 0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+            const int64_t i = i0 + u;
+            if (i < n && brk < 0) {
+                if (i % a.L == 0) {
+                    a.neg[(i / a.L - 1) * N + k] = anyneg ? 1 : 0;
+                    anyneg = false;
+                }
+                piv = __dadd_rn(vd[u], __dmul_rn(vs[u], alp));
+                if (fabs(piv) < kFloor) brk = i;
+                alp = i + 1 < n ? __ddiv_rn(-vu[u], piv) : 0.0;
+                anyneg |= !(piv > 0.0);
+                a.al[i * N + k] = alp;
+                a.pv[i * N + k] = piv;
+            }
+        }
+    }
+    a.neg[((n - 1) / a.L) * N + k] = anyneg ? 1 : 0;
+    a.brk[k] = brk;
+}
+
+// build_plan's per-row sweep coefficients of block t (psw_plan.cpp; the
+// unit-row block systems of local_solve.hpp:25-50)
+__global__ void batch_block_kernel(BatchArgs a) {
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t t = blockIdx.y;
+    if (k >= a.N) return;
+    const int64_t n = a.n, N = a.N, p = a.p;
+    const int64_t s = a.blk[2 * t], e = a.blk[2 * t + 1];
+    const int64_t h = t == p ? n - 1 : e;  // closed block end
+    double alpha_prev, wprev;
+    if (t > 0) {  // unit first row carrying x_{t-1}
+        a.rp[s * N + k] = 0.0;
+        a.ma[s * N + k] = 0.0;
+        a.w[s * N + k] = 1.0;
+        a.alb[s * N + k] = 0.0;
+        alpha_prev = 0.0;
+        wprev = 1.0;
+    } else {
+        const double piv = a.diag[k];
+        alpha_prev = h > s ? __ddiv_rn(-a.sup[k], piv) : 0.0;
+        a.rp[s * N + k] = __ddiv_rn(1.0, piv);
+        a.ma[s * N + k] = 0.0;
+        a.w[s * N + k] = 0.0;
+        a.alb[s * N + k] = alpha_prev;
+        wprev = 0.0;
+    }
+    const int64_t last = t == p ? n : e;
+    for (int64_t q0 = s + 1; q0 < last; q0 += kB) {
+        double vs[kB], vd[kB], vu[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+            const int64_t q = q0 + u;
+            if (q < last) {
+                vs[u] = a.sub[(q - 1) * N + k];
+                vd[u] = a.diag[q * N + k];
+                vu[u] = q < h ? a.sup[q * N + k] : 0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+            const int64_t q = q0 + u;
+            if (q < last) {
+                const double piv = __dadd_rn(vd[u], __dmul_rn(vs[u], alpha_prev));
+                const double al = q < h ? __ddiv_rn(-vu[u], piv) : 0.0;
+                const double ma = __ddiv_rn(-vs[u], piv);
+                wprev = t > 0 ? __dmul_rn(ma, wprev) : 0.0;
+                a.rp[q * N + k] = __ddiv_rn(1.0, piv);
+                a.ma[q * N + k] = ma;
+                a.w[q * N + k] = wprev;
+                a.alb[q * N + k] = al;
+                alpha_prev = al;
+            }
+        }
+    }
+}
+
+__global__ void batch_sweeps_kernel(BatchArgs a) {
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= a.N || a.brk[k] >= 0) return;
+    const int64_t N = a.N, p = a.p;
+    SweepView<Str> v{a.n, p, a.L, a.win,
+                     {a.sub + k, N}, {a.diag + k, N}, {a.sup + k, N}, {a.al + k, N}, {a.pv + k, N},
+                     {a.neg + k, N}, {a.gr + k, N}, {a.gl + k, N}, {a.bg + k, N}, {a.az + k, N},
+                     {a.bz + k, N}, a.bnd, a.blk, a.zr + k * (p * p + 2), a.zl + k * (p * p + 2),
+                     a.zmax + k * 2 * p, a.fail + k * p, a.overflow};
+    sweep_task(v, blockIdx.y, blockIdx.z);
+}
+
+template <typename T>
+__global__ void batch_assemble_kernel(BatchArgs a, FwdCoef<T>* __restrict__ fo,
+                                      BwdCoef<T>* __restrict__ bo) {
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= a.N) return;
+    for (int64_t q = blockIdx.y; q < a.n; q += gridDim.y) {
+        const int64_t o = q * a.N + k;
+        fo[o] = {T(a.rp[o]), T(a.ma[o]), T(a.gr[o]), T(a.gl[o])};
+        bo[o] = {T(a.w[o]), T(a.alb[o])};
+    }
+}
+
+}  // namespace
+
+size_t device_setup_batch_bytes(int64_t n, int64_t N, int64_t p) {
+    return sizeof(double) * size_t(n) * size_t(N) * (3 + 2 + 4 + 2 + 3 * size_t(p));
+}
+
+// sub / diag / sup: host arrays [N][n-1] / [N][n] / [N][n-1]. fwd / bwd: device
+// FwdCoef<T> / BwdCoef<T> [n][N]; zr / zl: device [N][p p + 2] (zeroed here).
+// PSW_PIVOT_BREAKDOWN reports the first failing system and its row in the
+// serial executor's order.
+int device_setup_batch(int64_t n, int64_t N, const double* sub, const double* diag,
+                       const double* sup, int64_t p, const int64_t* bnd,
+                       const std::vector<int32_t>& blk, int dtype, void* fwd, void* bwd, double* zr,
+                       double* zl, int64_t& bad_sys, int64_t& bad_row) {
+    const size_t nn = size_t(n), NN = size_t(N), pp = size_t(p);
+    BatchArgs a{};
+    a.n = n;
+    a.N = N;
+    a.p = p;
+    a.L = 512;
+    a.nchunk = (n + a.L - 1) / a.L;
+    a.win = n;
+    auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
+    const size_t plane = up(8 * nn * NN);
+    const size_t bytes = (11 + 3 * pp) * plane + up(8 * (nn - 1) * NN) * 0 + up(4 * size_t(a.nchunk) * NN) +
+                         up(8 * NN) + up(8 * pp) + up(4 * blk.size()) + up(8 * 2 * pp * NN + 8) +
+                         up(8 * pp * NN + 8) + 256;
+    char* base = nullptr;
+    PSW_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&base), bytes));
+    char* d = base;
+    auto carve = [&](size_t b) {
+        char* q = d;
+        d += up(b);
+        return q;
+    };
+    auto dplane = [&]() { return reinterpret_cast<double*>(carve(8 * nn * NN)); };
+    double *tsub = dplane(), *tdiag = dplane(), *tsup = dplane();
+    a.al = dplane();
+    a.pv = dplane();
+    a.rp = dplane();
+    a.ma = dplane();
+    a.w = dplane();
+    a.alb = dplane();
+    a.gr = dplane();
+    a.gl = dplane();
+    a.bg = reinterpret_cast<double*>(carve(plane * pp));
+    a.az = reinterpret_cast<double*>(carve(plane * pp));
+    a.bz = reinterpret_cast<double*>(carve(plane * pp));
+    a.neg = reinterpret_cast<int32_t*>(carve(4 * size_t(a.nchunk) * NN));
+    a.brk = reinterpret_cast<int64_t*>(carve(8 * NN));
+    int64_t* dbnd = reinterpret_cast<int64_t*>(carve(8 * pp));
+    int32_t* dblk = reinterpret_cast<int32_t*>(carve(4 * blk.size()));
+    a.zmax = reinterpret_cast<double*>(carve(8 * 2 * pp * NN + 8));
+    a.fail = reinterpret_cast<int64_t*>(carve(8 * pp * NN + 8));
+    a.overflow = reinterpret_cast<int64_t*>(carve(8));
+    a.sub = tsub;
+    a.diag = tdiag;
+    a.sup = tsup;
+    a.bnd = dbnd;
+    a.blk = dblk;
+    a.zr = zr;
+    a.zl = zl;
+    int rc = PSW_OK;
+    auto fail = [&](cudaError_t e, const char* what) {
+        rc = cuda_fail(e, what);
+        cudaFree(base);
+        return rc;
+    };
+    cudaError_t e;
+    // the host arrays go through the (not yet used) gr / gl / rp planes
+    double* stage[3] = {a.gr, a.gl, a.rp};
+    const double* host[3] = {sub, diag, sup};
+    const size_t len[3] = {nn - 1, nn, nn - 1};
+    double* dst[3] = {tsub, tdiag, tsup};
+    for (int q = 0; q < 3; ++q) {
+        if (len[q] == 0) continue;
+        if ((e = cudaMemcpy(stage[q], host[q], 8 * len[q] * NN, cudaMemcpyHostToDevice)))
+            return fail(e, "batched setup upload");
+        const dim3 grid(unsigned((N + 31) / 32), unsigned((len[q] + 31) / 32));
+        interleave_kernel<<<grid, dim3(32, 8)>>>(stage[q], dst[q], N, int64_t(len[q]));
+    }
+    if ((e = cudaMemcpy(dbnd, bnd, 8 * pp, cudaMemcpyHostToDevice)) ||
+        (e = cudaMemcpy(dblk, blk.data(), 4 * blk.size(), cudaMemcpyHostToDevice)) ||
+        (e = cudaMemsetAsync(a.gr, 0, 8 * nn * NN)) || (e = cudaMemsetAsync(a.gl, 0, 8 * nn * NN)) ||
+        (e = cudaMemsetAsync(zr, 0, 8 * (pp * pp + 2) * NN)) ||
+        (e = cudaMemsetAsync(zl, 0, 8 * (pp * pp + 2) * NN)) ||
+        (e = cudaMemsetAsync(a.overflow, 0, 8)) || (e = cudaMemsetAsync(a.fail, 0xff, 8 * pp * NN + 8)))
+        return fail(e, "batched setup init");
+    const unsigned gx = unsigned((N + 127) / 128);
+    batch_chain_kernel<<<gx, 128>>>(a);
+    batch_block_kernel<<<dim3(gx, unsigned(p + 1)), 128>>>(a);
+    if (p > 0) batch_sweeps_kernel<<<dim3(gx, unsigned(p), 3), 128>>>(a);
+    const dim3 ga(gx, unsigned(std::min<int64_t>(n, 1024)));
+    if (dtype == PSW_F64)
+        batch_assemble_kernel<double><<<ga, 128>>>(a, static_cast<FwdCoef<double>*>(fwd),
+                                                   static_cast<BwdCoef<double>*>(bwd));
+    else
+        batch_assemble_kernel<float><<<ga, 128>>>(a, static_cast<FwdCoef<float>*>(fwd),
+                                                  static_cast<BwdCoef<float>*>(bwd));
+    if ((e = cudaGetLastError()) || (e = cudaDeviceSynchronize())) return fail(e, "batched setup");
+    std::vector<int64_t> brk(NN), fails(pp * NN + 1);
+    if ((e = cudaMemcpy(brk.data(), a.brk, 8 * NN, cudaMemcpyDeviceToHost)) ||
+        (e = cudaMemcpy(fails.data(), a.fail, 8 * pp * NN, cudaMemcpyDeviceToHost)))
+        return fail(e, "batched setup download");
+    cudaFree(base);
+    bad_sys = bad_row = -1;
+    for (size_t k = 0; k < NN && bad_row < 0; ++k) {
+        if (brk[k] >= 0) bad_row = brk[k];
+        for (size_t j = 0; j < pp && bad_row < 0; ++j)
+            if (fails[k * pp + j] >= 0) bad_row = fails[k * pp + j];
+        if (bad_row >= 0) bad_sys = int64_t(k);
+    }
+    return bad_row >= 0 ? PSW_PIVOT_BREAKDOWN : PSW_OK;
 }
 
 }  // namespace psw

@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import math
 
+import numpy as np
 import torch
 
 from . import F64, MultiPlan, Plan, TridiagMatrix
@@ -34,17 +35,25 @@ from .adi import _make_partition
 
 
 class HarmonicSystem:
-    """fourier.hpp:16-33"""
+    """fourier.hpp:16-33 (the matrix is materialised on first use: the
+    workspace sets all harmonics up from d_l alone)."""
 
-    def __init__(self, l: int, d_l: float, matrix: TridiagMatrix):
-        self.l, self.d_l, self.matrix = l, d_l, matrix
+    def __init__(self, l: int, d_l: float, order: int):
+        self.l, self.d_l, self.order = l, d_l, order
+        self._matrix = None
+
+    @property
+    def matrix(self) -> TridiagMatrix:
+        if self._matrix is None:
+            self._matrix = TridiagMatrix.constant(self.order, 1.0, -(2.0 + self.d_l), 1.0)
+        return self._matrix
 
 
 def harmonic_system(n1: int, n2: int, h1: float, h2: float, l: int) -> HarmonicSystem:
     """fourier.hpp:25-33: B_l = T - d_l I, d_l = 4 (h1/h2)^2 sin^2(pi l / (2 N2))."""
     s = math.sin(math.pi * float(l) / (2.0 * n2))
     d_l = 4.0 * (h1 * h1) / (h2 * h2) * s * s
-    return HarmonicSystem(l, d_l, TridiagMatrix.constant(n1 - 1, 1.0, -(2.0 + d_l), 1.0))
+    return HarmonicSystem(l, d_l, n1 - 1)
 
 
 def dst_raw(x: torch.Tensor, out: torch.Tensor | None = None, scale: float = 1.0,
@@ -81,10 +90,23 @@ class FourierWorkspace:
         order = n1 - 1
         self.part = _make_partition(order, dichotomy_pes)
         self.harmonics = [harmonic_system(n1, n2, h1, h2, l) for l in range(1, n2)]
-        # one plan per harmonic, only what the multi-matrix solve reads
-        self.plans = [Plan(hs.matrix, self.part, dtype=F64, device=device, staged_only=True)
-                      for hs in self.harmonics]
-        self._multi = None  # the plans' tables gathered for psw_multi_solve (first use)
+        # every harmonic's tables in one device pass (psw_multi_create_systems):
+        # B_l = tri(1, -(2 + d_l), 1) as rows of three arrays
+        d = np.array([hs.d_l for hs in self.harmonics], dtype=np.float64)
+        off = np.ones((len(self.harmonics), order - 1), dtype=np.float64)
+        diag = np.repeat(-(2.0 + d)[:, None], order, axis=1)
+        self._multi = MultiPlan.from_systems(off, diag, off, self.part, dtype=F64, device=device)
+        self._plans = None
+
+    @property
+    def plans(self):
+        """One device plan per harmonic (the reference's cached HarmonicPlan
+        list, fourier.hpp:53-60). The solver itself runs on the batched bundle;
+        the per-harmonic plans are only built when asked for."""
+        if self._plans is None:
+            self._plans = [Plan(hs.matrix, self.part, dtype=F64, device=self.device, staged_only=True)
+                           for hs in self.harmonics]
+        return self._plans
 
     def partition(self):
         return self.part
@@ -94,8 +116,6 @@ class FourierWorkspace:
         row i-1 = direction-1 node i) is the right-hand side of B_l."""
         if out is None:
             out = torch.empty_like(coeff)
-        if self._multi is None:
-            self._multi = MultiPlan(self.plans)
         self._multi.solve(coeff, out, stream=stream)
         return out
 

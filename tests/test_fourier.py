@@ -178,3 +178,64 @@ def test_staged_only_plan(psw, cuda):
     for path in (psw.PATH_CLUSTER, psw.PATH_RESWEEP, psw.PATH_FUSED):
         with pytest.raises(psw.NotSupported):
             gpu_solve(psw, cuda, lean, g["F"], 0, path=path)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["dominant", "mixed_sign", "harmonics", "fp32", "p0", "size2"])
+def test_bundle_from_systems_is_bitwise_the_per_plan_bundle(psw, cuda, kind):
+    """psw_multi_create_systems (every system's preliminary and block sweep
+    coefficients in one device pass, [row][system] tables) against
+    psw_multi_create over plans created one by one on the host: the same
+    solution bit for bit on every column."""
+    rng = np.random.default_rng({"dominant": 1, "mixed_sign": 2, "harmonics": 3, "fp32": 4,
+                                 "p0": 5, "size2": 6}[kind])
+    n, K = (700, 45) if kind != "harmonics" else (1500, 40)
+    dt = psw.F32 if kind == "fp32" else psw.F64
+    if kind == "p0":
+        part = psw.Partition(n, [])
+    elif kind == "size2":
+        part = psw.Partition(n, [2, 4, 300, 302, 696, 698])
+    else:
+        part = psw.Partition(n, sorted(rng.choice(np.arange(2, n), 7, replace=False).tolist()))
+    sub = np.empty((K, n - 1))
+    diag = np.empty((K, n))
+    for k in range(K):
+        if kind == "harmonics":  # near-singular to strongly dominant Toeplitz systems
+            sub[k] = 1.0
+            diag[k] = -(2.0 + 10.0 ** rng.uniform(-7, 1))
+        else:
+            a = rng.uniform(0.5, 1.0, n - 1) * rng.choice([-1.0, 1.0], n - 1)
+            b = np.abs(np.r_[0, a]) + np.abs(np.r_[a, 0]) + rng.uniform(0.1, 1, n)
+            if kind == "mixed_sign":
+                b *= rng.choice([-1.0, 1.0], n)
+            sub[k], diag[k] = a, b
+    plans = [psw.Plan(psw.TridiagMatrix.symmetric(sub[k], diag[k]), part, dtype=dt, staged_only=True)
+             for k in range(K)]
+    tdt = cuda.float32 if kind == "fp32" else cuda.float64
+    F = cuda.from_numpy(rng.uniform(-1, 1, (n, K + 5))).cuda().to(tdt)
+    want = psw.MultiPlan(plans).solve(F, cuda.zeros_like(F))
+    got = psw.MultiPlan.from_systems(sub, diag, sub, part, dtype=dt).solve(F, cuda.zeros_like(F))
+    cuda.cuda.synchronize()
+    assert bool((want[:, :K] == got[:, :K]).all())
+    assert bool(cuda.isfinite(got[:, :K]).all())
+
+
+@pytest.mark.gpu
+def test_bundle_from_systems_errors(psw, cuda):
+    n, K = 40, 5
+    part = psw.Partition(n, [10, 20, 30])
+    sub = -np.ones((K, n - 1))
+    diag = np.full((K, n), 2.5)
+    sup = sub.copy()
+    sup[3, 7] = -0.5
+    with pytest.raises(psw.NotSupported):  # not symmetric: plans one by one
+        psw.MultiPlan.from_systems(sub, diag, sup, part)
+    diag[2] = 2.0  # the Neumann matrix of test_device_setup_pivot_breakdown: pivot 0 at row n-1
+    diag[2, 0] = diag[2, -1] = 1.0
+    with pytest.raises(psw.PivotBreakdown) as e:
+        psw.MultiPlan.from_systems(sub, diag, sub, part)
+    with pytest.raises(psw.PivotBreakdown) as e1:
+        psw.Plan(psw.TridiagMatrix.symmetric(sub[2], diag[2]), part)
+    assert e.value.row == e1.value.row == n - 1
+    with pytest.raises(ValueError):
+        psw.MultiPlan.from_systems(sub, diag[:, :-1], sub, part)
