@@ -566,39 +566,8 @@ struct Choice {
     size_t smem = 0;
 };
 
-// Row width of an RHS tile: 128 B (default) or 256 B (PSW_FUSED_ROW_BYTES).
-int tile_row_bytes() {
-    static int rb = [] {
-        const char* e = std::getenv("PSW_FUSED_ROW_BYTES");
-        const int v = e ? std::atoi(e) : 128;
-        return v == 256 ? 256 : 128;
-    }();
-    return rb;
-}
-
-// LAG schedule (FusedTile::step_lag) with PSW_FUSED_LAG=1. Measured on C1
-// (tools/trace_fused.py): it removes the exchange wait (4956 -> 978 cycles
-// per tile) but its second slab cuts co-resident clusters from 22 to 15, a
-// net loss (124.6 vs 92.5 us), so the default is the single-slab schedule.
-bool fused_lag() {
-    static bool lag = [] {
-        const char* e = std::getenv("PSW_FUSED_LAG");
-        return e && std::atoi(e) == 1;
-    }();
-    return lag;
-}
-
-// Sweep coefficients read from global memory / L1 (PSW_FUSED_GCOEF=1)
-// instead of the per-CTA shared-memory copy. Measured on C1: the freed shared
-// memory does not buy more resident clusters and the sweeps then wait on L1
-// misses (184 vs 92.5 us), so the copy is the default.
-bool fused_gcoef() {
-    static bool gc = [] {
-        const char* e = std::getenv("PSW_FUSED_GCOEF");
-        return e && std::atoi(e) == 1;
-    }();
-    return gc;
-}
+// Row width of an RHS tile: 128 B.
+int tile_row_bytes() { return 128; }
 
 // Smallest G (blocks per CTA) whose cluster C = P/G fits (<= 16 CTAs), then
 // grow G while the CTA stays under the occupancy target.
@@ -619,7 +588,7 @@ Choice choose_w(const psw_plan* pl, int es, int row_bytes) {
         const int rows_alloc = G * m + 1;
         const int nchunks = (rows_alloc + kChunk - 1) / kChunk;
         const size_t smem =
-            FusedLayout(rows_alloc, nchunks, G, S, P, W, es, fused_lag(), fused_gcoef()).total;
+            FusedLayout(rows_alloc, nchunks, G, S, P, W, es, false, false).total;
         if (smem > kSmemMax || G * S * W > kMaxThreads) break;
         if ((G * S * W) % 32) continue;  // consumer warps must be full
         if (ch.G == 0 || smem <= kSmemTarget) {
@@ -752,22 +721,12 @@ template <typename T>
 int launch_fused(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_t ldx, int64_t N,
                  cudaStream_t s, void** ev, int nev) {
     const Choice ch = choose(pl, int(sizeof(T)));
-    const bool w256 = ch.W * int(sizeof(T)) == 256;
-    const int mode = (fused_lag() ? 1 : 0) + (fused_gcoef() ? 2 : 0);
-    switch (mode) {
-        case 0:
-            return w256 ? launch_w<T, 256 / sizeof(T), false, false>(pl, ch, F, ldf, X, ldx, N, s, ev, nev)
-                        : launch_w<T, 128 / sizeof(T), false, false>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
-        case 1:
-            return w256 ? launch_w<T, 256 / sizeof(T), true, false>(pl, ch, F, ldf, X, ldx, N, s, ev, nev)
-                        : launch_w<T, 128 / sizeof(T), true, false>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
-        case 2:
-            return w256 ? launch_w<T, 256 / sizeof(T), false, true>(pl, ch, F, ldf, X, ldx, N, s, ev, nev)
-                        : launch_w<T, 128 / sizeof(T), false, true>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
-        default:
-            return w256 ? launch_w<T, 256 / sizeof(T), true, true>(pl, ch, F, ldf, X, ldx, N, s, ev, nev)
-                        : launch_w<T, 128 / sizeof(T), true, true>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
-    }
+    // one variant is built: 128-byte RHS rows, single-slab schedule, coefficients
+    // in shared memory. The LAG schedule, global-memory coefficients and 256-byte
+    // rows (template parameters LAG, GC, W) were measured slower on C1 (124.6,
+    // 184 and 97 us against 92.5 us before the segment fix) and are no longer
+    // instantiated.
+    return launch_w<T, 128 / sizeof(T), false, false>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
 }
 
 template <typename T>
