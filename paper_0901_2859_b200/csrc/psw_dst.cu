@@ -28,6 +28,15 @@ constexpr double kPi = 3.141592653589793238462643383279502884;  // std::numbers:
 constexpr int kDstThreads = 512;
 constexpr int kDstMaxL = 8192;
 
+// Twiddle w_i lives at tw[twi(i)]: the stages read the table with power-of-two
+// strides (index k * step, step up to L / 4), which in the plain layout puts
+// a warp's 32 loads in one bank (16-byte entries, 8 per bank row). XOR-ing
+// the low three index bits with the next three groups of three spreads every
+// such stride over all eight 16-byte banks.
+__device__ __forceinline__ int twi(int i) {
+    return i ^ ((i >> 3) & 7) ^ ((i >> 6) & 7) ^ ((i >> 9) & 7);
+}
+
 __global__ void __launch_bounds__(kDstThreads) dst_pair_kernel(
     const double* __restrict__ in, int64_t ldin, double* __restrict__ out, int64_t ldout,
     int64_t rows, int N, int logL, const double2* __restrict__ gtw, double scale) {
@@ -39,7 +48,7 @@ __global__ void __launch_bounds__(kDstThreads) dst_pair_kernel(
     const bool hasb = rb < rows;
     const double* a = in + ra * ldin;
     const double* b = in + (hasb ? rb : ra) * ldin;
-    for (int k = threadIdx.x; k < L / 2; k += blockDim.x) tw[k] = gtw[k];
+    for (int k = threadIdx.x; k < L / 2; k += blockDim.x) tw[twi(k)] = gtw[k];
     // the odd extension, stored bit-reversed (Radix2Fft::transform's swap pass)
     for (int i = threadIdx.x; i < L; i += blockDim.x) {
         double re = 0.0, im = 0.0;
@@ -64,7 +73,7 @@ __global__ void __launch_bounds__(kDstThreads) dst_pair_kernel(
         const int half = len >> 1, step = L / len;
         for (int bf = threadIdx.x; bf < L / 2; bf += blockDim.x) {
             const int k = bf & (half - 1), i0 = (bf - k) * 2 + k;
-            const double2 w = tw[k * step];
+            const double2 w = tw[twi(k * step)];
             const double2 x = v[i0], y = v[i0 + half];
             const double tr = w.x * y.x - w.y * y.y, ti = w.x * y.y + w.y * y.x;  // w * b
             v[i0 + half] = make_double2(x.x - tr, x.y - ti);
@@ -86,7 +95,7 @@ __global__ void __launch_bounds__(kDstThreads) dst_pair_kernel(
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     if (j & h) continue;
-                    const double2 w = tw[(k + (j & (h - 1)) * q) * step];
+                    const double2 w = tw[twi((k + (j & (h - 1)) * q) * step)];
                     const double2 y = e[j + h];
                     const double tr = w.x * y.x - w.y * y.y, ti = w.x * y.y + w.y * y.x;
                     e[j + h] = make_double2(e[j].x - tr, e[j].y - ti);

@@ -566,7 +566,7 @@ struct Choice {
     size_t smem = 0;
 };
 
-// Row width of an RHS tile: 128 B.
+// Row width of an RHS tile: 128 B (choose() falls back to 256 B for tiny systems).
 int tile_row_bytes() { return 128; }
 
 // Smallest G (blocks per CTA) whose cluster C = P/G fits (<= 16 CTAs), then
@@ -721,12 +721,14 @@ template <typename T>
 int launch_fused(const psw_plan* pl, const void* F, int64_t ldf, void* X, int64_t ldx, int64_t N,
                  cudaStream_t s, void** ev, int nev) {
     const Choice ch = choose(pl, int(sizeof(T)));
-    // one variant is built: 128-byte RHS rows, single-slab schedule, coefficients
-    // in shared memory. The LAG schedule, global-memory coefficients and 256-byte
-    // rows (template parameters LAG, GC, W) were measured slower on C1 (124.6,
-    // 184 and 97 us against 92.5 us before the segment fix) and are no longer
-    // instantiated.
-    return launch_w<T, 128 / sizeof(T), false, false>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
+    // the single-slab schedule with the coefficients in shared memory, 128-byte RHS
+    // rows, or 256-byte rows where 128 bytes cannot fill a warp (choose(): tiny
+    // systems of one segment per block). The LAG schedule and global-memory
+    // coefficients (template parameters LAG, GC) were measured slower on C1 (124.6
+    // and 184 us against 92.5 us before the segment fix) and are no longer built.
+    return ch.W * int(sizeof(T)) == 256
+               ? launch_w<T, 256 / sizeof(T), false, false>(pl, ch, F, ldf, X, ldx, N, s, ev, nev)
+               : launch_w<T, 128 / sizeof(T), false, false>(pl, ch, F, ldf, X, ldx, N, s, ev, nev);
 }
 
 template <typename T>
