@@ -36,6 +36,12 @@ constexpr int kDstMaxL = 8192;
 __device__ __forceinline__ int twi(int i) {
     return i ^ ((i >> 3) & 7) ^ ((i >> 6) & 7) ^ ((i >> 9) & 7);
 }
+// The signal gets the same treatment (element x at v[vsw(x)]): the bit-reversed
+// scatter of the odd extension writes with strides of L / 32 entries, and the
+// first passes (q < 32) read 8-element blocks 512 bytes apart.
+__device__ __forceinline__ int vsw(int i) {
+    return i ^ ((i >> 3) & 7) ^ ((i >> 6) & 7) ^ ((i >> 9) & 7) ^ ((i >> 12) & 7);
+}
 
 __global__ void __launch_bounds__(kDstThreads) dst_pair_kernel(
     const double* __restrict__ in, int64_t ldin, double* __restrict__ out, int64_t ldout,
@@ -59,7 +65,7 @@ __global__ void __launch_bounds__(kDstThreads) dst_pair_kernel(
             re = -a[L - i - 1];
             im = hasb ? -b[L - i - 1] : 0.0;
         }
-        v[__brev(unsigned(i)) >> (32 - logL)] = make_double2(re, im);
+        v[vsw(int(__brev(unsigned(i)) >> (32 - logL)))] = make_double2(re, im);
     }
     __syncthreads();
     // Radix2Fft::transform's stages len = 2, 4, ..., L, three at a time: the
@@ -74,10 +80,10 @@ __global__ void __launch_bounds__(kDstThreads) dst_pair_kernel(
         for (int bf = threadIdx.x; bf < L / 2; bf += blockDim.x) {
             const int k = bf & (half - 1), i0 = (bf - k) * 2 + k;
             const double2 w = tw[twi(k * step)];
-            const double2 x = v[i0], y = v[i0 + half];
+            const double2 x = v[vsw(i0)], y = v[vsw(i0 + half)];
             const double tr = w.x * y.x - w.y * y.y, ti = w.x * y.y + w.y * y.x;  // w * b
-            v[i0 + half] = make_double2(x.x - tr, x.y - ti);
-            v[i0] = make_double2(x.x + tr, x.y + ti);
+            v[vsw(i0 + half)] = make_double2(x.x - tr, x.y - ti);
+            v[vsw(i0)] = make_double2(x.x + tr, x.y + ti);
         }
         __syncthreads();
     }
@@ -87,7 +93,7 @@ __global__ void __launch_bounds__(kDstThreads) dst_pair_kernel(
             const int k = bf & (q - 1), i0 = (bf - k) * 8 + k;
             double2 e[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) e[j] = v[i0 + j * q];
+            for (int j = 0; j < 8; ++j) e[j] = v[vsw(i0 + j * q)];
 #pragma unroll
             for (int t = 0; t < 3; ++t) {
                 const int h = 1 << t;                  // in units of q
@@ -103,7 +109,7 @@ __global__ void __launch_bounds__(kDstThreads) dst_pair_kernel(
                 }
             }
 #pragma unroll
-            for (int j = 0; j < 8; ++j) v[i0 + j * q] = e[j];
+            for (int j = 0; j < 8; ++j) v[vsw(i0 + j * q)] = e[j];
         }
         __syncthreads();
     }
@@ -111,8 +117,8 @@ __global__ void __launch_bounds__(kDstThreads) dst_pair_kernel(
     double* oa = out + ra * ldout;
     double* ob = out + rb * ldout;
     for (int l = 1 + threadIdx.x; l < N; l += blockDim.x) {
-        const double2 x = v[l];
-        const double2 y = make_double2(v[L - l].x, -v[L - l].y);  // conj(v[2N - l])
+        const double2 x = v[vsw(l)], z = v[vsw(L - l)];
+        const double2 y = make_double2(z.x, -z.y);  // conj(v[2N - l])
         oa[l - 1] = scale * (-0.25 * (x.y + y.y));
         if (hasb) ob[l - 1] = scale * (0.25 * (x.x - y.x));
     }
