@@ -465,9 +465,9 @@ int64_t env_i64(const char* name, int64_t dflt) {
 // Device preliminary of a DirectSymmetric plan: fills gr, gl (n), zr, zl
 // (p x p), max_z. Returns PSW_OK, PSW_PIVOT_BREAKDOWN with *bad_row (the
 // serial executor's first failure: boundary, then g, z_left, z_right), a CUDA
-// error, or PSW_NOT_SUPPORTED when a chain outgrew its scratch window (the caller
-// then runs the host setup). *serial = 1 if the global chain took the
-// one-thread path.
+// error, or PSW_NOT_SUPPORTED when a chain outgrew its scratch window or the
+// scratch could not be allocated (the caller then runs the host setup).
+// *serial = 1 if the global chain took the one-thread path.
 int device_preliminary(int64_t n, const double* sub, const double* diag, const double* sup,
                        int64_t p, const int64_t* bnd, const std::vector<int32_t>& blk,
                        std::vector<double>& gr, std::vector<double>& gl, std::vector<double>& zr,
@@ -486,7 +486,10 @@ int device_preliminary(int64_t n, const double* sub, const double* diag, const d
                          up(8 * 4) + 2 * up(8 * pp * pp) + up(8 * 2 * pp) + up(8 * pp) +
                          3 * up(8 * pp * win);
     char* base = nullptr;
-    PSW_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&base), bytes));
+    if (cudaMalloc(reinterpret_cast<void**>(&base), bytes) != cudaSuccess) {
+        cudaGetLastError();  // no room for the device sweeps' scratch: the host runs them
+        return PSW_NOT_SUPPORTED;
+    }
     char* d = base;
     auto carve = [&](size_t b) {
         char* q = d;
