@@ -13,6 +13,7 @@
 // signal and the twiddles live in shared memory (L <= 8192: N <= 4096).
 // Other N (dst.hpp:120-128): the direct sine sum over the reference's
 // sines[m] table, one thread per output.
+#include <algorithm>
 #include <cmath>
 #include <mutex>
 
@@ -25,7 +26,7 @@ namespace psw {
 namespace {
 
 constexpr double kPi = 3.141592653589793238462643383279502884;  // std::numbers::pi
-constexpr int kDstThreads = 512;
+constexpr int kDstThreads = 1024;
 constexpr int kDstMaxL = 8192;
 
 // Twiddle w_i lives at tw[twi(i)]: the stages read the table with power-of-two
@@ -213,7 +214,9 @@ extern "C" int psw_dst_rows(const double* in, int64_t ldin, double* out, int64_t
                                      int(sizeof(double2) * (psw::kDstMaxL + psw::kDstMaxL / 2)));
         });
         PSW_CUDA_TRY(e);
-        psw::dst_pair_kernel<<<unsigned((rows + 1) / 2), psw::kDstThreads, smem, s>>>(
+        // one thread per 8-element block of a pass (L / 8), 64 .. kDstThreads
+        const int threads = std::min(psw::kDstThreads, std::max(64, (L / 8 + 31) / 32 * 32));
+        psw::dst_pair_kernel<<<unsigned((rows + 1) / 2), threads, smem, s>>>(
             in, ldin, out, ldout, rows, n, logL, static_cast<const double2*>(tab), scale);
     } else {
         const dim3 grid(unsigned((n - 1 + 127) / 128), unsigned(rows < 65535 ? rows : 65535));
