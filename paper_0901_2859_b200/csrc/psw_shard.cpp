@@ -15,6 +15,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -42,9 +43,13 @@ const NcclApi& nccl() {
     static NcclApi api;
     static std::once_flag once;
     std::call_once(once, [] {
-        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        // PSW_NCCL_LIB: another NCCL build, or the tests' host-staged stand-in
+        // (tests/cpp/fake_nccl.cpp) that lets several ranks share one GPU
+        const char* lib = std::getenv("PSW_NCCL_LIB");
+        if (!lib || !*lib) lib = "libnccl.so.2";
+        void* h = dlopen(lib, RTLD_NOW | RTLD_GLOBAL);
         if (!h) {
-            api.why = std::string("libnccl.so.2 not loadable: ") + dlerror();
+            api.why = std::string(lib) + " not loadable: " + dlerror();
             return;
         }
         auto sym = [&](const char* name) { return dlsym(h, name); };
@@ -55,7 +60,7 @@ const NcclApi& nccl() {
         api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
         api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce &&
                  api.GetErrorString;
-        if (!api.ok) api.why = "libnccl.so.2 lacks the expected symbols";
+        if (!api.ok) api.why = std::string(lib) + " lacks the expected symbols";
     });
     return api;
 }

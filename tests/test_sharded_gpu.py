@@ -178,3 +178,39 @@ def test_rhs_slices_equal_full_batch(psw, cuda, world):
         Xs = plan.solve(Fs, cuda.empty_like(Fs), path=psw.PATH_RESWEEP)
         cuda.cuda.synchronize()
         assert bool((Xs == full[:, k0:k1]).all())
+
+
+@pytest.mark.parametrize("name,world", [("c1_n4096_P16", 2), ("decomp_n333_P9", 3), ("c0_n1024_P4", 4)])
+def test_shard_solve_multi_process_through_the_c_abi(psw, cuda, name, world, tmp_path):
+    """psw_shard_solve with world_size > 1: one PROCESS per rank, all on cuda:0,
+    each with its own shard plan and a communicator of `world` ranks; the
+    all-reduce between the two halves of the solve is the host-staged
+    stand-in of tests/cpp/fake_nccl.cpp (PSW_NCCL_LIB), which sums the ranks'
+    partial boundary values in rank order. What runs is the C-ABI path of the
+    multi-GPU bench — rank > 0 plans, communicator checks, forward, in-place
+    sum, backward — and the assembled solution matches the reference."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    fake = os.path.join(root, "paper_0901_2859_b200", "_lib", "libfake_nccl.so")
+    if not os.path.exists(fake):
+        pytest.skip("libfake_nccl.so not built")
+    env = dict(os.environ, PSW_NCCL_LIB=fake)
+    uid = str(tmp_path / "uid")
+    outs = [str(tmp_path / f"x{r}.npy") for r in range(world)]
+    procs = [subprocess.Popen([sys.executable, os.path.join(root, "tests", "_shard_worker.py"), name,
+                               str(world), str(r), uid, outs[r]], env=env, stdout=subprocess.PIPE,
+                              stderr=subprocess.STDOUT) for r in range(world)]
+    logs = []
+    for p in procs:
+        out, _ = p.communicate(timeout=300)
+        logs.append(out.decode()[-2000:])
+    assert all(p.returncode == 0 for p in procs), logs
+    g = load_golden(name)
+    X = np.concatenate([np.load(o) for o in outs], axis=0)
+    assert rel_l2(X.T, g["X"]) <= 1e-12
+    # and bitwise the in-process emulation, whose sum also runs in rank order
+    A = psw.TridiagMatrix(g["sub"], g["diag"], g["super"])
+    part = psw.Partition(A.n(), g["bnd"].tolist())
+    assert np.array_equal(X, _emulate(psw, cuda, A, part, np.ascontiguousarray(g["F"].T), world))
