@@ -41,6 +41,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "psw_internal.h"
@@ -784,7 +785,12 @@ int device_setup_batch(int64_t n, int64_t N, const double* sub, const double* di
                          up(8 * NN) + up(8 * pp) + up(4 * blk.size()) + up(8 * 2 * pp * NN + 8) +
                          up(8 * pp * NN + 8) + 256;
     char* base = nullptr;
-    PSW_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&base), bytes));
+    if (cudaMalloc(reinterpret_cast<void**>(&base), bytes) != cudaSuccess) {
+        cudaGetLastError();
+        set_error(PSW_NOT_SUPPORTED, "batched setup: no room for " + std::to_string(bytes >> 20) +
+                                         " MB of device scratch (create the plans one by one)");
+        return PSW_NOT_SUPPORTED;
+    }
     char* d = base;
     auto carve = [&](size_t b) {
         char* q = d;

@@ -30,7 +30,7 @@ import math
 import numpy as np
 import torch
 
-from . import F64, MultiPlan, Plan, TridiagMatrix
+from . import F64, MultiPlan, NotSupported, Plan, TridiagMatrix
 from .adi import _make_partition
 
 
@@ -95,8 +95,11 @@ class FourierWorkspace:
         d = np.array([hs.d_l for hs in self.harmonics], dtype=np.float64)
         off = np.ones((len(self.harmonics), order - 1), dtype=np.float64)
         diag = np.repeat(-(2.0 + d)[:, None], order, axis=1)
-        self._multi = MultiPlan.from_systems(off, diag, off, self.part, dtype=F64, device=device)
         self._plans = None
+        try:
+            self._multi = MultiPlan.from_systems(off, diag, off, self.part, dtype=F64, device=device)
+        except NotSupported:  # no room for the batched setup's scratch: one plan per harmonic
+            self._multi = MultiPlan(self.plans)
 
     @property
     def plans(self):
